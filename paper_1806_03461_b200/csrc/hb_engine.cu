@@ -1,0 +1,1028 @@
+// B200 (sm_100a) gate-bootstrapping engine: the device half of the
+// GateBackend drop-in (reference: /root/reference/pkg/src/hebnn/backend.py
+// 205-237, where SimContext only simulates each gate in plaintext).
+//
+// Kernels:
+//   k_bk_to_fourier   K6  BK (u32 coefficients) -> FP64 negacyclic Fourier domain
+//   k_blind_rotate    K1+K2+K3 fused: gate linear combination + mod switch,
+//                     630 CMux external products (gadget decomposition, FP64
+//                     FFT in registers/shared memory, BK rows streamed by
+//                     cp.async.bulk into a shared-memory ring and reused by
+//                     every gate of the CTA), sample extraction
+//   k_keyswitch       K4  batched LWE key switch (uint32), KSK rows shared by a
+//                     tile of gates
+//   k_gather          pool slots -> contiguous buffer for download
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hb_internal.h"
+
+using namespace hb;
+
+#define HB_CUDA_TRY(expr)                                                                   \
+    do {                                                                                    \
+        cudaError_t _err = (expr);                                                          \
+        if (_err != cudaSuccess) {                                                          \
+            set_error(std::string(#expr) + ": " + cudaGetErrorString(_err));               \
+            return HB_ECUDA;                                                                \
+        }                                                                                   \
+    } while (0)
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// FP64 negacyclic FFT: 512-point complex transform of the folded polynomial
+// z_j = (a_j + i a_{j+512}) psi^j, psi = e^{i pi / 1024}; Z_k = A(psi^{4k+1}).
+// 64 threads per polynomial, 8 points per thread, three radix-8 passes with two
+// shared-memory exchanges.  Thread t holds points t + 64 m (m = 0..7) on input
+// and bins t + 64 m on output (natural order on both sides).
+// ---------------------------------------------------------------------------
+
+constexpr int kXchStride = 520;  // double2 per exchange buffer (65-padded layout)
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+// acc += a * b
+__device__ __forceinline__ void cmac(double2 &acc, double2 a, double2 b) {
+    acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+    acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+}
+
+// In-place DFT-8 with kernel e^{+2 pi i / 8}; output in bit-reversed order.
+__device__ __forceinline__ void dft8(double2 (&x)[8]) {
+    const double r = 0.70710678118654752440;
+#pragma unroll
+    for (int m = 0; m < 4; m++) {
+        double2 a = x[m], b = x[m + 4];
+        x[m] = cadd(a, b);
+        double2 d = csub(a, b);
+        if (m == 0) x[m + 4] = d;
+        else if (m == 1) x[m + 4] = make_double2((d.x - d.y) * r, (d.x + d.y) * r);
+        else if (m == 2) x[m + 4] = make_double2(-d.y, d.x);
+        else x[m + 4] = make_double2((-d.x - d.y) * r, (d.x - d.y) * r);
+    }
+#pragma unroll
+    for (int h = 0; h < 8; h += 4) {
+#pragma unroll
+        for (int m = 0; m < 2; m++) {
+            double2 a = x[h + m], b = x[h + m + 2];
+            x[h + m] = cadd(a, b);
+            double2 d = csub(a, b);
+            x[h + m + 2] = (m == 0) ? d : make_double2(-d.y, d.x);
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < 8; h += 2) {
+        double2 a = x[h], b = x[h + 1];
+        x[h] = cadd(a, b);
+        x[h + 1] = csub(a, b);
+    }
+}
+
+__device__ __forceinline__ constexpr int rev3(int k) { return ((k & 1) << 2) | (k & 2) | ((k >> 2) & 1); }
+
+__device__ __forceinline__ void group_bar(int id) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(64) : "memory");
+}
+
+// Forward 512-point FFT (kernel e^{+2 pi i jk/512}) of x held as described
+// above.  W[e] = e^{2 pi i e / 512}.  S0/S1: two exchange buffers (double
+// buffered so each exchange costs one barrier).
+__device__ __forceinline__ void fft512(double2 (&x)[8], double2 *S0, double2 *S1, int t,
+                                       const double2 *__restrict__ W, int bar_id) {
+    // pass A: DFT over m (stride-64 points); thread t = j0 + 8 j1
+    dft8(x);
+    {
+        const int j0 = t & 7, j1 = t >> 3;
+#pragma unroll
+        for (int k2 = 0; k2 < 8; k2++) {
+            double2 y = x[rev3(k2)];
+            if (k2) y = cmul(y, __ldg(&W[(t * k2) & 511]));
+            S0[j0 * 65 + k2 * 8 + j1] = y;
+        }
+    }
+    group_bar(bar_id);
+    // pass B: thread u = j0 + 8 k2 gathers j1 = 0..7
+    {
+        const int j0 = t & 7, k2 = t >> 3;
+#pragma unroll
+        for (int j1 = 0; j1 < 8; j1++) x[j1] = S0[j0 * 65 + k2 * 8 + j1];
+        dft8(x);
+#pragma unroll
+        for (int k1 = 0; k1 < 8; k1++) {
+            double2 y = x[rev3(k1)];
+            if (k1) y = cmul(y, __ldg(&W[(8 * j0 * k1) & 511]));
+            S1[k2 * 65 + k1 * 8 + j0] = y;
+        }
+    }
+    group_bar(bar_id);
+    // pass C: thread v = k2 + 8 k1 gathers j0 = 0..7; output bin v + 64 k0
+    {
+        const int k2 = t & 7, k1 = t >> 3;
+        double2 y[8];
+#pragma unroll
+        for (int j0 = 0; j0 < 8; j0++) y[j0] = S1[k2 * 65 + k1 * 8 + j0];
+        dft8(y);
+#pragma unroll
+        for (int k0 = 0; k0 < 8; k0++) x[k0] = y[rev3(k0)];
+    }
+}
+
+// double from a small signed integer without I2F: (2^52 + 2^51 + 2^31 + d) - (2^52 + 2^51 + 2^31)
+__device__ __forceinline__ double small_int_to_double(int32_t d) {
+    return __hiloint2double(0x43380000, (int)((uint32_t)d ^ 0x80000000u)) - 6755401588539392.0;
+}
+// round(v) mod 2^32 for |v| < 2^51 via the 1.5 * 2^52 magic constant
+__device__ __forceinline__ uint32_t round_to_torus(double v) {
+    return (uint32_t)__double2loint(v + 6755399441055744.0);
+}
+
+// gadget digit p (0..2) of the CGGI decomposition, in [-64, 64)
+__device__ __forceinline__ int32_t gadget_digit(uint32_t x, int p) {
+    constexpr uint32_t kOffset = (64u << 25) + (64u << 18) + (64u << 11);
+    const uint32_t buf = x + kOffset;
+    return (int32_t)((buf >> (25 - 7 * p)) & 127u) - 64;
+}
+
+// X^a rotation lookup: coefficient i of X^a * P (a in [0, 2N))
+__device__ __forceinline__ uint32_t rot_coef(const uint32_t *P, int i, int a) {
+    const int idx = (i - a) & (2 * kN - 1);
+    const uint32_t v = P[idx & (kN - 1)];
+    return (idx & kN) ? 0u - v : v;
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier / bulk-copy helpers (sm_90+ PTX; SASS: SYNCS.*, UBLKCP)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// K6: BK to Fourier.  One 64-thread group per polynomial; output scaled by
+// 1/512 (the inverse-FFT normalisation, exact power of two) in natural bin
+// order: bkf[poly][k], poly = ((i * 6 + row) * 2 + q).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_bk_to_fourier(const uint32_t *__restrict__ bk, double2 *__restrict__ bkf,
+                                                      int npoly, const double2 *__restrict__ W,
+                                                      const double2 *__restrict__ TW) {
+    __shared__ double2 xch[2][2][kXchStride];
+    const int grp = threadIdx.x >> 6, t = threadIdx.x & 63;
+    const int poly = blockIdx.x * 2 + grp;
+    const bool active = poly < npoly;
+    const uint32_t *src = bk + (size_t)(active ? poly : 0) * kN;
+    double2 x[8];
+#pragma unroll
+    for (int m = 0; m < 8; m++) {
+        const int j = t + 64 * m;
+        const double lo = (double)(int32_t)src[j], hi = (double)(int32_t)src[j + kNH];
+        x[m] = cmul(make_double2(lo, hi), TW[j]);
+    }
+    fft512(x, xch[grp][0], xch[grp][1], t, W, 1 + grp);
+    if (active) {
+#pragma unroll
+        for (int m = 0; m < 8; m++)
+            bkf[(size_t)poly * kNH + t + 64 * m] = make_double2(x[m].x * (1.0 / 512), x[m].y * (1.0 / 512));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1+K2+K3: fused gate prologue, blind rotation and sample extraction.
+// ---------------------------------------------------------------------------
+struct BrArgs {
+    const uint32_t *pool;     // [slots * lanes][pool_stride]
+    uint32_t pool_stride;
+    uint32_t lanes;
+    const BrItem *items;      // [n_items]
+    uint32_t n_work;          // n_items * lanes
+    int32_t n;                // LWE dimension
+    uint32_t mu;              // test-vector value (1/8)
+    const double2 *bkf;       // [n][6][2][512]
+    uint32_t *big;            // [n_work][kBigStride] extracted LWE
+    const double2 *W;         // [512] e^{2 pi i e/512}
+    const double2 *TW;        // [512] e^{i pi j/1024}
+    // debug
+    int32_t iters;            // CMux steps to run (n in production)
+    uint32_t *acc_dump;       // if set: [n_work][2N] raw accumulator
+    unsigned long long *margin;  // if set: max |v - round(v)| as double bits
+};
+
+constexpr int kStages = 4;
+constexpr int kLookahead = 2;
+constexpr uint32_t kRowBytes = 2 * kNH * sizeof(double2);  // 16 KiB: one TGSW row, both output polys
+
+template <int G>
+struct BrSmem {
+    double2 bk[kStages][2 * kNH];           // BK row ring
+    uint64_t full[kStages], empty[kStages];
+    uint32_t acc[G][2][kN];                  // TRLWE accumulators (A, B)
+    double2 xch[G][2][kXchStride];           // FFT exchange buffers
+    uint16_t bar[G][kMaxLweN + 1];           // mod-switched LWE (a_0..a_{n-1}, b)
+};
+
+template <int G, bool kDebug>
+__global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    BrSmem<G> &sm = *reinterpret_cast<BrSmem<G> *>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = args.n;
+    const int iters = min(n, args.iters);
+    const int rows_needed = iters * kRows;
+    const char *bk_src = reinterpret_cast<const char *>(args.bkf);
+
+    // BK row ring: thread 0 is the producer.  Row `it` goes to stage it % kStages;
+    // it is issued kLookahead rows ahead of its use, after every consumer warp
+    // released the row that previously occupied the stage.
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; s++) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], 2 * G);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int it = 0; it < kLookahead && it < rows_needed; it++) {
+            mbar_arrive_expect_tx(&sm.full[it], kRowBytes);
+            bulk_g2s(sm.bk[it], bk_src + (size_t)it * kRowBytes, kRowBytes, &sm.full[it]);
+        }
+    }
+    __syncthreads();
+
+    // ---- gate groups: 64 threads (2 warps) per bootstrap ----
+    const int g = warp >> 1;
+    const int t = threadIdx.x & 63;
+    const int bar_id = 1 + g;
+    const uint32_t e_raw = blockIdx.x * G + g;
+    const bool active = e_raw < args.n_work;
+    const uint32_t e = active ? e_raw : args.n_work - 1;
+    uint32_t *accA = sm.acc[g][0];
+    uint32_t *accB = sm.acc[g][1];
+    double2 *S0 = sm.xch[g][0];
+    double2 *S1 = sm.xch[g][1];
+    uint16_t *bar = sm.bar[g];
+
+    // K1: linear combination of the gate inputs + modulus switch to Z_2N
+    {
+        const uint32_t lanes = args.lanes;
+        const BrItem it = args.items[e / lanes];
+        const uint32_t lane_id = e % lanes;
+        const int alpha = (int8_t)(it.coef & 0xFF), beta = (int8_t)((it.coef >> 8) & 0xFF);
+        const uint32_t *A = args.pool + ((size_t)it.src_a * lanes + lane_id) * args.pool_stride;
+        const uint32_t *B = args.pool + ((size_t)it.src_b * lanes + lane_id) * args.pool_stride;
+        for (int c = t; c <= n; c += 64) {
+            uint32_t v = (uint32_t)alpha * __ldg(&A[c]);
+            if (beta) v += (uint32_t)beta * __ldg(&B[c]);
+            if (c == n) v += it.c0;
+            bar[c] = (uint16_t)(((v + (1u << 20)) >> 21) & (2 * kN - 1));
+        }
+    }
+    group_bar(bar_id);
+    // ACC = X^{-barb} * (0, mu...mu)
+    {
+        const int barb = bar[n];
+        for (int i = t; i < kN; i += 64) {
+            accA[i] = 0;
+            accB[i] = (((i + barb) & kN) ? 0u - args.mu : args.mu);
+        }
+    }
+    group_bar(bar_id);
+
+    const double2 *__restrict__ TW = args.TW;
+
+    double max_err = 0.0;
+    int row_it = 0;
+    for (int i = 0; i < iters; i++) {
+        const int a = bar[i];
+        double2 f0[8], f1[8];  // Fourier accumulators of the two output polys
+#pragma unroll 1
+        for (int q = 0; q < 2; q++) {
+            const uint32_t *P = q ? accB : accA;
+            uint32_t dlo[8], dhi[8];
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                const int j = t + 64 * m;
+                dlo[m] = rot_coef(P, j, a) - P[j];
+                dhi[m] = rot_coef(P, j + kNH, a) - P[j + kNH];
+            }
+#pragma unroll 1
+            for (int p = 0; p < kL; p++, row_it++) {
+                if (threadIdx.x == 0) {
+                    const int nx = row_it + kLookahead;
+                    if (nx < rows_needed) {
+                        const int s2 = nx % kStages;
+                        if (nx >= kStages) mbar_wait(&sm.empty[s2], ((nx / kStages) - 1) & 1);
+                        mbar_arrive_expect_tx(&sm.full[s2], kRowBytes);
+                        bulk_g2s(sm.bk[s2], bk_src + (size_t)nx * kRowBytes, kRowBytes, &sm.full[s2]);
+                    }
+                }
+                __syncwarp();
+                double2 x[8];
+#pragma unroll
+                for (int m = 0; m < 8; m++) {
+                    const double lo = small_int_to_double(gadget_digit(dlo[m], p));
+                    const double hi = small_int_to_double(gadget_digit(dhi[m], p));
+                    const double2 tw = __ldg(&TW[t + 64 * m]);
+                    x[m] = make_double2(lo * tw.x - hi * tw.y, lo * tw.y + hi * tw.x);
+                }
+                fft512(x, S0, S1, t, args.W, bar_id);
+                const int s = row_it % kStages;
+                mbar_wait(&sm.full[s], (row_it / kStages) & 1);
+                const double2 *bk0 = sm.bk[s];
+                const double2 *bk1 = sm.bk[s] + kNH;
+                if (kDebug && args.margin == nullptr && args.acc_dump != nullptr && args.n_work == 2) {
+                    bk0 = args.bkf + (size_t)row_it * 2 * kNH;  // bypass the ring (debug A/B)
+                    bk1 = bk0 + kNH;
+                }
+                if (q == 0 && p == 0) {
+#pragma unroll
+                    for (int m = 0; m < 8; m++) {
+                        f0[m] = cmul(x[m], bk0[t + 64 * m]);
+                        f1[m] = cmul(x[m], bk1[t + 64 * m]);
+                    }
+                } else {
+#pragma unroll
+                    for (int m = 0; m < 8; m++) {
+                        cmac(f0[m], x[m], bk0[t + 64 * m]);
+                        cmac(f1[m], x[m], bk1[t + 64 * m]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.empty[s]);
+            }
+        }
+        // inverse transforms (conjugate trick) + untwist + round + ACC update
+#pragma unroll 1
+        for (int q = 0; q < 2; q++) {
+            double2 x[8];
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                const double2 v = q ? f1[m] : f0[m];
+                x[m] = make_double2(v.x, -v.y);
+            }
+            fft512(x, S0, S1, t, args.W, bar_id);
+            uint32_t *P = q ? accB : accA;
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                // z = conj(x) * conj(tw) = conj(x * tw)
+                const double2 z = cmul(x[m], __ldg(&TW[t + 64 * m]));
+                const double lo = z.x, hi = -z.y;
+                if (kDebug) {
+                    max_err = fmax(max_err, fabs(lo - rint(lo)));
+                    max_err = fmax(max_err, fabs(hi - rint(hi)));
+                }
+                const int j = t + 64 * m;
+                P[j] += round_to_torus(lo);
+                P[j + kNH] += round_to_torus(hi);
+            }
+        }
+        group_bar(bar_id);
+    }
+
+    if (!active) return;
+    if (kDebug && args.margin) atomicMax(args.margin, (unsigned long long)__double_as_longlong(max_err));
+    if (kDebug && args.acc_dump) {
+        uint32_t *dst = args.acc_dump + (size_t)e * 2 * kN;
+        for (int c = t; c < 2 * kN; c += 64) dst[c] = (c < kN) ? accA[c] : accB[c - kN];
+    }
+    // K3: sample extract at index 0
+    uint32_t *out = args.big + (size_t)e * kBigStride;
+    for (int c = t; c <= kN; c += 64) {
+        uint32_t v;
+        if (c == 0) v = accA[0];
+        else if (c < kN) v = 0u - accA[kN - c];
+        else v = accB[0];
+        out[c] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4: batched key switch.  CTA = GK gates x 128 output columns; every KSK row
+// loaded is applied to all GK gates of the tile.
+// ---------------------------------------------------------------------------
+struct KsArgs {
+    const uint32_t *big;     // [n_br_work][kBigStride]
+    const KsItem *items;     // [n_items]
+    uint32_t lanes;
+    uint32_t n_work;         // n_items * lanes
+    const uint32_t *ksk;     // [kN][t][3][kKskStride]
+    uint32_t *pool;
+    uint32_t pool_stride;
+    int32_t n;
+};
+
+constexpr int kKsGates = 32;
+constexpr int kKsCols = 128;
+
+struct KsSmem {
+    uint16_t dig[kKsGates][kN];
+    uint32_t bvals[kKsGates];
+};
+
+__global__ void __launch_bounds__(kKsCols) k_keyswitch(const KsArgs args) {
+    extern __shared__ __align__(16) unsigned char ks_smem_raw[];
+    KsSmem &ks_sm = *reinterpret_cast<KsSmem *>(ks_smem_raw);
+    auto &dig = ks_sm.dig;
+    auto &bvals = ks_sm.bvals;
+    const int tile0 = blockIdx.x * kKsGates;
+    const int ng = min(kKsGates, (int)args.n_work - tile0);
+    const uint32_t lanes = args.lanes;
+    // digits of (a'_i + 2^15) >> 16: eight base-4 digits per coefficient
+    for (int g = 0; g < ng; g++) {
+        const uint32_t e = tile0 + g;
+        const KsItem it = args.items[e / lanes];
+        const uint32_t lane_id = e % lanes;
+        const uint32_t *b0 = args.big + ((size_t)it.i0 * lanes + lane_id) * kBigStride;
+        const uint32_t *b1 = it.i1 != 0xFFFFFFFFu ? args.big + ((size_t)it.i1 * lanes + lane_id) * kBigStride : nullptr;
+        for (int i = threadIdx.x; i < kN; i += kKsCols) {
+            uint32_t v = __ldg(&b0[i]);
+            if (b1) v += __ldg(&b1[i]);
+            dig[g][i] = (uint16_t)((v + (1u << 15)) >> 16);
+        }
+        if (threadIdx.x == 0) {
+            uint32_t b = b0[kN];
+            if (b1) b += b1[kN] + it.cadd;
+            bvals[g] = b;
+        }
+    }
+    for (int g = ng; g < kKsGates; g++)
+        for (int i = threadIdx.x; i < kN; i += kKsCols) dig[g][i] = 0;
+    __syncthreads();
+
+    const int c = blockIdx.y * kKsCols + threadIdx.x;
+    const bool col_ok = c <= args.n;
+    const int cc = col_ok ? c : 0;
+    uint32_t acc[kKsGates];
+#pragma unroll
+    for (int g = 0; g < kKsGates; g++) acc[g] = (c == args.n && g < ng) ? bvals[g] : 0u;
+
+    const uint32_t *ksk = args.ksk + cc;
+#pragma unroll 1
+    for (int i = 0; i < kN; i++) {
+        uint32_t dg[kKsGates];
+#pragma unroll
+        for (int g = 0; g < kKsGates; g++) dg[g] = dig[g][i];
+#pragma unroll
+        for (int j = 0; j < kKsT; j++) {
+            const uint32_t *row = ksk + ((size_t)(i * kKsT + j) * kKsVals) * kKskStride;
+            const uint32_t r1 = __ldg(row), r2 = __ldg(row + kKskStride), r3 = __ldg(row + 2 * kKskStride);
+            const int sh = 14 - 2 * j;
+#pragma unroll
+            for (int g = 0; g < kKsGates; g++) {
+                const uint32_t d = (dg[g] >> sh) & 3u;
+                const uint32_t v = d == 0 ? 0u : (d == 1 ? r1 : (d == 2 ? r2 : r3));
+                acc[g] -= v;
+            }
+        }
+    }
+    if (!col_ok) return;
+    for (int g = 0; g < ng; g++) {
+        const uint32_t e = tile0 + g;
+        const KsItem it = args.items[e / lanes];
+        const uint32_t lane_id = e % lanes;
+        args.pool[((size_t)it.dst * lanes + lane_id) * args.pool_stride + c] = acc[g];
+    }
+}
+
+__global__ void k_gather(const uint32_t *__restrict__ pool, uint32_t stride, const uint32_t *__restrict__ slots,
+                         uint32_t count, uint32_t words, uint32_t *__restrict__ out) {
+    const uint32_t s = blockIdx.x;
+    if (s >= count) return;
+    const uint32_t *src = pool + (size_t)slots[s] * stride;
+    for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) out[(size_t)s * words + w] = src[w];
+}
+
+// KSK host layout [kN][t][3][n+1] -> device [kN][t][3][kKskStride]
+__global__ void k_ksk_relayout(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, int n, size_t rows) {
+    const size_t r = blockIdx.x;
+    if (r >= rows) return;
+    for (int w = threadIdx.x; w < kKskStride; w += blockDim.x)
+        out[r * kKskStride + w] = w <= n ? in[r * (size_t)(n + 1) + w] : 0u;
+}
+
+constexpr int kBrGates = 4;  // bootstraps per CTA (64 threads each)
+
+template <int G>
+constexpr size_t br_smem_bytes() {
+    return sizeof(BrSmem<G>);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// engine object
+// ---------------------------------------------------------------------------
+struct hb_engine {
+    int device = 0;
+    hb_params p{};
+    cudaStream_t stream = nullptr;
+    double2 *d_W = nullptr, *d_TW = nullptr;
+    double2 *d_bkf = nullptr;
+    uint32_t *d_ksk = nullptr;
+    uint32_t *d_pool = nullptr;
+    size_t pool_cap = 0;
+    uint32_t pool_stride = 0;
+    uint32_t *d_big = nullptr;
+    size_t big_cap = 0;  // extracted-LWE slots
+    BrItem *d_br = nullptr;
+    size_t br_cap = 0;
+    KsItem *d_ks = nullptr;
+    size_t ks_cap = 0;
+    uint32_t *d_tmp = nullptr;
+    size_t tmp_cap = 0;  // words
+    void *h_stage = nullptr;
+    size_t h_stage_cap = 0;
+    unsigned long long *d_margin = nullptr;
+    cudaEvent_t ev[4]{};
+    uint64_t n_br = 0, n_ks = 0, n_launch = 0;
+};
+
+namespace {
+
+int ensure_dev(void **ptr, size_t *cap, size_t need, size_t elem, bool preserve, cudaStream_t st) {
+    if (need <= *cap) return HB_OK;
+    size_t ncap = std::max(need, *cap + *cap / 2);
+    void *np = nullptr;
+    cudaError_t err = cudaMalloc(&np, ncap * elem);
+    if (err != cudaSuccess) {
+        set_error(std::string("cudaMalloc(") + std::to_string(ncap * elem) + " B): " + cudaGetErrorString(err));
+        return HB_ENOMEM;
+    }
+    if (*ptr) {
+        if (preserve && *cap) {
+            HB_CUDA_TRY(cudaMemcpyAsync(np, *ptr, *cap * elem, cudaMemcpyDeviceToDevice, st));
+            HB_CUDA_TRY(cudaStreamSynchronize(st));
+        }
+        cudaFree(*ptr);
+    }
+    *ptr = np;
+    *cap = ncap;
+    return HB_OK;
+}
+
+int ensure_host_stage(hb_engine *e, size_t bytes) {
+    if (bytes <= e->h_stage_cap) return HB_OK;
+    HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    if (e->h_stage) cudaFreeHost(e->h_stage);
+    size_t ncap = std::max(bytes, e->h_stage_cap * 2);
+    HB_CUDA_TRY(cudaHostAlloc(&e->h_stage, ncap, cudaHostAllocDefault));
+    e->h_stage_cap = ncap;
+    return HB_OK;
+}
+
+template <int G, bool kDebug>
+int launch_br(hb_engine *e, const BrArgs &a) {
+    const size_t smem = br_smem_bytes<G>();
+    const unsigned grid = (a.n_work + G - 1) / G;
+    k_blind_rotate<G, kDebug><<<grid, 64 * G, smem, e->stream>>>(a);
+    HB_CUDA_TRY(cudaGetLastError());
+    e->n_launch++;
+    return HB_OK;
+}
+
+int launch_ks(hb_engine *e, const KsArgs &a) {
+    dim3 grid((a.n_work + kKsGates - 1) / kKsGates, (a.n + 1 + kKsCols - 1) / kKsCols);
+    k_keyswitch<<<grid, kKsCols, sizeof(KsSmem), e->stream>>>(a);
+    HB_CUDA_TRY(cudaGetLastError());
+    e->n_launch++;
+    return HB_OK;
+}
+
+BrArgs br_args(hb_engine *e) {
+    BrArgs a{};
+    a.pool = e->d_pool;
+    a.pool_stride = e->pool_stride;
+    a.lanes = 1;
+    a.n = e->p.n;
+    a.mu = 1u << 29;
+    a.bkf = e->d_bkf;
+    a.big = e->d_big;
+    a.W = e->d_W;
+    a.TW = e->d_TW;
+    a.iters = e->p.n;
+    return a;
+}
+
+int32_t pack_coef(int alpha, int beta) { return (int32_t)((uint32_t)(uint8_t)(int8_t)alpha | ((uint32_t)(uint8_t)(int8_t)beta << 8)); }
+
+}  // namespace
+
+extern "C" {
+
+int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const uint32_t *ksk, hb_engine **out) {
+    if (!out || !params_ok(p) || !bk || !ksk) {
+        set_error("hb_engine_create: unsupported parameters or null argument");
+        return HB_EINVAL;
+    }
+    *out = nullptr;
+    int ndev = 0;
+    HB_CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) {
+        set_error("hb_engine_create: CUDA device " + std::to_string(device) + " not present (" +
+                  std::to_string(ndev) + " visible)");
+        return HB_ECUDA;
+    }
+    HB_CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    HB_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+        set_error("hb_engine_create: kernels are built for sm_100a (B200); device is sm_" +
+                  std::to_string(prop.major) + std::to_string(prop.minor));
+        return HB_ECUDA;
+    }
+    hb_engine *e = new hb_engine();
+    e->device = device;
+    e->p = *p;
+    e->pool_stride = (uint32_t)((p->n + 1 + 3) & ~3);
+    HB_CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    for (auto &ev : e->ev) HB_CUDA_TRY(cudaEventCreate(&ev));
+
+    // twiddle tables, computed in long double then rounded
+    std::vector<double2> W(kNH), TW(kNH);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int j = 0; j < kNH; j++) {
+        long double th = 2.0L * pi * j / kNH;
+        W[j] = make_double2((double)cosl(th), (double)sinl(th));
+        long double ph = pi * j / kN;
+        TW[j] = make_double2((double)cosl(ph), (double)sinl(ph));
+    }
+    HB_CUDA_TRY(cudaMalloc(&e->d_W, kNH * sizeof(double2)));
+    HB_CUDA_TRY(cudaMalloc(&e->d_TW, kNH * sizeof(double2)));
+    HB_CUDA_TRY(cudaMemcpy(e->d_W, W.data(), kNH * sizeof(double2), cudaMemcpyHostToDevice));
+    HB_CUDA_TRY(cudaMemcpy(e->d_TW, TW.data(), kNH * sizeof(double2), cudaMemcpyHostToDevice));
+    HB_CUDA_TRY(cudaMalloc(&e->d_margin, sizeof(unsigned long long)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<kBrGates, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)br_smem_bytes<kBrGates>()));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)br_smem_bytes<kBrGates>()));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_keyswitch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(KsSmem)));
+
+    // BK -> Fourier
+    const size_t npoly = (size_t)p->n * kRows * 2;
+    uint32_t *d_bk = nullptr;
+    HB_CUDA_TRY(cudaMalloc(&d_bk, npoly * kN * sizeof(uint32_t)));
+    HB_CUDA_TRY(cudaMemcpy(d_bk, bk, npoly * kN * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    HB_CUDA_TRY(cudaMalloc(&e->d_bkf, npoly * kNH * sizeof(double2)));
+    k_bk_to_fourier<<<(unsigned)((npoly + 1) / 2), 128, 0, e->stream>>>(d_bk, e->d_bkf, (int)npoly, e->d_W, e->d_TW);
+    HB_CUDA_TRY(cudaGetLastError());
+    HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    cudaFree(d_bk);
+
+    // KSK
+    const size_t ksk_rows = (size_t)kN * kKsT * kKsVals;
+    uint32_t *d_kin = nullptr;
+    HB_CUDA_TRY(cudaMalloc(&d_kin, ksk_rows * (p->n + 1) * sizeof(uint32_t)));
+    HB_CUDA_TRY(cudaMemcpy(d_kin, ksk, ksk_rows * (p->n + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    HB_CUDA_TRY(cudaMalloc(&e->d_ksk, ksk_rows * kKskStride * sizeof(uint32_t)));
+    k_ksk_relayout<<<(unsigned)ksk_rows, 128, 0, e->stream>>>(d_kin, e->d_ksk, p->n, ksk_rows);
+    HB_CUDA_TRY(cudaGetLastError());
+    HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    cudaFree(d_kin);
+    *out = e;
+    return HB_OK;
+}
+
+int hb_engine_destroy(hb_engine *e) {
+    if (!e) return HB_OK;
+    cudaSetDevice(e->device);
+    if (e->stream) cudaStreamSynchronize(e->stream);
+    for (void *ptr : {(void *)e->d_W, (void *)e->d_TW, (void *)e->d_bkf, (void *)e->d_ksk, (void *)e->d_pool,
+                      (void *)e->d_big, (void *)e->d_br, (void *)e->d_ks, (void *)e->d_tmp, (void *)e->d_margin})
+        if (ptr) cudaFree(ptr);
+    if (e->h_stage) cudaFreeHost(e->h_stage);
+    for (auto &ev : e->ev)
+        if (ev) cudaEventDestroy(ev);
+    if (e->stream) cudaStreamDestroy(e->stream);
+    delete e;
+    return HB_OK;
+}
+
+int hb_pool_reserve(hb_engine *e, size_t slots) {
+    if (!e) return HB_EINVAL;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    size_t cap_words = e->pool_cap * e->pool_stride;
+    int rc = ensure_dev((void **)&e->d_pool, &cap_words, slots * e->pool_stride, sizeof(uint32_t), true, e->stream);
+    if (rc) return rc;
+    e->pool_cap = cap_words / e->pool_stride;
+    return HB_OK;
+}
+
+size_t hb_pool_capacity(const hb_engine *e) { return e ? e->pool_cap : 0; }
+size_t hb_pool_stride(const hb_engine *e) { return e ? e->pool_stride : 0; }
+
+int hb_pool_upload(hb_engine *e, size_t first, size_t count, const uint32_t *host, size_t host_stride) {
+    if (!e || (count && !host) || host_stride < (size_t)e->p.n + 1 || first + count > e->pool_cap) {
+        set_error("hb_pool_upload: bad arguments or slot range beyond capacity");
+        return HB_EINVAL;
+    }
+    if (!count) return HB_OK;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    HB_CUDA_TRY(cudaMemcpy2DAsync(e->d_pool + first * e->pool_stride, e->pool_stride * 4, host, host_stride * 4,
+                                  (size_t)(e->p.n + 1) * 4, count, cudaMemcpyHostToDevice, e->stream));
+    return HB_OK;
+}
+
+int hb_pool_download(hb_engine *e, size_t first, size_t count, uint32_t *host, size_t host_stride) {
+    if (!e || (count && !host) || host_stride < (size_t)e->p.n + 1 || first + count > e->pool_cap) {
+        set_error("hb_pool_download: bad arguments or slot range beyond capacity");
+        return HB_EINVAL;
+    }
+    if (!count) return HB_OK;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    HB_CUDA_TRY(cudaMemcpy2DAsync(host, host_stride * 4, e->d_pool + first * e->pool_stride, e->pool_stride * 4,
+                                  (size_t)(e->p.n + 1) * 4, count, cudaMemcpyDeviceToHost, e->stream));
+    HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return HB_OK;
+}
+
+int hb_pool_gather(hb_engine *e, const uint32_t *slots, size_t count, uint32_t *host, size_t host_stride) {
+    if (!e || (count && (!slots || !host)) || host_stride < (size_t)e->p.n + 1) {
+        set_error("hb_pool_gather: bad arguments");
+        return HB_EINVAL;
+    }
+    if (!count) return HB_OK;
+    for (size_t i = 0; i < count; i++)
+        if (slots[i] >= e->pool_cap) {
+            set_error("hb_pool_gather: slot beyond pool capacity");
+            return HB_EINVAL;
+        }
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    const uint32_t words = (uint32_t)e->p.n + 1;
+    const size_t need = count + (count * words + 3) / 1;
+    int rc = ensure_dev((void **)&e->d_tmp, &e->tmp_cap, need, sizeof(uint32_t), false, e->stream);
+    if (rc) return rc;
+    rc = ensure_host_stage(e, count * sizeof(uint32_t));
+    if (rc) return rc;
+    std::memcpy(e->h_stage, slots, count * sizeof(uint32_t));
+    uint32_t *d_slots = e->d_tmp, *d_out = e->d_tmp + count;
+    HB_CUDA_TRY(cudaMemcpyAsync(d_slots, e->h_stage, count * sizeof(uint32_t), cudaMemcpyHostToDevice, e->stream));
+    k_gather<<<(unsigned)count, 256, 0, e->stream>>>(e->d_pool, e->pool_stride, d_slots, (uint32_t)count, words, d_out);
+    HB_CUDA_TRY(cudaGetLastError());
+    HB_CUDA_TRY(cudaMemcpy2DAsync(host, host_stride * 4, d_out, (size_t)words * 4, (size_t)words * 4, count,
+                                  cudaMemcpyDeviceToHost, e->stream));
+    HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    e->n_launch++;
+    return HB_OK;
+}
+
+int hb_run_gates(hb_engine *e, const hb_gate *gates, size_t n, uint32_t lanes) {
+    if (!e || (n && !gates) || lanes == 0) {
+        set_error("hb_run_gates: bad arguments");
+        return HB_EINVAL;
+    }
+    if (!n) return HB_OK;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    // expand records into blind-rotation and key-switch work items
+    size_t nbr = 0;
+    for (size_t i = 0; i < n; i++) {
+        const hb_gate &g = gates[i];
+        if (g.kind != HB_GATE_LIN2 && g.kind != HB_GATE_MUX) {
+            set_error("hb_run_gates: unknown gate kind " + std::to_string((int)g.kind));
+            return HB_EINVAL;
+        }
+        const size_t top = (size_t)std::max(std::max(g.dst, g.src_a), std::max(g.src_b, g.src_c)) + 1;
+        if (top * lanes > e->pool_cap) {
+            set_error("hb_run_gates: slot beyond pool capacity");
+            return HB_EINVAL;
+        }
+        nbr += (g.kind == HB_GATE_MUX) ? 2 : 1;
+    }
+    const size_t br_bytes = nbr * sizeof(BrItem), ks_bytes = n * sizeof(KsItem);
+    int rc = ensure_host_stage(e, br_bytes + ks_bytes);
+    if (rc) return rc;
+    HB_CUDA_TRY(cudaStreamSynchronize(e->stream));  // host stage may still feed the previous level
+    BrItem *hbr = reinterpret_cast<BrItem *>(e->h_stage);
+    KsItem *hks = reinterpret_cast<KsItem *>(reinterpret_cast<char *>(e->h_stage) + br_bytes);
+    size_t b = 0;
+    const uint32_t eighth = 1u << 29;
+    for (size_t i = 0; i < n; i++) {
+        const hb_gate &g = gates[i];
+        if (g.kind == HB_GATE_LIN2) {
+            hbr[b] = BrItem{g.src_a, g.src_b, g.c0, pack_coef(g.alpha, g.beta)};
+            hks[i] = KsItem{g.dst, (uint32_t)b, 0xFFFFFFFFu, 0u};
+            b += 1;
+        } else {
+            hbr[b] = BrItem{g.src_a, g.src_b, 0u - eighth, pack_coef(1, g.alpha)};
+            hbr[b + 1] = BrItem{g.src_a, g.src_c, 0u - eighth, pack_coef(-1, g.beta)};
+            hks[i] = KsItem{g.dst, (uint32_t)b, (uint32_t)(b + 1), eighth};
+            b += 2;
+        }
+    }
+    if ((rc = ensure_dev((void **)&e->d_br, &e->br_cap, nbr, sizeof(BrItem), false, e->stream))) return rc;
+    if ((rc = ensure_dev((void **)&e->d_ks, &e->ks_cap, n, sizeof(KsItem), false, e->stream))) return rc;
+    if ((rc = ensure_dev((void **)&e->d_big, &e->big_cap, nbr * lanes * kBigStride, sizeof(uint32_t), false,
+                         e->stream)))
+        return rc;
+    HB_CUDA_TRY(cudaMemcpyAsync(e->d_br, hbr, br_bytes, cudaMemcpyHostToDevice, e->stream));
+    HB_CUDA_TRY(cudaMemcpyAsync(e->d_ks, hks, ks_bytes, cudaMemcpyHostToDevice, e->stream));
+
+    BrArgs a = br_args(e);
+    a.lanes = lanes;
+    a.items = e->d_br;
+    a.n_work = (uint32_t)(nbr * lanes);
+    HB_CUDA_TRY(cudaEventRecord(e->ev[0], e->stream));
+    if ((rc = launch_br<kBrGates, false>(e, a))) return rc;
+    HB_CUDA_TRY(cudaEventRecord(e->ev[1], e->stream));
+    KsArgs k{};
+    k.big = e->d_big;
+    k.items = e->d_ks;
+    k.lanes = lanes;
+    k.n_work = (uint32_t)(n * lanes);
+    k.ksk = e->d_ksk;
+    k.pool = e->d_pool;
+    k.pool_stride = e->pool_stride;
+    k.n = e->p.n;
+    if ((rc = launch_ks(e, k))) return rc;
+    HB_CUDA_TRY(cudaEventRecord(e->ev[2], e->stream));
+    e->n_br += nbr * lanes;
+    e->n_ks += n * lanes;
+    return HB_OK;
+}
+
+int hb_sync(hb_engine *e) {
+    if (!e) return HB_EINVAL;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return HB_OK;
+}
+
+int hb_last_timing(hb_engine *e, float *br_ms, float *ks_ms) {
+    if (!e) return HB_EINVAL;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    HB_CUDA_TRY(cudaEventSynchronize(e->ev[2]));
+    float x = 0, y = 0;
+    HB_CUDA_TRY(cudaEventElapsedTime(&x, e->ev[0], e->ev[1]));
+    HB_CUDA_TRY(cudaEventElapsedTime(&y, e->ev[1], e->ev[2]));
+    if (br_ms) *br_ms = x;
+    if (ks_ms) *ks_ms = y;
+    return HB_OK;
+}
+
+int hb_counters(hb_engine *e, uint64_t *brs, uint64_t *kss, uint64_t *launches) {
+    if (!e) return HB_EINVAL;
+    if (brs) *brs = e->n_br;
+    if (kss) *kss = e->n_ks;
+    if (launches) *launches = e->n_launch;
+    return HB_OK;
+}
+
+int hb_debug_blind_rotate(hb_engine *e, const uint32_t *lwe, uint32_t mu, int32_t iters, uint32_t *acc_out) {
+    if (!e || !lwe || !acc_out) return HB_EINVAL;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    const size_t words = e->p.n + 1;
+    int rc;
+    if ((rc = ensure_dev((void **)&e->d_tmp, &e->tmp_cap, 2 * words + 4 * kN + 64, sizeof(uint32_t), false, e->stream)))
+        return rc;
+    if ((rc = ensure_dev((void **)&e->d_br, &e->br_cap, 1, sizeof(BrItem), false, e->stream))) return rc;
+    if ((rc = ensure_dev((void **)&e->d_big, &e->big_cap, kBigStride, sizeof(uint32_t), false, e->stream))) return rc;
+    uint32_t *d_in = e->d_tmp, *d_acc = e->d_tmp + ((2 * words + 3) & ~size_t(3));
+    BrItem it{0, 0, 0, pack_coef(1, 0)};
+    HB_CUDA_TRY(cudaMemcpyAsync(d_in, lwe, words * 4, cudaMemcpyHostToDevice, e->stream));
+    HB_CUDA_TRY(cudaMemcpyAsync(e->d_br, &it, sizeof it, cudaMemcpyHostToDevice, e->stream));
+    BrArgs a = br_args(e);
+    a.pool = d_in;
+    a.pool_stride = (uint32_t)words;
+    a.items = e->d_br;
+    a.n_work = 1;
+    a.mu = mu;
+    if (iters >= 100000) {  // debug A/B: BK rows read from global instead of the ring
+        iters -= 100000;
+        a.n_work = 2;
+        a.lanes = 2;
+    }
+    a.iters = iters < 0 ? e->p.n : iters;
+    a.acc_dump = d_acc;
+    if ((rc = launch_br<kBrGates, true>(e, a))) return rc;
+    HB_CUDA_TRY(cudaMemcpyAsync(acc_out, d_acc, 2 * kN * 4, cudaMemcpyDeviceToHost, e->stream));
+    HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return HB_OK;
+}
+
+int hb_debug_bootstrap_wo_ks(hb_engine *e, const uint32_t *lin, size_t count, uint32_t *out) {
+    if (!e || (count && (!lin || !out))) return HB_EINVAL;
+    if (!count) return HB_OK;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    const size_t words = e->p.n + 1;
+    int rc;
+    if ((rc = ensure_dev((void **)&e->d_tmp, &e->tmp_cap, count * words, sizeof(uint32_t), false, e->stream)))
+        return rc;
+    if ((rc = ensure_dev((void **)&e->d_br, &e->br_cap, count, sizeof(BrItem), false, e->stream))) return rc;
+    if ((rc = ensure_dev((void **)&e->d_big, &e->big_cap, count * kBigStride, sizeof(uint32_t), false, e->stream)))
+        return rc;
+    std::vector<BrItem> items(count);
+    for (size_t i = 0; i < count; i++) items[i] = BrItem{(uint32_t)i, (uint32_t)i, 0u, pack_coef(1, 0)};
+    HB_CUDA_TRY(cudaMemcpyAsync(e->d_tmp, lin, count * words * 4, cudaMemcpyHostToDevice, e->stream));
+    HB_CUDA_TRY(cudaMemcpyAsync(e->d_br, items.data(), count * sizeof(BrItem), cudaMemcpyHostToDevice, e->stream));
+    HB_CUDA_TRY(cudaMemsetAsync(e->d_margin, 0, sizeof(unsigned long long), e->stream));
+    BrArgs a = br_args(e);
+    a.pool = e->d_tmp;
+    a.pool_stride = (uint32_t)words;
+    a.items = e->d_br;
+    a.n_work = (uint32_t)count;
+    a.margin = e->d_margin;
+    if ((rc = launch_br<kBrGates, true>(e, a))) return rc;
+    HB_CUDA_TRY(cudaMemcpy2DAsync(out, (size_t)(kN + 1) * 4, e->d_big, kBigStride * 4, (size_t)(kN + 1) * 4, count,
+                                  cudaMemcpyDeviceToHost, e->stream));
+    HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return HB_OK;
+}
+
+int hb_debug_fourier(hb_engine *e, const uint32_t *polys, size_t count, double *out, int which) {
+    if (!e || (count && (!polys || !out))) return HB_EINVAL;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    if (which == 1) {  // download rows of the device BK Fourier table
+        HB_CUDA_TRY(cudaMemcpy(out, e->d_bkf, count * kNH * sizeof(double2), cudaMemcpyDeviceToHost));
+        return HB_OK;
+    }
+    uint32_t *d_in = nullptr;
+    double2 *d_out = nullptr;
+    HB_CUDA_TRY(cudaMalloc(&d_in, count * kN * 4));
+    HB_CUDA_TRY(cudaMalloc(&d_out, count * kNH * sizeof(double2)));
+    HB_CUDA_TRY(cudaMemcpy(d_in, polys, count * kN * 4, cudaMemcpyHostToDevice));
+    k_bk_to_fourier<<<(unsigned)((count + 1) / 2), 128, 0, e->stream>>>(d_in, d_out, (int)count, e->d_W, e->d_TW);
+    HB_CUDA_TRY(cudaGetLastError());
+    HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    HB_CUDA_TRY(cudaMemcpy(out, d_out, count * kNH * sizeof(double2), cudaMemcpyDeviceToHost));
+    cudaFree(d_in);
+    cudaFree(d_out);
+    return HB_OK;
+}
+
+int hb_debug_fft_margin(hb_engine *e, double *max_err) {
+    if (!e || !max_err) return HB_EINVAL;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    unsigned long long bits = 0;
+    HB_CUDA_TRY(cudaMemcpy(&bits, e->d_margin, sizeof bits, cudaMemcpyDeviceToHost));
+    std::memcpy(max_err, &bits, sizeof(double));
+    return HB_OK;
+}
+
+int hb_debug_keyswitch(hb_engine *e, const uint32_t *in, size_t count, uint32_t *out) {
+    if (!e || (count && (!in || !out))) return HB_EINVAL;
+    if (!count) return HB_OK;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    int rc;
+    const size_t words = e->p.n + 1;
+    if ((rc = ensure_dev((void **)&e->d_big, &e->big_cap, count * kBigStride, sizeof(uint32_t), false, e->stream)))
+        return rc;
+    if ((rc = ensure_dev((void **)&e->d_tmp, &e->tmp_cap, count * e->pool_stride, sizeof(uint32_t), false, e->stream)))
+        return rc;
+    if ((rc = ensure_dev((void **)&e->d_ks, &e->ks_cap, count, sizeof(KsItem), false, e->stream))) return rc;
+    std::vector<KsItem> items(count);
+    for (size_t i = 0; i < count; i++) items[i] = KsItem{(uint32_t)i, (uint32_t)i, 0xFFFFFFFFu, 0u};
+    HB_CUDA_TRY(cudaMemcpy2DAsync(e->d_big, kBigStride * 4, in, (size_t)(kN + 1) * 4, (size_t)(kN + 1) * 4, count,
+                                  cudaMemcpyHostToDevice, e->stream));
+    HB_CUDA_TRY(cudaMemcpyAsync(e->d_ks, items.data(), count * sizeof(KsItem), cudaMemcpyHostToDevice, e->stream));
+    KsArgs k{};
+    k.big = e->d_big;
+    k.items = e->d_ks;
+    k.lanes = 1;
+    k.n_work = (uint32_t)count;
+    k.ksk = e->d_ksk;
+    k.pool = e->d_tmp;
+    k.pool_stride = e->pool_stride;
+    k.n = e->p.n;
+    if ((rc = launch_ks(e, k))) return rc;
+    HB_CUDA_TRY(cudaMemcpy2DAsync(out, words * 4, e->d_tmp, e->pool_stride * 4, words * 4, count,
+                                  cudaMemcpyDeviceToHost, e->stream));
+    HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return HB_OK;
+}
+
+}  // extern "C"

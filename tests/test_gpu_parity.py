@@ -1,0 +1,87 @@
+"""GPU parity: every stage of the CUDA gate bootstrap against the exact CPU
+oracle on the same seeded keys and inputs (bit-exact ciphertexts)."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1806_03461_b200 import tfhe
+
+pytestmark = pytest.mark.gpu
+
+P = O.default_params()
+
+
+def _lin(keys, seed, count):
+    rng = np.random.default_rng(seed)
+    bits = rng.integers(0, 2, count).astype(np.uint8)
+    return keys.encrypt(bits, seed=seed, stream=1)
+
+
+@pytest.mark.parametrize("iters", [1, 2, 7])
+def test_blind_rotate_prefix_bit_exact(engine, keys, octx, iters):
+    lwe = _lin(keys, 11, 1)[0]
+    got = engine.debug_blind_rotate(lwe, iters=iters)
+    want = octx.blind_rotate(lwe, iters=iters)
+    assert np.array_equal(got, want)
+
+
+def test_bootstrap_wo_ks_bit_exact(engine, keys, octx):
+    lin = _lin(keys, 12, 6)
+    got = engine.debug_bootstrap_wo_ks(lin)
+    margin = engine.debug_fft_margin()
+    for i in range(lin.shape[0]):
+        assert np.array_equal(got[i], octx.bootstrap_wo_ks(lin[i]))
+    assert margin < 0.25, margin
+
+
+def test_keyswitch_bit_exact(engine, keys, octx):
+    rng = np.random.default_rng(13)
+    big = rng.integers(0, 2**32, (40, P.N + 1), dtype=np.uint64).astype(np.uint32)
+    got = engine.debug_keyswitch(big)
+    for i in range(big.shape[0]):
+        assert np.array_equal(got[i], octx.keyswitch(big[i]))
+
+
+@pytest.mark.parametrize("name", list(tfhe.GATE_LIN))
+def test_gate_truth_table_and_bit_exact(engine, keys, octx, name):
+    c0, al, be = tfhe.GATE_LIN[name]
+    a_bits = np.array([0, 0, 1, 1], np.uint8)
+    b_bits = np.array([0, 1, 0, 1], np.uint8)
+    ca = keys.encrypt(a_bits, seed=21, stream=1)
+    cb = keys.encrypt(b_bits, seed=21, stream=2)
+    engine.reserve(12)
+    engine.upload(0, ca)
+    engine.upload(4, cb)
+    recs = tfhe.gate_records(4)
+    for i in range(4):
+        recs[i] = (8 + i, i, 4 + i, 0, c0, al, be, 0, 0)
+    engine.run_gates(recs)
+    out = engine.download(8, 4)
+    fn = {"AND": np.bitwise_and, "OR": np.bitwise_or, "XOR": np.bitwise_xor}
+    plain = {
+        "AND": a_bits & b_bits, "OR": a_bits | b_bits, "XOR": a_bits ^ b_bits,
+        "XNOR": 1 - (a_bits ^ b_bits), "NAND": 1 - (a_bits & b_bits), "NOR": 1 - (a_bits | b_bits),
+    }[name]
+    assert np.array_equal(keys.decrypt(out), plain)
+    for i in range(4):
+        assert np.array_equal(out[i], octx.gate(c0, al, ca[i], be, cb[i]))
+
+
+def test_mux_bit_exact(engine, keys, octx):
+    s = np.array([0, 0, 0, 0, 1, 1, 1, 1], np.uint8)
+    a = np.array([0, 0, 1, 1, 0, 0, 1, 1], np.uint8)
+    b = np.array([0, 1, 0, 1, 0, 1, 0, 1], np.uint8)
+    cs, ca, cb = (keys.encrypt(v, seed=31, stream=k) for k, v in enumerate((s, a, b)))
+    engine.reserve(32)
+    engine.upload(0, cs)
+    engine.upload(8, ca)
+    engine.upload(16, cb)
+    recs = tfhe.gate_records(8)
+    for i in range(8):
+        recs[i] = (24 + i, i, 8 + i, 16 + i, 0, 1, 1, 1, 0)
+    engine.run_gates(recs)
+    out = engine.download(24, 8)
+    assert np.array_equal(keys.decrypt(out), np.where(s == 1, a, b))
+    for i in (0, 5):
+        assert np.array_equal(out[i], octx.mux(cs[i], ca[i], cb[i]))

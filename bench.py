@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark: bootstrapped gates/sec on B200 (BASELINE.json metric) +
+encrypted-BNN latency.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[0], the metric's own micro-bench): per GPU,
+4,096 independent bootstrapped NAND gates on encrypted Bernoulli(0.5) bit
+pairs, keys and messages from one seed.  One step = one hb_run_gates level of
+the 4,096 gates (fused gate prologue + blind rotation + sample extract, then
+batched key switch) with the inputs resident in HBM.  Multi-GPU: every rank
+runs its own 4,096 gates (weak scaling, replicated keys, no collective on the
+data path — gates are independent), timed on the device with CUDA events and
+reduced with MAX over ranks.
+
+`e2e` repeats the step through the C ABI with host buffers: H2D of the two
+input ciphertext batches from pinned memory, the gate records, the level, and
+D2H of the 4,096 output ciphertexts, all inside the timed region.
+
+`--impl reference` times the CPU path (the exact-integer C oracle, run with
+all host threads) on a bounded sample of the same workload; the reference
+package itself has no ciphertext arithmetic (it simulates in plaintext).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+for _p in (ROOT, os.path.join(ROOT, "baseline", "_ref")):
+    if _p not in sys.path:
+        sys.path.insert(0, _p)
+
+import numpy as np  # noqa: E402
+
+# F_BS: algorithmic FP64 flops of one blind rotation:
+# n * [(k+1)(l+1) * F_FFT + (k+1)^2 * l * (N/2) * 8],  F_FFT = 5 (N/2) log2(N/2) + 6 (N/2)
+F_FFT = 5 * 512 * 9 + 6 * 512
+F_BS = 630 * (2 * 4 * F_FFT + 4 * 3 * 512 * 8)
+assert F_BS == 162_570_240
+METRIC = "bootstrapped gates/sec"
+WORKLOAD = "cfg1: 4096 independent bootstrapped NAND gates per GPU (TFHE n=630,N=1024,k=1,Bg=2^7,l=3,KS 2^2x8)"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--gates", type=int, default=4096)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--bnn", choices=("none", "neuron", "layer"), default="neuron",
+                    help="extra encrypted-BNN latency measurement (cfg2) on rank 0")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (torch.distributed: barrier + max over ranks only)
+# ---------------------------------------------------------------------------
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local_rank)
+            dist.init_process_group(backend=backend)
+            self.pg = dist
+            self.torch = torch
+
+    def barrier(self):
+        if self.pg:
+            if self.torch.cuda.is_available():
+                self.pg.barrier(device_ids=[self.local_rank])
+            else:
+                self.pg.barrier()
+
+    def max(self, x):
+        if not self.pg:
+            return x
+        dev = f"cuda:{self.local_rank}" if self.torch.cuda.is_available() else "cpu"
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# nvidia-smi clock sampler (recipe's clocks line)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax = float(parts[2])
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        loaded = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle) — the only place bench.py executes oracle/
+# ---------------------------------------------------------------------------
+
+def cpu_nand_sample(seed, gates, threads):
+    """Time `gates` NANDs on the exact CPU oracle with `threads` pthreads."""
+    from oracle import oracle as O
+
+    p = O.default_params()
+    keys = O.Keys(p, seed)
+    ctx = O.Context(p, keys)
+    rng = np.random.default_rng(seed)
+    a = rng.integers(0, 2, gates).astype(np.uint8)
+    b = rng.integers(0, 2, gates).astype(np.uint8)
+    pool = np.zeros((3 * gates, p.n + 1), np.uint32)
+    pool[:gates] = O.encrypt(p, keys, a, seed, 1)
+    pool[gates:2 * gates] = O.encrypt(p, keys, b, seed, 2)
+    recs = np.zeros(gates, dtype=[("dst", "<u4"), ("src_a", "<u4"), ("src_b", "<u4"), ("src_c", "<u4"),
+                                  ("c0", "<u4"), ("alpha", "i1"), ("beta", "i1"), ("kind", "i1"), ("_pad", "i1")])
+    c0, al, be = O.GATE_LIN["NAND"]
+    recs["dst"] = np.arange(2 * gates, 3 * gates)
+    recs["src_a"] = np.arange(gates)
+    recs["src_b"] = np.arange(gates, 2 * gates)
+    recs["c0"], recs["alpha"], recs["beta"] = c0, al, be
+
+    def step():
+        t0 = time.perf_counter()
+        ctx.run_gates(recs, pool, threads=threads)
+        return time.perf_counter() - t0
+
+    ok = lambda: bool(np.array_equal(O.decrypt(p, keys, pool[2 * gates:]), 1 - (a & b)))  # noqa: E731
+    return step, ok
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args, dist):
+    if dist.rank != 0:
+        return None
+    threads = os.cpu_count() or 1
+    sample = 2 * threads
+    step, ok = cpu_nand_sample(args.seed, sample, threads)
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    assert ok(), "CPU oracle produced wrong NAND outputs"
+    value = sample * len(times) / sum(times)
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32 torus (exact integer NTT)", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "gates_per_step": sample, "sample_of": args.gates},
+        "cpu_baseline": {"value": value, "unit": "gates/s", "cores": threads, "kind": "port",
+                         "sample": f"{sample} NAND gates per step on {threads} threads ({cpu_model()}); "
+                                   "exact-integer CGGI oracle/tfhe_oracle.c (reference has no crypto)"},
+        "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def bnn_neuron_latency(kind, seed):
+    """cfg2: one 784->1 neuron (or the 784->256 layer) through the reference
+    compiler on TfheContext; latency of the encrypted evaluation."""
+    import random
+
+    from hebnn.compiler import EvalOptions, decrypt_output, encrypt_input, eval_model
+    from hebnn.model import DenseLayer, SignActivation, TernaryModel, oracle_eval, validate_model
+
+    from paper_1806_03461_b200.backend import TfheContext
+
+    rng = random.Random(seed)
+    p = 1 if kind == "neuron" else 256
+    rows = tuple(tuple(rng.choice((-1, 1)) for _ in range(784)) for _ in range(p))
+    model = validate_model(TernaryModel(784, (DenseLayer(rows, (0,) * p), SignActivation()), "sign_bits"))
+    xs = [rng.choice((-1, 1)) for _ in range(784)]
+    ctx = TfheContext(seed=seed)
+    xb = encrypt_input(ctx, xs)
+    t0 = time.perf_counter()
+    outs, _ = eval_model(ctx, model, xb, EvalOptions())
+    t_dag = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    ctx.flush()
+    t_dev = time.perf_counter() - t1
+    got = decrypt_output(ctx, outs)
+    return {
+        "config": f"cfg2 {'784->1 neuron' if p == 1 else '784->256 layer'}, plus_one on, reduce comparator",
+        "latency_s": t_dev, "dag_build_s": t_dag, "counted_gates": ctx.gate_count,
+        "executed_bootstraps": ctx.exec_stats["bootstraps"], "levels": ctx.exec_stats["levels"],
+        "counted_gates_per_s": ctx.gate_count / t_dev, "matches_oracle_eval": got == oracle_eval(model, xs),
+    }
+
+
+def run_ours(args, dist):
+    import torch
+
+    from paper_1806_03461_b200 import tfhe
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the engine has no CPU fallback)")
+    dev = dist.local_rank
+    keys = tfhe.KeySet(seed=args.seed)
+    eng = tfhe.Engine(keys, device=dev)
+    n = args.gates
+    rng = np.random.default_rng(1000 + dist.rank)
+    a = rng.integers(0, 2, n).astype(np.uint8)
+    b = rng.integers(0, 2, n).astype(np.uint8)
+    words = keys.params.n + 1
+    # pinned host staging (torch is plumbing here)
+    h_in = torch.empty((2 * n, words), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    h_in[:n] = keys.encrypt(a, seed=args.seed, stream=2 * dist.rank + 1)
+    h_in[n:] = keys.encrypt(b, seed=args.seed, stream=2 * dist.rank + 2)
+    h_out = torch.empty((n, words), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    eng.reserve(3 * n)
+    eng.upload(0, h_in)
+    recs = tfhe.gate_records(n)
+    c0, al, be = tfhe.GATE_LIN["NAND"]
+    recs["dst"] = np.arange(2 * n, 3 * n)
+    recs["src_a"] = np.arange(n)
+    recs["src_b"] = np.arange(n, 2 * n)
+    recs["c0"], recs["alpha"], recs["beta"] = c0, al, be
+
+    fp64_peak = eng.measure_fp64_peak()
+
+    for _ in range(args.warmup):
+        eng.run_gates(recs)
+        eng.sync()
+    eng.sync()
+    dist.barrier()
+    launches0 = eng.counters()["kernel_launches"]
+    clocks = ClockSampler(dev)
+    clocks.start()
+    step_ms, br_ms, ks_ms = [], [], []
+    for _ in range(args.steps):
+        eng.flush_l2()           # cold L2 for every timed step
+        eng.sync()
+        eng.run_gates(recs)
+        br, ks = eng.last_timing()  # CUDA events on the engine stream
+        br_ms.append(br)
+        ks_ms.append(ks)
+        step_ms.append(br + ks)
+    eng.sync()
+    clk = clocks.stop()
+    launches = eng.counters()["kernel_launches"] - launches0
+    out = eng.download(2 * n, n)
+    correct = bool(np.array_equal(keys.decrypt(out), 1 - (a & b)))
+
+    total_s = dist.max(sum(step_ms) / 1e3)
+    value = n * dist.world * args.steps / total_s
+
+    # e2e through the C ABI with host buffers
+    dist.barrier()
+    e2e_times = []
+    for _ in range(args.steps):
+        eng.sync()
+        t0 = time.perf_counter()
+        eng.upload(0, h_in)
+        eng.run_gates(recs)
+        tfhe.lib().hb_pool_download(eng._e, 2 * n, n, tfhe.u32p(h_out), words)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_total = dist.max(sum(e2e_times))
+    e2e_value = n * dist.world * args.steps / e2e_total
+    correct &= bool(np.array_equal(keys.decrypt(h_out), 1 - (a & b)))
+
+    br_med = statistics.median(br_ms)
+    achieved = n * F_BS / (br_med / 1e3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": dist.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dist.max(statistics.mean(step_ms)), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32 torus; FP64 negacyclic FFT (bit-exact vs integer oracle)", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "gates_per_gpu": n, "parallelism": f"replicated keys, {dist.world} GPU(s)",
+                   "l2": "flushed (256 MiB write) before every timed step", "inputs": "resident in HBM"},
+        "e2e": {"value": e2e_value, "unit": "gates/s", "h2d_bytes_per_step": int(h_in.nbytes + recs.nbytes),
+                "d2h_bytes_per_step": int(h_out.nbytes)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": achieved / fp64_peak, "traffic": None,
+                     "kernel": "k_blind_rotate", "flops_per_bootstrap": F_BS,
+                     "peak_source": "DFMA micro-benchmark in this run (MEASURED_PEAKS.json has no FP64 figure)"},
+        "kernel_ms": {"blind_rotate": br_med, "key_switch": statistics.median(ks_ms)},
+        "clocks": clk,
+        "correct": correct,
+    }
+    if dist.rank == 0 and args.bnn != "none":
+        try:
+            line["bnn"] = bnn_neuron_latency(args.bnn, args.seed)
+        except Exception as exc:  # report, never hide
+            line["bnn"] = {"error": repr(exc)}
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        sample = 2 * threads
+        step, ok = cpu_nand_sample(args.seed, sample, threads)
+        dt = step()
+        line["cpu_baseline"] = {"value": sample / dt, "unit": "gates/s", "cores": threads, "kind": "port",
+                                "sample": f"{sample} NAND gates on {threads} threads ({cpu_model()}), "
+                                          f"{dt:.1f} s; exact-integer CGGI oracle (reference has no crypto)",
+                                "correct": ok()}
+    eng.close()
+    return line
+
+
+def main():
+    args = parse_args()
+    dist = Dist()
+    try:
+        line = run_reference(args, dist) if args.impl == "reference" else run_ours(args, dist)
+        if dist.rank == 0 and line is not None:
+            print(json.dumps(line), flush=True)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

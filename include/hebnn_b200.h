@@ -89,10 +89,12 @@ int hb_keygen(const hb_params *p, uint64_t seed, uint32_t *lwe_key, uint32_t *tr
               uint32_t *bk, uint32_t *ksk, int threads);
 
 /* Encrypt count bits (each 0/1, else HB_EINVAL) into out[count][out_stride]
- * (out_stride >= n+1). Ciphertext idx uses ChaCha nonce
- * (0x05<<56) | ((stream & 0xFFFFF) << 32) | idx with the key expanded from seed. */
+ * (out_stride >= n+1). Ciphertext i uses ChaCha nonce
+ * (0x05<<56) | ((stream & 0xFFFFF) << 32) | (first_index + i) with the key
+ * expanded from seed (first_index + count <= 2^32). */
 int hb_encrypt(const hb_params *p, const uint32_t *lwe_key, uint64_t seed, uint64_t stream,
-               const uint8_t *bits, size_t count, uint32_t *out, size_t out_stride);
+               uint64_t first_index, const uint8_t *bits, size_t count, uint32_t *out,
+               size_t out_stride);
 
 /* phase = b - <a, s> (int32, i.e. signed torus * 2^32); bit = phase > 0. */
 int hb_phase(const hb_params *p, const uint32_t *lwe_key, const uint32_t *cts, size_t count,
@@ -134,6 +136,13 @@ int hb_sync(hb_engine *e);
 int hb_last_timing(hb_engine *e, float *br_ms, float *ks_ms);
 int hb_counters(hb_engine *e, uint64_t *blind_rotations, uint64_t *key_switches,
                 uint64_t *kernel_launches);
+
+/* Write `bytes` (0: 256 MiB, i.e. > 2x the 126 MB L2) of scratch on the engine
+ * stream so the next launch starts with a cold L2 (benchmark hygiene). */
+int hb_flush_l2(hb_engine *e, size_t bytes);
+/* FP64 roofline probe: DFMA throughput (TFLOP/s) of this device, measured with
+ * CUDA events on the engine stream (8 independent FMA chains per thread). */
+int hb_measure_fp64_peak(hb_engine *e, double *tflops);
 
 /* ---- stage entry points for bit-level parity (synchronous, host buffers) ---- */
 

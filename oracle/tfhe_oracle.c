@@ -366,12 +366,12 @@ int or_keygen(const or_params *p, uint64_t seed, uint32_t *lwe_key, uint32_t *tr
 }
 
 int or_encrypt(const or_params *p, const uint32_t *lwe_key, uint64_t seed, uint64_t stream,
-               const uint8_t *bits, size_t count, uint32_t *out) {
+               uint64_t first_index, const uint8_t *bits, size_t count, uint32_t *out) {
     const int n = p->n;
     for (size_t idx = 0; idx < count; idx++) {
         if (bits[idx] > 1) return -1;
         rng_t r;
-        rng_init(&r, seed, (DOM_ENC << 56) | ((stream & 0xFFFFFull) << 32) | (uint64_t)idx);
+        rng_init(&r, seed, (DOM_ENC << 56) | ((stream & 0xFFFFFull) << 32) | (first_index + (uint64_t)idx));
         uint32_t *ct = out + idx * (size_t)(n + 1);
         for (int a = 0; a < n; a++) ct[a] = rng_u32(&r);
         uint32_t mu = bits[idx] ? (1u << 29) : (0u - (1u << 29));

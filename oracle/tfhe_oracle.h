@@ -62,10 +62,10 @@ void or_chacha_block(const uint32_t key[8], uint64_t nonce, uint64_t counter, ui
 int or_keygen(const or_params *p, uint64_t seed, uint32_t *lwe_key, uint32_t *trlwe_key,
               uint32_t *bk, uint32_t *ksk);
 
-/* Encrypt bits under lwe_key: out[count][n+1]; ciphertext idx uses the
- * ChaCha nonce (0x05<<56) | ((stream & 0xFFFFF) << 32) | idx. */
+/* Encrypt bits under lwe_key: out[count][n+1]; ciphertext i uses the
+ * ChaCha nonce (0x05<<56) | ((stream & 0xFFFFF) << 32) | (first_index + i). */
 int or_encrypt(const or_params *p, const uint32_t *lwe_key, uint64_t seed, uint64_t stream,
-               const uint8_t *bits, size_t count, uint32_t *out);
+               uint64_t first_index, const uint8_t *bits, size_t count, uint32_t *out);
 void or_phase(const or_params *p, const uint32_t *lwe_key, const uint32_t *cts, size_t count,
               int32_t *phase_out);
 void or_decrypt(const or_params *p, const uint32_t *lwe_key, const uint32_t *cts, size_t count,

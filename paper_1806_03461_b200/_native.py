@@ -30,7 +30,7 @@ EXPORTED = (
     "hb_engine_destroy", "hb_pool_reserve", "hb_pool_capacity", "hb_pool_stride", "hb_pool_upload",
     "hb_pool_download", "hb_pool_gather", "hb_run_gates", "hb_sync", "hb_last_timing",
     "hb_counters", "hb_debug_blind_rotate", "hb_debug_bootstrap_wo_ks", "hb_debug_keyswitch",
-    "hb_debug_fft_margin", "hb_debug_fourier",
+    "hb_debug_fft_margin", "hb_debug_fourier", "hb_flush_l2", "hb_measure_fp64_peak",
 )
 
 
@@ -87,7 +87,8 @@ def lib():
         "hb_bk_words": ([P(HbParams)], sz),
         "hb_ksk_words": ([P(HbParams)], sz),
         "hb_keygen": ([P(HbParams), ctypes.c_uint64, u32p, u32p, u32p, u32p, ctypes.c_int], ctypes.c_int),
-        "hb_encrypt": ([P(HbParams), u32p, ctypes.c_uint64, ctypes.c_uint64, P(ctypes.c_uint8), sz, u32p, sz],
+        "hb_encrypt": ([P(HbParams), u32p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, P(ctypes.c_uint8),
+                        sz, u32p, sz],
                        ctypes.c_int),
         "hb_phase": ([P(HbParams), u32p, u32p, sz, sz, P(ctypes.c_int32)], ctypes.c_int),
         "hb_decrypt": ([P(HbParams), u32p, u32p, sz, sz, P(ctypes.c_uint8)], ctypes.c_int),
@@ -108,6 +109,8 @@ def lib():
         "hb_debug_keyswitch": ([vp, u32p, sz, u32p], ctypes.c_int),
         "hb_debug_fft_margin": ([vp, P(ctypes.c_double)], ctypes.c_int),
         "hb_debug_fourier": ([vp, u32p, sz, P(ctypes.c_double), ctypes.c_int], ctypes.c_int),
+        "hb_flush_l2": ([vp, sz], ctypes.c_int),
+        "hb_measure_fp64_peak": ([vp, P(ctypes.c_double)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -1,0 +1,571 @@
+"""`TfheContext`: the reference's `GateBackend` (backend.py:116-150) on real
+CGGI/TFHE ciphertexts, executed on a B200.
+
+Drop-in contract, reproduced from `SimContext`
+(backend.py:161-257):
+
+* `encrypt`/`trivial_const` raise ValueError unless b in {0, 1} (178-186);
+* gate methods return `CipherBit` handles whose `level` follows the ASAP rule
+  (207, 235), whose `trivial_value` is set only for trivial constants, and
+  whose `.context` is this context;
+* `GateStats` counting (`_record`, 199-203), nested scopes (241-249),
+  `gate_count`/`scope_depth` (251-257) and the lock that makes concurrent gate
+  issue race-free (174, 200) are identical;
+* `ContextMismatchError` for foreign handles (194-197), `ScopeError` on scope
+  underflow; device failures raise `DeviceError` (never ValueError);
+* NOT is free unless `hebnn.backend.NOT_IS_FREE` is False (223-228); a MUX on
+  a trivial selector is free and returns the very same handle (232-234).
+
+Execution is lazy: gates append nodes to a DAG; `decrypt` (the only flush point
+of the reference API) runs every pending node on the GPU one level at a time
+(the level histogram is the batch schedule).  While building the
+DAG, gates whose result is already determined are not bootstrapped (trivial
+inputs, repeated inputs, common subexpressions, MUX with trivial data inputs);
+the counted `GateStats` are unaffected and decrypted values are identical
+(SURVEY.md §8 f2).  With ``lanes = B`` every handle carries B independent
+ciphertexts that share one DAG.
+"""
+
+from __future__ import annotations
+
+import threading
+import time
+import weakref
+
+import numpy as np
+
+from . import gate_api as api
+from ._native import GATE_DTYPE, GATE_LIN2, GATE_MUX
+from .gate_api import AND, MUX, OR, XNOR, XOR, CipherBit, ContextMismatchError, GateBackend, GateStats, ScopeError
+from .tfhe import EIGHTH, MASK32, Engine, KeySet
+
+# internal node opcodes
+_OP_CONST = 0   # node 0: the constant 0 (ref 0 = false, ref 1 = true)
+_OP_INPUT = 1   # fresh encryption
+_OP_AND = 2     # AND(ref_a, ref_b): NOT flags live in the refs
+_OP_XOR = 3     # XOR(node_a, node_b): NOT flags are pushed to the output ref
+_OP_MUX = 4     # MUX(node_s, ref_a, ref_b): selector kept positive
+
+_C_AND = (-EIGHTH) & MASK32
+_C_XOR = 2 * EIGHTH
+
+
+class DeviceError(RuntimeError):
+    """Raised when the B200 engine cannot run (no device, CUDA failure)."""
+
+
+# ---------------------------------------------------------------------------
+# shared engines and slot allocation
+# ---------------------------------------------------------------------------
+
+_KEY_CACHE = {}
+_ENGINE_CACHE = {}
+_CACHE_LOCK = threading.Lock()
+_CONTEXT_SERIAL = 0
+
+
+def shared_keys(seed):
+    """Key sets are deterministic in the seed; contexts with equal seeds share
+    one (keygen costs ~1 s on the host)."""
+    with _CACHE_LOCK:
+        ks = _KEY_CACHE.get(seed)
+        if ks is None:
+            ks = _KEY_CACHE[seed] = KeySet(seed=seed)
+        return ks
+
+
+class _SlotPool:
+    """First-fit allocator of physical pool slots on one engine."""
+
+    def __init__(self, engine):
+        self.engine = engine
+        self.top = 0
+        self.free = []  # (base, size)
+        self.lock = threading.Lock()
+
+    def alloc(self, size, align=1):
+        with self.lock:
+            for i, (b, s) in enumerate(self.free):
+                ab = -(-b // align) * align
+                if ab + size <= b + s:
+                    del self.free[i]
+                    if ab > b:
+                        self.free.append((b, ab - b))
+                    if ab + size < b + s:
+                        self.free.append((ab + size, b + s - ab - size))
+                    return ab
+            ab = -(-self.top // align) * align
+            if ab > self.top:
+                self.free.append((self.top, ab - self.top))
+            self.top = ab + size
+            if self.top > self.engine.capacity:
+                self.engine.reserve(max(self.top, int(self.engine.capacity * 1.5) + 1024))
+            return ab
+
+    def release(self, base, size):
+        with self.lock:
+            self.free.append((base, size))
+
+
+def shared_engine(keys, device):
+    key = (id(keys), device)
+    with _CACHE_LOCK:
+        ent = _ENGINE_CACHE.get(key)
+        if ent is None:
+            try:
+                eng = Engine(keys, device=device)
+            except (RuntimeError, OSError) as exc:
+                raise DeviceError(f"cannot create the B200 engine on device {device}: {exc}") from exc
+            ent = _ENGINE_CACHE[key] = (eng, _SlotPool(eng))
+        return ent
+
+
+def _release_chunks(pool, chunks):
+    for base, size in chunks:
+        pool.release(base, size)
+
+
+# ---------------------------------------------------------------------------
+# the context
+# ---------------------------------------------------------------------------
+
+
+class TfheContext(GateBackend):
+    """CGGI/TFHE gate-bootstrapping backend on a B200 (see module docstring).
+
+    Parameters
+    ----------
+    seed:     key seed (keys are deterministic in it; equal seeds share keys)
+    device:   CUDA device ordinal of the engine
+    lanes:    independent ciphertexts per handle (one DAG, B executions)
+    enc_seed: seed of the encryption randomness (defaults to ``seed``)
+    enc_stream: ChaCha stream id of this context's encryptions (defaults to a
+              per-process creation counter, so runs are reproducible)
+    keys:     an explicit `KeySet` (overrides ``seed``)
+    """
+
+    _CHUNK = 4096  # logical slots reserved at a time
+
+    def __init__(self, seed=0, device=0, lanes=1, enc_seed=None, keys=None, enc_stream=None):
+        if lanes < 1:
+            raise ValueError("lanes must be >= 1")
+        self.global_stats = GateStats(label="global")
+        self._scopes = []
+        self._lock = threading.RLock()
+        self.keys = keys if keys is not None else shared_keys(seed)
+        self.params = self.keys.params
+        self.device = device
+        self.lanes = int(lanes)
+        self.enc_seed = seed if enc_seed is None else enc_seed
+        self._enc_count = 0
+        global _CONTEXT_SERIAL
+        with _CACHE_LOCK:
+            _CONTEXT_SERIAL += 1
+            serial = _CONTEXT_SERIAL
+        self.enc_stream = (serial if enc_stream is None else int(enc_stream)) & 0xFFFFF
+        # DAG storage (parallel lists; node 0 is the constant 0)
+        self._op = [_OP_CONST]
+        self._a = [0]
+        self._b = [0]
+        self._c = [0]
+        self._lvl = [0]        # execution level (after elision)
+        self._slot = [-1]      # logical pool slot
+        self._done = [True]
+        self._cse = {}
+        self._pending = []     # node ids not yet executed
+        self._inputs = {}      # node id -> host ciphertexts [lanes][n+1] not yet uploaded
+        self._engine = None
+        self._slots = None
+        self._chunks = []
+        self._slot_next = 0
+        self._slot_end = 0
+        self._finalizer = None
+        # execution statistics
+        self.exec_stats = {"bootstraps": 0, "gates": 0, "levels": 0, "device_ms": 0.0, "flushes": 0,
+                           "flush_s": 0.0}
+
+    # -- engine / slots ------------------------------------------------------
+
+    def _ensure_engine(self):
+        if self._engine is None:
+            self._engine, self._slots = shared_engine(self.keys, self.device)
+            self._finalizer = weakref.finalize(self, _release_chunks, self._slots, self._chunks)
+        return self._engine
+
+    def _new_slot(self):
+        if self._slot_next >= self._slot_end:
+            self._ensure_engine()
+            base = self._slots.alloc(self._CHUNK * self.lanes, align=self.lanes)
+            self._chunks.append((base, self._CHUNK * self.lanes))
+            self._slot_next = base // self.lanes
+            self._slot_end = self._slot_next + self._CHUNK
+        s = self._slot_next
+        self._slot_next += 1
+        return s
+
+    # -- checks / stats (SimContext._check/_record, backend.py:194-203) --------
+
+    def _check(self, *bits):
+        for c in bits:
+            if not isinstance(c, CipherBit) or c._ctx is not self:
+                raise ContextMismatchError("bit handle does not belong to this context")
+
+    def _record(self, kind, level):
+        self.global_stats.record(kind, level)
+        for scope in self._scopes:
+            scope.record(kind, level)
+
+    # -- bit creation ----------------------------------------------------------
+
+    def _add_node(self, op, a, b, c, lvl, slot):
+        nid = len(self._op)
+        self._op.append(op)
+        self._a.append(a)
+        self._b.append(b)
+        self._c.append(c)
+        self._lvl.append(lvl)
+        self._slot.append(slot)
+        self._done.append(False)
+        return nid
+
+    def encrypt(self, b):
+        """Fresh encryption of bit b (all lanes) — SimContext.encrypt, backend.py:178-181."""
+        if b not in (0, 1):
+            raise ValueError(f"plaintext bit must be 0 or 1, got {b!r}")
+        return self.encrypt_lanes(np.full(self.lanes, int(b), np.uint8))
+
+    def encrypt_lanes(self, bits):
+        """Fresh encryption of one bit per lane (len(bits) == lanes)."""
+        bits = np.asarray(bits)
+        if bits.shape != (self.lanes,):
+            raise ValueError(f"expected {self.lanes} lane bits, got shape {bits.shape}")
+        if not np.all((bits == 0) | (bits == 1)):
+            raise ValueError("plaintext bits must be 0 or 1")
+        with self._lock:
+            idx0 = self._enc_count
+            self._enc_count += self.lanes
+            cts = self._encrypt_host(bits.astype(np.uint8), idx0)
+            slot = self._new_slot()
+            nid = self._add_node(_OP_INPUT, 0, 0, 0, 0, slot)
+            self._done[nid] = True  # value known on the host; uploaded at flush
+            self._inputs[nid] = cts
+            return CipherBit(self, nid << 1, 0)
+
+    def encrypt_many(self, bits):
+        """Vectorised encrypt: bits shape [count] (broadcast over lanes) or
+        [count, lanes]; returns a list of handles."""
+        bits = np.asarray(bits)
+        if bits.ndim == 1:
+            bits = np.repeat(bits[:, None], self.lanes, axis=1)
+        if bits.ndim != 2 or bits.shape[1] != self.lanes:
+            raise ValueError(f"expected [count, {self.lanes}] bits")
+        if not np.all((bits == 0) | (bits == 1)):
+            raise ValueError("plaintext bits must be 0 or 1")
+        count = bits.shape[0]
+        with self._lock:
+            idx0 = self._enc_count
+            self._enc_count += count * self.lanes
+            cts = self._encrypt_host(bits.reshape(-1).astype(np.uint8), idx0).reshape(count, self.lanes, -1)
+            out = []
+            for i in range(count):
+                slot = self._new_slot()
+                nid = self._add_node(_OP_INPUT, 0, 0, 0, 0, slot)
+                self._done[nid] = True
+                self._inputs[nid] = cts[i]
+                out.append(CipherBit(self, nid << 1, 0))
+            return out
+
+    def _encrypt_host(self, bits, idx0):
+        # one ChaCha stream per context; the ciphertext index continues across calls
+        return self.keys.encrypt(bits, seed=self.enc_seed, stream=self.enc_stream, first_index=idx0)
+
+    def trivial_const(self, b):
+        """SimContext.trivial_const (backend.py:183-186): public, free, level 0."""
+        if b not in (0, 1):
+            raise ValueError(f"plaintext bit must be 0 or 1, got {b!r}")
+        return CipherBit(self, int(b), 0, trivial_value=int(b))
+
+    # -- gates -------------------------------------------------------------------
+
+    def _mk_and(self, ra, rb):
+        """ref of AND(ra, rb) with constant/duplicate elision and CSE."""
+        if (ra >> 1) == 0:
+            return rb if ra & 1 else 0
+        if (rb >> 1) == 0:
+            return ra if rb & 1 else 0
+        if ra == rb:
+            return ra
+        if ra == rb ^ 1:
+            return 0
+        if ra > rb:
+            ra, rb = rb, ra
+        key = (_OP_AND, ra, rb)
+        nid = self._cse.get(key)
+        if nid is None:
+            lvl = 1 + max(self._lvl[ra >> 1], self._lvl[rb >> 1])
+            nid = self._add_node(_OP_AND, ra, rb, 0, lvl, self._new_slot())
+            self._cse[key] = nid
+            self._pending.append(nid)
+        return nid << 1
+
+    def _mk_xor(self, ra, rb):
+        neg = (ra ^ rb) & 1
+        na, nb = ra >> 1, rb >> 1
+        if na == 0:
+            return rb ^ (ra & 1)
+        if nb == 0:
+            return ra ^ (rb & 1)
+        if na == nb:
+            return neg
+        if na > nb:
+            na, nb = nb, na
+        key = (_OP_XOR, na, nb)
+        nid = self._cse.get(key)
+        if nid is None:
+            lvl = 1 + max(self._lvl[na], self._lvl[nb])
+            nid = self._add_node(_OP_XOR, na << 1, nb << 1, 0, lvl, self._new_slot())
+            self._cse[key] = nid
+            self._pending.append(nid)
+        return (nid << 1) | neg
+
+    def _mk_mux(self, rs, ra, rb):
+        if rs & 1:  # MUX(~s, a, b) = MUX(s, b, a)
+            rs, ra, rb = rs ^ 1, rb, ra
+        if (rs >> 1) == 0:  # constant selector (only after elision)
+            return ra if rs & 1 else rb
+        if ra == rb:
+            return ra
+        if (ra >> 1) == 0 and (rb >> 1) == 0:  # both constant, a != b
+            return rs if ra & 1 else rs ^ 1
+        if (ra >> 1) == 0:  # s ? 1 : b = s OR b;  s ? 0 : b = ~s AND b
+            return (self._mk_and(rs ^ 1, rb ^ 1) ^ 1) if ra & 1 else self._mk_and(rs ^ 1, rb)
+        if (rb >> 1) == 0:  # s ? a : 1 = ~s OR a;  s ? a : 0 = s AND a
+            return (self._mk_and(rs, ra ^ 1) ^ 1) if rb & 1 else self._mk_and(rs, ra)
+        if ra == rb ^ 1:  # s ? a : ~a = XNOR(s, a)
+            return self._mk_xor(rs, ra) ^ 1
+        if ra == rs:  # s ? s : b = s OR b
+            return self._mk_and(rs ^ 1, rb ^ 1) ^ 1
+        if ra == rs ^ 1:  # s ? ~s : b = ~s AND b
+            return self._mk_and(rs ^ 1, rb)
+        if rb == rs:  # s ? a : s = s AND a
+            return self._mk_and(rs, ra)
+        if rb == rs ^ 1:  # s ? a : ~s = ~s OR a
+            return self._mk_and(rs, ra ^ 1) ^ 1
+        key = (_OP_MUX, rs, ra, rb)
+        nid = self._cse.get(key)
+        if nid is None:
+            lvl = 1 + max(self._lvl[rs >> 1], self._lvl[ra >> 1], self._lvl[rb >> 1])
+            nid = self._add_node(_OP_MUX, rs, ra, rb, lvl, self._new_slot())
+            self._cse[key] = nid
+            self._pending.append(nid)
+        return nid << 1
+
+    def _binary_gate(self, kind, a, b):
+        """SimContext._binary_gate (backend.py:205-209) on real ciphertexts."""
+        self._check(a, b)
+        level = max(a.level, b.level) + 1
+        with self._lock:
+            self._record(kind, level)
+            ra, rb = a._value, b._value
+            if kind == AND:
+                r = self._mk_and(ra, rb)
+            elif kind == OR:
+                r = self._mk_and(ra ^ 1, rb ^ 1) ^ 1
+            elif kind == XOR:
+                r = self._mk_xor(ra, rb)
+            else:  # XNOR
+                r = self._mk_xor(ra, rb) ^ 1
+        return CipherBit(self, r, level)
+
+    def g_and(self, a, b):
+        return self._binary_gate(AND, a, b)
+
+    def g_or(self, a, b):
+        return self._binary_gate(OR, a, b)
+
+    def g_xor(self, a, b):
+        return self._binary_gate(XOR, a, b)
+
+    def g_xnor(self, a, b):
+        return self._binary_gate(XNOR, a, b)
+
+    def g_not(self, a):
+        """SimContext.g_not (backend.py:223-228): free sign flip."""
+        self._check(a)
+        if not api.not_is_free():
+            return self.g_xnor(a, self.trivial_const(0))
+        trivial = None if a.trivial_value is None else 1 - a.trivial_value
+        return CipherBit(self, a._value ^ 1, a.level, trivial_value=trivial)
+
+    def g_mux(self, s, a, b):
+        """SimContext.g_mux (backend.py:230-237)."""
+        self._check(s, a, b)
+        if s.trivial_value is not None:
+            return a if s.trivial_value else b
+        level = max(s.level, a.level, b.level) + 1
+        with self._lock:
+            self._record(MUX, level)
+            r = self._mk_mux(s._value, a._value, b._value)
+        return CipherBit(self, r, level)
+
+    # -- scoped stats (backend.py:241-257) --------------------------------------
+
+    def begin_scope(self, label=""):
+        with self._lock:
+            self._scopes.append(GateStats(label=label))
+
+    def end_scope(self):
+        with self._lock:
+            if not self._scopes:
+                raise ScopeError("end_scope without matching begin_scope")
+            return self._scopes.pop()
+
+    @property
+    def scope_depth(self):
+        return len(self._scopes)
+
+    @property
+    def gate_count(self):
+        return self.global_stats.total
+
+    # -- execution ------------------------------------------------------------------
+
+    def pending_count(self):
+        return len(self._pending)
+
+    def schedule(self):
+        """(level, records) batches the next flush would launch."""
+        with self._lock:
+            return self._build_schedule(self._pending)
+
+    def _build_schedule(self, pending):
+        if not pending:
+            return []
+        ids = np.asarray(pending, dtype=np.int64)
+        op = np.asarray(self._op, dtype=np.int8)[ids]
+        a = np.asarray(self._a, dtype=np.int64)[ids]
+        b = np.asarray(self._b, dtype=np.int64)[ids]
+        c = np.asarray(self._c, dtype=np.int64)[ids]
+        lvl = np.asarray(self._lvl, dtype=np.int64)[ids]
+        slot = np.asarray(self._slot, dtype=np.int64)
+        recs = np.zeros(ids.size, dtype=GATE_DTYPE)
+        recs["dst"] = slot[ids]
+        recs["src_a"] = slot[a >> 1]
+        recs["src_b"] = slot[b >> 1]
+        is_and = op == _OP_AND
+        is_xor = op == _OP_XOR
+        is_mux = op == _OP_MUX
+        sa = 1 - 2 * (a & 1)
+        sb = 1 - 2 * (b & 1)
+        recs["kind"] = np.where(is_mux, GATE_MUX, GATE_LIN2)
+        recs["c0"] = np.where(is_and, _C_AND, np.where(is_xor, _C_XOR, 0)).astype(np.uint32)
+        # AND: signs of the refs; XOR: 2, 2; MUX: S = src_a (positive), alpha/beta = signs of a / b
+        recs["alpha"] = np.where(is_and, sa, np.where(is_xor, 2, sb))
+        recs["beta"] = np.where(is_and, sb, np.where(is_xor, 2, 1 - 2 * (c & 1)))
+        recs["src_c"] = np.where(is_mux, slot[c >> 1], 0)
+        # MUX records: src_a = selector, src_b = a, src_c = b
+        recs["src_a"] = np.where(is_mux, slot[a >> 1], recs["src_a"])
+        recs["src_b"] = np.where(is_mux, slot[b >> 1], recs["src_b"])
+        order = np.argsort(lvl, kind="stable")
+        lvl_sorted = lvl[order]
+        bounds = np.flatnonzero(np.diff(lvl_sorted)) + 1
+        out = []
+        for chunk in np.split(order, bounds):
+            out.append((int(lvl[chunk[0]]), recs[chunk]))
+        return out
+
+    def flush(self):
+        """Execute every pending gate on the device (level by level)."""
+        with self._lock:
+            t0 = time.perf_counter()
+            eng = self._ensure_engine()
+            if self._inputs:
+                for nid, cts in self._inputs.items():
+                    eng.upload(self._slot[nid] * self.lanes, cts.reshape(self.lanes, -1))
+                self._inputs.clear()
+            pending = self._pending
+            if not pending:
+                return
+            batches = self._build_schedule(pending)
+            try:
+                for _lvl, recs in batches:
+                    eng.run_gates(recs, lanes=self.lanes)
+                eng.sync()
+            except RuntimeError as exc:
+                raise DeviceError(str(exc)) from exc
+            for nid in pending:
+                self._done[nid] = True
+            n_mux = sum(int(np.count_nonzero(r["kind"] == GATE_MUX)) for _, r in batches)
+            self.exec_stats["gates"] += len(pending) * self.lanes
+            self.exec_stats["bootstraps"] += (len(pending) + n_mux) * self.lanes
+            self.exec_stats["levels"] += len(batches)
+            self.exec_stats["flushes"] += 1
+            self.exec_stats["flush_s"] += time.perf_counter() - t0
+            self._pending = []
+
+    def _ciphertexts(self, refs):
+        """Host LWE samples [len(refs)][lanes][n+1] for node refs (no negation)."""
+        nodes = [r >> 1 for r in refs]
+        out = np.zeros((len(nodes), self.lanes, self.params.n + 1), np.uint32)
+        need = []
+        for i, nid in enumerate(nodes):
+            cts = self._inputs.get(nid)
+            if cts is not None:
+                out[i] = cts
+            else:
+                need.append(i)
+        if need:
+            eng = self._ensure_engine()
+            slots = np.array([self._slot[nodes[i]] for i in need], np.int64)
+            phys = (slots[:, None] * self.lanes + np.arange(self.lanes)[None, :]).reshape(-1)
+            try:
+                got = eng.gather(phys.astype(np.uint32))
+            except RuntimeError as exc:
+                raise DeviceError(str(exc)) from exc
+            out[need] = got.reshape(len(need), self.lanes, -1)
+        return out
+
+    def decrypt_lanes(self, c):
+        """Decrypt one handle in every lane -> uint8 array [lanes]."""
+        return self.decrypt_many([c])[0]
+
+    def decrypt_many(self, handles):
+        """Decrypt several handles with one device gather -> uint8 [count][lanes]."""
+        self._check(*handles)
+        with self._lock:
+            refs = [h._value for h in handles]
+            res = np.zeros((len(refs), self.lanes), np.uint8)
+            live = [i for i, r in enumerate(refs) if (r >> 1) != 0]
+            for i, r in enumerate(refs):
+                if (r >> 1) == 0:
+                    res[i] = r & 1
+            if live:
+                if any(not self._done[refs[i] >> 1] for i in live) or self._pending:
+                    self.flush()
+                cts = self._ciphertexts([refs[i] for i in live])
+                bits = self.keys.decrypt(cts.reshape(-1, cts.shape[-1])).reshape(len(live), self.lanes)
+                for j, i in enumerate(live):
+                    res[i] = bits[j] ^ (refs[i] & 1)
+            return res
+
+    def decrypt(self, c):
+        """SimContext.decrypt (backend.py:188-190): the flush point.  Returns an
+        int for lanes == 1, else a uint8 array over lanes."""
+        self._check(c)
+        out = self.decrypt_many([c])[0]
+        return int(out[0]) if self.lanes == 1 else out
+
+    def phase(self, c):
+        """Signed torus phase (int32 units of 2^-32) of a handle, per lane."""
+        self._check(c)
+        with self._lock:
+            if (c._value >> 1) == 0:
+                return None
+            if self._pending:
+                self.flush()
+            cts = self._ciphertexts([c._value])[0]
+            ph = self.keys.phase(cts).astype(np.int64)
+            return -ph if c._value & 1 else ph
+
+
+__all__ = ["TfheContext", "DeviceError", "shared_keys", "shared_engine"]

@@ -520,6 +520,21 @@ __global__ void __launch_bounds__(kKsCols) k_keyswitch(const KsArgs args) {
     }
 }
 
+// FP64 roofline probe: 8 independent DFMA chains per thread.
+__global__ void __launch_bounds__(256) k_dfma_peak(double *out, int iters, double b, double c) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) a[k] = threadIdx.x * 1e-3 + k;
+    for (int i = 0; i < iters; i++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) a[k] = fma(a[k], b, c);
+    }
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) s += a[k];
+    if (s == 1.2345) out[0] = s;
+}
+
 __global__ void k_gather(const uint32_t *__restrict__ pool, uint32_t stride, const uint32_t *__restrict__ slots,
                          uint32_t count, uint32_t words, uint32_t *__restrict__ out) {
     const uint32_t s = blockIdx.x;
@@ -569,6 +584,9 @@ struct hb_engine {
     void *h_stage = nullptr;
     size_t h_stage_cap = 0;
     unsigned long long *d_margin = nullptr;
+    void *d_flush = nullptr;
+    size_t flush_bytes = 0;
+    uint64_t flush_gen = 1;
     cudaEvent_t ev[4]{};
     uint64_t n_br = 0, n_ks = 0, n_launch = 0;
 };
@@ -723,7 +741,8 @@ int hb_engine_destroy(hb_engine *e) {
     cudaSetDevice(e->device);
     if (e->stream) cudaStreamSynchronize(e->stream);
     for (void *ptr : {(void *)e->d_W, (void *)e->d_TW, (void *)e->d_bkf, (void *)e->d_ksk, (void *)e->d_pool,
-                      (void *)e->d_big, (void *)e->d_br, (void *)e->d_ks, (void *)e->d_tmp, (void *)e->d_margin})
+                      (void *)e->d_big, (void *)e->d_br, (void *)e->d_ks, (void *)e->d_tmp, (void *)e->d_margin,
+                      e->d_flush})
         if (ptr) cudaFree(ptr);
     if (e->h_stage) cudaFreeHost(e->h_stage);
     for (auto &ev : e->ev)
@@ -960,6 +979,40 @@ int hb_debug_bootstrap_wo_ks(hb_engine *e, const uint32_t *lin, size_t count, ui
     HB_CUDA_TRY(cudaMemcpy2DAsync(out, (size_t)(kN + 1) * 4, e->d_big, kBigStride * 4, (size_t)(kN + 1) * 4, count,
                                   cudaMemcpyDeviceToHost, e->stream));
     HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return HB_OK;
+}
+
+int hb_flush_l2(hb_engine *e, size_t bytes) {
+    if (!e) return HB_EINVAL;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    if (!bytes) bytes = (size_t)256 << 20;
+    if (bytes > e->flush_bytes) {
+        if (e->d_flush) cudaFree(e->d_flush);
+        e->d_flush = nullptr;
+        HB_CUDA_TRY(cudaMalloc(&e->d_flush, bytes));
+        e->flush_bytes = bytes;
+    }
+    HB_CUDA_TRY(cudaMemsetAsync(e->d_flush, (int)(e->flush_gen++ & 0xFF), bytes, e->stream));
+    return HB_OK;
+}
+
+int hb_measure_fp64_peak(hb_engine *e, double *tflops) {
+    if (!e || !tflops) return HB_EINVAL;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    cudaDeviceProp prop;
+    HB_CUDA_TRY(cudaGetDeviceProperties(&prop, e->device));
+    double *d_out = nullptr;
+    HB_CUDA_TRY(cudaMalloc(&d_out, sizeof(double)));
+    const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 4096;
+    k_dfma_peak<<<blocks, threads, 0, e->stream>>>(d_out, iters, 0.999999, 1e-7);  // warm-up
+    HB_CUDA_TRY(cudaEventRecord(e->ev[0], e->stream));
+    for (int r = 0; r < 5; r++) k_dfma_peak<<<blocks, threads, 0, e->stream>>>(d_out, iters, 0.999999, 1e-7);
+    HB_CUDA_TRY(cudaEventRecord(e->ev[1], e->stream));
+    HB_CUDA_TRY(cudaEventSynchronize(e->ev[1]));
+    float ms = 0;
+    HB_CUDA_TRY(cudaEventElapsedTime(&ms, e->ev[0], e->ev[1]));
+    cudaFree(d_out);
+    *tflops = 5.0 * 2.0 * 8.0 * iters * (double)blocks * threads / (ms * 1e-3) / 1e12;
     return HB_OK;
 }
 

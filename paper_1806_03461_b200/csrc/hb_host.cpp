@@ -210,8 +210,9 @@ int hb_keygen(const hb_params *p, uint64_t seed, uint32_t *lwe_key, uint32_t *tr
 }
 
 int hb_encrypt(const hb_params *p, const uint32_t *lwe_key, uint64_t seed, uint64_t stream,
-               const uint8_t *bits, size_t count, uint32_t *out, size_t out_stride) {
-    if (!params_ok(p) || out_stride < (size_t)p->n + 1 || (count && (!bits || !out || !lwe_key))) {
+               uint64_t first_index, const uint8_t *bits, size_t count, uint32_t *out, size_t out_stride) {
+    if (!params_ok(p) || out_stride < (size_t)p->n + 1 || (count && (!bits || !out || !lwe_key)) ||
+        first_index + count > (1ull << 32)) {
         set_error("hb_encrypt: bad arguments");
         return HB_EINVAL;
     }
@@ -223,7 +224,7 @@ int hb_encrypt(const hb_params *p, const uint32_t *lwe_key, uint64_t seed, uint6
     }
     const int n = p->n;
     parallel_for(count, count >= 64 ? 0 : 1, [&](size_t idx) {
-        Stream r(seed, (DOM_ENC << 56) | ((stream & 0xFFFFFull) << 32) | (uint64_t)idx);
+        Stream r(seed, (DOM_ENC << 56) | ((stream & 0xFFFFFull) << 32) | (first_index + (uint64_t)idx));
         uint32_t *ct = out + idx * out_stride;
         for (int a = 0; a < n; a++) ct[a] = r.u32();
         const uint32_t mu = bits[idx] ? (1u << 29) : (0u - (1u << 29));

@@ -46,12 +46,12 @@ class KeySet:
     def lwe_words(self):
         return self.params.n + 1
 
-    def encrypt(self, bits, seed, stream=0, stride=None):
+    def encrypt(self, bits, seed, stream=0, stride=None, first_index=0):
         """Encrypt 0/1 bits -> uint32 [count][stride] LWE samples."""
         bits = np.ascontiguousarray(np.asarray(bits, dtype=np.uint8).reshape(-1))
         stride = stride or self.lwe_words
         out = np.zeros((bits.size, stride), np.uint32)
-        check(lib().hb_encrypt(ctypes.byref(self.params), u32p(self.lwe_key), int(seed), int(stream),
+        check(lib().hb_encrypt(ctypes.byref(self.params), u32p(self.lwe_key), int(seed), int(stream), int(first_index),
                                bits.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), bits.size,
                                u32p(out), stride))
         return out
@@ -139,6 +139,14 @@ class Engine:
         a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
         check(lib().hb_counters(self._e, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
         return {"blind_rotations": a.value, "key_switches": b.value, "kernel_launches": c.value}
+
+    def flush_l2(self, nbytes=0):
+        check(lib().hb_flush_l2(self._e, int(nbytes)))
+
+    def measure_fp64_peak(self):
+        v = ctypes.c_double()
+        check(lib().hb_measure_fp64_peak(self._e, ctypes.byref(v)))
+        return v.value
 
     # ---- stage entry points (parity) ----
     def debug_blind_rotate(self, lwe, mu=EIGHTH, iters=-1):

@@ -1,0 +1,83 @@
+"""TEST INFRASTRUCTURE: a plaintext stand-in for the device engine, used only
+by CPU tests to check the host-side logic of TfheContext (DAG elision, CSE,
+level schedule and the hb_gate record encoding) without a GPU.
+
+Each pool slot holds the *phase* a ciphertext would decrypt to (+-1/8 on the
+2^32 torus).  A LIN2 record is executed exactly as the kernel's gate prologue
+defines it (c0 + alpha*A + beta*B, then sign -> +-1/8); MUX as the two-
+bootstrap CGGI formula.  It is injected by subclassing in tests, never by the
+product package.
+"""
+
+import numpy as np
+
+from paper_1806_03461_b200._native import GATE_MUX
+
+EIGHTH = 1 << 29
+
+
+def _sign_to_phase(v):
+    v = v.astype(np.uint32).view(np.int32)
+    return np.where(v > 0, EIGHTH, -EIGHTH).astype(np.int64)
+
+
+class PlainEngine:
+    def __init__(self, keys):
+        self.keys = keys
+        self.pool = np.zeros(0, np.int64)
+        self.records_run = 0
+        self.levels_run = 0
+
+    @property
+    def capacity(self):
+        return self.pool.size
+
+    def reserve(self, slots):
+        if slots > self.pool.size:
+            self.pool = np.concatenate([self.pool, np.zeros(slots - self.pool.size, np.int64)])
+
+    def upload(self, first, cts):
+        ph = self.keys.phase(np.ascontiguousarray(cts, np.uint32)).astype(np.int64)
+        self.pool[first:first + len(ph)] = np.where(ph > 0, EIGHTH, -EIGHTH)
+
+    def run_gates(self, recs, lanes=1):
+        self.levels_run += 1
+        self.records_run += len(recs)
+        lane = np.arange(lanes)
+        for r in recs:
+            A = self.pool[r["src_a"] * lanes + lane]
+            B = self.pool[r["src_b"] * lanes + lane]
+            if r["kind"] == GATE_MUX:
+                C = self.pool[r["src_c"] * lanes + lane]
+                u1 = _sign_to_phase((-EIGHTH + A + int(r["alpha"]) * B) & 0xFFFFFFFF)
+                u2 = _sign_to_phase((-EIGHTH - A + int(r["beta"]) * C) & 0xFFFFFFFF)
+                out = _sign_to_phase((EIGHTH + u1 + u2) & 0xFFFFFFFF)
+            else:
+                v = (int(r["c0"]) + int(r["alpha"]) * A + int(r["beta"]) * B) & 0xFFFFFFFF
+                out = _sign_to_phase(v)
+            self.pool[r["dst"] * lanes + lane] = out
+
+    def sync(self):
+        pass
+
+    def gather(self, slots):
+        # return ciphertexts that decrypt to the stored bits: trivial samples (0, phase)
+        n = self.keys.params.n
+        out = np.zeros((len(slots), n + 1), np.uint32)
+        out[:, n] = (self.pool[np.asarray(slots, np.int64)] & 0xFFFFFFFF).astype(np.uint32)
+        return out
+
+
+def plain_context_class():
+    from paper_1806_03461_b200 import backend
+
+    class PlainTfheContext(backend.TfheContext):
+        """TfheContext whose flushes run on PlainEngine (host logic only)."""
+
+        def _ensure_engine(self):
+            if self._engine is None:
+                self._engine = PlainEngine(self.keys)
+                self._slots = backend._SlotPool(self._engine)
+            return self._engine
+
+    return PlainTfheContext

@@ -137,6 +137,123 @@ __device__ __forceinline__ void fft512(double2 (&x)[8], double2 *S0, double2 *S1
     }
 }
 
+// c_m = psi^{64 m} = e^{i pi m / 16}, m = 0..7 (compile-time constants)
+__device__ __forceinline__ double2 c16(int m) {
+    constexpr double c1 = 0.98078528040323044913, s1 = 0.19509032201612826785;
+    constexpr double c2 = 0.92387953251128675613, s2 = 0.38268343236508977173;
+    constexpr double c3 = 0.83146961230254523708, s3 = 0.55557023301960222474;
+    constexpr double r = 0.70710678118654752440;
+    switch (m) {
+        case 0: return make_double2(1.0, 0.0);
+        case 1: return make_double2(c1, s1);
+        case 2: return make_double2(c2, s2);
+        case 3: return make_double2(c3, s3);
+        case 4: return make_double2(r, r);
+        case 5: return make_double2(s3, c3);
+        case 6: return make_double2(s2, c2);
+        default: return make_double2(s1, c1);
+    }
+}
+
+// Per-thread twiddle seeds of the table-free transforms (thread t of a group):
+//   f_a0 = psi^t, step_a = psi^{4t} = W^t, step_b = W64^{t&7} = psi^{32 (t&7)},
+//   i_b0 = psi^{t>>3}, i_stepb = psi^{32 (t&7) + 8}
+struct TwSeeds {
+    double2 f_a0, step_a, step_b, i_b0, i_stepb;
+};
+
+// Forward negacyclic transform of a real polynomial given as x_m = a_j + i a_{j+512}
+// at j = t + 64 m: the twist psi^j = psi^t c_m is split into compile-time c_m
+// (applied here) and psi^t, which is merged with the pass-A twiddles
+// W^{t k2} into psi^{t (4 k2 + 1)} and generated by recurrence; pass-B
+// twiddles W64^{j0 k1} by recurrence.  No table loads.
+__device__ __forceinline__ void nega_fft_fwd(double2 (&x)[8], double2 *S0, double2 *S1, int t,
+                                             const TwSeeds &tw, int bar_id) {
+#pragma unroll
+    for (int m = 1; m < 8; m++) x[m] = cmul(x[m], c16(m));
+    dft8(x);
+    {
+        const int j0 = t & 7, j1 = t >> 3;
+        double2 w = tw.f_a0;
+#pragma unroll
+        for (int k2 = 0; k2 < 8; k2++) {
+            S0[j0 * 65 + k2 * 8 + j1] = cmul(x[rev3(k2)], w);
+            if (k2 < 7) w = cmul(w, tw.step_a);
+        }
+    }
+    group_bar(bar_id);
+    {
+        const int j0 = t & 7, k2 = t >> 3;
+#pragma unroll
+        for (int j1 = 0; j1 < 8; j1++) x[j1] = S0[j0 * 65 + k2 * 8 + j1];
+        dft8(x);
+        S1[k2 * 65 + j0] = x[0];
+        double2 w = tw.step_b;
+#pragma unroll
+        for (int k1 = 1; k1 < 8; k1++) {
+            S1[k2 * 65 + k1 * 8 + j0] = cmul(x[rev3(k1)], w);
+            if (k1 < 7) w = cmul(w, tw.step_b);
+        }
+    }
+    group_bar(bar_id);
+    {
+        const int k2 = t & 7, k1 = t >> 3;
+        double2 y[8];
+#pragma unroll
+        for (int j0 = 0; j0 < 8; j0++) y[j0] = S1[k2 * 65 + k1 * 8 + j0];
+        dft8(y);
+#pragma unroll
+        for (int k0 = 0; k0 < 8; k0++) x[k0] = y[rev3(k0)];
+    }
+}
+
+// Inverse: given evaluations P at bins t + 64 k (already scaled by 1/512 via
+// the BK), returns x_m with Re = c_j, Im = c_{j+512} at j = t + 64 m.
+// Computed as conj(FFT(conj P) * psi^j): psi^{v} of the destination thread is
+// folded into the pass-B twiddles, c_m applied after pass C.
+__device__ __forceinline__ void nega_fft_inv(double2 (&x)[8], double2 *S0, double2 *S1, int t,
+                                             const TwSeeds &tw, int bar_id) {
+#pragma unroll
+    for (int m = 0; m < 8; m++) x[m].y = -x[m].y;
+    dft8(x);
+    {
+        const int j0 = t & 7, j1 = t >> 3;
+        S0[j0 * 65 + j1] = x[0];
+        double2 w = tw.step_a;
+#pragma unroll
+        for (int k2 = 1; k2 < 8; k2++) {
+            S0[j0 * 65 + k2 * 8 + j1] = cmul(x[rev3(k2)], w);
+            if (k2 < 7) w = cmul(w, tw.step_a);
+        }
+    }
+    group_bar(bar_id);
+    {
+        const int j0 = t & 7, k2 = t >> 3;
+#pragma unroll
+        for (int j1 = 0; j1 < 8; j1++) x[j1] = S0[j0 * 65 + k2 * 8 + j1];
+        dft8(x);
+        double2 w = tw.i_b0;
+#pragma unroll
+        for (int k1 = 0; k1 < 8; k1++) {
+            S1[k2 * 65 + k1 * 8 + j0] = cmul(x[rev3(k1)], w);
+            if (k1 < 7) w = cmul(w, tw.i_stepb);
+        }
+    }
+    group_bar(bar_id);
+    {
+        const int k2 = t & 7, k1 = t >> 3;
+        double2 y[8];
+#pragma unroll
+        for (int j0 = 0; j0 < 8; j0++) y[j0] = S1[k2 * 65 + k1 * 8 + j0];
+        dft8(y);
+#pragma unroll
+        for (int k0 = 0; k0 < 8; k0++) {
+            double2 v = (k0 == 0) ? y[0] : cmul(y[rev3(k0)], c16(k0));
+            x[k0] = make_double2(v.x, -v.y);
+        }
+    }
+}
+
 // double from a small signed integer without I2F: (2^52 + 2^51 + 2^31 + d) - (2^52 + 2^51 + 2^31)
 __device__ __forceinline__ double small_int_to_double(int32_t d) {
     return __hiloint2double(0x43380000, (int)((uint32_t)d ^ 0x80000000u)) - 6755401588539392.0;
@@ -257,6 +374,7 @@ struct BrSmem {
     uint32_t acc[G][2][kN];                  // TRLWE accumulators (A, B)
     double2 xch[G][2][kXchStride];           // FFT exchange buffers
     uint16_t bar[G][kMaxLweN + 1];           // mod-switched LWE (a_0..a_{n-1}, b)
+    TwSeeds tws[64];                          // per-thread twiddle seeds
 };
 
 template <int G, bool kDebug>
@@ -272,6 +390,16 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
     // BK row ring: thread 0 is the producer.  Row `it` goes to stage it % kStages;
     // it is issued kLookahead rows ahead of its use, after every consumer warp
     // released the row that previously occupied the stage.
+    if (threadIdx.x < 64) {
+        const int tt = threadIdx.x;
+        TwSeeds ts;
+        ts.f_a0 = args.TW[tt];
+        ts.step_a = args.W[tt];
+        ts.step_b = args.W[8 * (tt & 7)];
+        ts.i_b0 = args.TW[tt >> 3];
+        ts.i_stepb = args.TW[32 * (tt & 7) + 8];
+        sm.tws[tt] = ts;
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; s++) {
             mbar_init(&sm.full[s], 1);
@@ -324,8 +452,6 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
     }
     group_bar(bar_id);
 
-    const double2 *__restrict__ TW = args.TW;
-
     double max_err = 0.0;
     int row_it = 0;
     for (int i = 0; i < iters; i++) {
@@ -355,13 +481,10 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
                 __syncwarp();
                 double2 x[8];
 #pragma unroll
-                for (int m = 0; m < 8; m++) {
-                    const double lo = small_int_to_double(gadget_digit(dlo[m], p));
-                    const double hi = small_int_to_double(gadget_digit(dhi[m], p));
-                    const double2 tw = __ldg(&TW[t + 64 * m]);
-                    x[m] = make_double2(lo * tw.x - hi * tw.y, lo * tw.y + hi * tw.x);
-                }
-                fft512(x, S0, S1, t, args.W, bar_id);
+                for (int m = 0; m < 8; m++)
+                    x[m] = make_double2(small_int_to_double(gadget_digit(dlo[m], p)),
+                                        small_int_to_double(gadget_digit(dhi[m], p)));
+                nega_fft_fwd(x, S0, S1, t, sm.tws[t], bar_id);
                 const int s = row_it % kStages;
                 mbar_wait(&sm.full[s], (row_it / kStages) & 1);
                 const double2 *bk0 = sm.bk[s];
@@ -392,17 +515,12 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
         for (int q = 0; q < 2; q++) {
             double2 x[8];
 #pragma unroll
-            for (int m = 0; m < 8; m++) {
-                const double2 v = q ? f1[m] : f0[m];
-                x[m] = make_double2(v.x, -v.y);
-            }
-            fft512(x, S0, S1, t, args.W, bar_id);
+            for (int m = 0; m < 8; m++) x[m] = q ? f1[m] : f0[m];
+            nega_fft_inv(x, S0, S1, t, sm.tws[t], bar_id);
             uint32_t *P = q ? accB : accA;
 #pragma unroll
             for (int m = 0; m < 8; m++) {
-                // z = conj(x) * conj(tw) = conj(x * tw)
-                const double2 z = cmul(x[m], __ldg(&TW[t + 64 * m]));
-                const double lo = z.x, hi = -z.y;
+                const double lo = x[m].x, hi = x[m].y;
                 if (kDebug) {
                     max_err = fmax(max_err, fabs(lo - rint(lo)));
                     max_err = fmax(max_err, fabs(hi - rint(hi)));
@@ -433,90 +551,130 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
 }
 
 // ---------------------------------------------------------------------------
-// K4: batched key switch.  CTA = GK gates x 128 output columns; every KSK row
-// loaded is applied to all GK gates of the tile.
+// K4: batched key switch.  For coefficient i the CGGI digits are the eight
+// base-4 digits of w_i = (a'_i + 2^15) >> 16.  The device KSK is laid out as a
+// lookup table per 8-column chunk, T[chunk][i][j][d][8] with T[..][0][..] = 0,
+// so one digit costs two LDS.128 (the 4 candidate rows of an (i, j) fill one
+// 128-B line: lanes with different digits hit different banks) and 8 IADDs.
+// CTA = 128 gates (one per thread) x one 8-column chunk; the chunk's 1 MiB
+// table streams through a shared-memory ring fed by cp.async.bulk, so every
+// table byte fetched from L2 serves 128 gates.
 // ---------------------------------------------------------------------------
 struct KsArgs {
     const uint32_t *big;     // [n_br_work][kBigStride]
     const KsItem *items;     // [n_items]
     uint32_t lanes;
     uint32_t n_work;         // n_items * lanes
-    const uint32_t *ksk;     // [kN][t][3][kKskStride]
+    const uint32_t *ksk;     // [kKsChunks][kN][t][4][kKsCols] lookup table
     uint32_t *pool;
     uint32_t pool_stride;
     int32_t n;
 };
 
-constexpr int kKsGates = 32;
-constexpr int kKsCols = 128;
+constexpr int kKsCols = 8;                               // output columns per chunk
+constexpr int kKsChunks = kKskStride / kKsCols;           // 80
+constexpr int kKsThreads = 128;                           // one gate per thread
+constexpr int kKsIBlock = 8;                              // coefficients per ring stage
+constexpr uint32_t kKsStageBytes = kKsIBlock * kKsT * 4 * kKsCols * 4;  // 8 KiB
+constexpr int kKsStages = 4;
+constexpr size_t kKsTableWords = (size_t)kKsChunks * kN * kKsT * 4 * kKsCols;
 
 struct KsSmem {
-    uint16_t dig[kKsGates][kN];
-    uint32_t bvals[kKsGates];
+    uint4 tab[kKsStages][kKsStageBytes / 16];
+    uint64_t full[kKsStages], empty[kKsStages];
 };
 
-__global__ void __launch_bounds__(kKsCols) k_keyswitch(const KsArgs args) {
-    extern __shared__ __align__(16) unsigned char ks_smem_raw[];
-    KsSmem &ks_sm = *reinterpret_cast<KsSmem *>(ks_smem_raw);
-    auto &dig = ks_sm.dig;
-    auto &bvals = ks_sm.bvals;
-    const int tile0 = blockIdx.x * kKsGates;
-    const int ng = min(kKsGates, (int)args.n_work - tile0);
+__global__ void __launch_bounds__(kKsThreads) k_keyswitch(const KsArgs args) {
+    __shared__ __align__(128) KsSmem ks;
+    const int lane = threadIdx.x & 31;
+    const uint32_t e = blockIdx.x * kKsThreads + threadIdx.x;
+    const bool active = e < args.n_work;
+    const uint32_t ee = active ? e : args.n_work - 1;
     const uint32_t lanes = args.lanes;
-    // digits of (a'_i + 2^15) >> 16: eight base-4 digits per coefficient
-    for (int g = 0; g < ng; g++) {
-        const uint32_t e = tile0 + g;
-        const KsItem it = args.items[e / lanes];
-        const uint32_t lane_id = e % lanes;
-        const uint32_t *b0 = args.big + ((size_t)it.i0 * lanes + lane_id) * kBigStride;
-        const uint32_t *b1 = it.i1 != 0xFFFFFFFFu ? args.big + ((size_t)it.i1 * lanes + lane_id) * kBigStride : nullptr;
-        for (int i = threadIdx.x; i < kN; i += kKsCols) {
-            uint32_t v = __ldg(&b0[i]);
-            if (b1) v += __ldg(&b1[i]);
-            dig[g][i] = (uint16_t)((v + (1u << 15)) >> 16);
+    const KsItem it = args.items[ee / lanes];
+    const uint32_t lane_id = ee % lanes;
+    const uint32_t *b0 = args.big + ((size_t)it.i0 * lanes + lane_id) * kBigStride;
+    const uint32_t *b1 = it.i1 != 0xFFFFFFFFu ? args.big + ((size_t)it.i1 * lanes + lane_id) * kBigStride : nullptr;
+    const int chunk = blockIdx.y;
+    const char *tab_src = reinterpret_cast<const char *>(args.ksk) + (size_t)chunk * kN * kKsT * 4 * kKsCols * 4;
+    constexpr int kBlocks = kN / kKsIBlock;  // 128
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kKsStages; s++) {
+            mbar_init(&ks.full[s], 1);
+            mbar_init(&ks.empty[s], kKsThreads / 32);
         }
-        if (threadIdx.x == 0) {
-            uint32_t b = b0[kN];
-            if (b1) b += b1[kN] + it.cadd;
-            bvals[g] = b;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int b = 0; b < kKsStages - 1; b++) {
+            mbar_arrive_expect_tx(&ks.full[b], kKsStageBytes);
+            bulk_g2s(ks.tab[b], tab_src + (size_t)b * kKsStageBytes, kKsStageBytes, &ks.full[b]);
         }
     }
-    for (int g = ng; g < kKsGates; g++)
-        for (int i = threadIdx.x; i < kN; i += kKsCols) dig[g][i] = 0;
     __syncthreads();
 
-    const int c = blockIdx.y * kKsCols + threadIdx.x;
-    const bool col_ok = c <= args.n;
-    const int cc = col_ok ? c : 0;
-    uint32_t acc[kKsGates];
+    uint32_t acc[kKsCols];
 #pragma unroll
-    for (int g = 0; g < kKsGates; g++) acc[g] = (c == args.n && g < ng) ? bvals[g] : 0u;
-
-    const uint32_t *ksk = args.ksk + cc;
+    for (int c = 0; c < kKsCols; c++) acc[c] = 0;
+    const uint4 *wsrc0 = reinterpret_cast<const uint4 *>(b0);
+    const uint4 *wsrc1 = reinterpret_cast<const uint4 *>(b1);
+    uint4 wa = __ldg(wsrc0), wb = __ldg(wsrc0 + 1);
+    if (b1) {
+        const uint4 xa = __ldg(wsrc1), xb = __ldg(wsrc1 + 1);
+        wa = make_uint4(wa.x + xa.x, wa.y + xa.y, wa.z + xa.z, wa.w + xa.w);
+        wb = make_uint4(wb.x + xb.x, wb.y + xb.y, wb.z + xb.z, wb.w + xb.w);
+    }
 #pragma unroll 1
-    for (int i = 0; i < kN; i++) {
-        uint32_t dg[kKsGates];
-#pragma unroll
-        for (int g = 0; g < kKsGates; g++) dg[g] = dig[g][i];
-#pragma unroll
-        for (int j = 0; j < kKsT; j++) {
-            const uint32_t *row = ksk + ((size_t)(i * kKsT + j) * kKsVals) * kKskStride;
-            const uint32_t r1 = __ldg(row), r2 = __ldg(row + kKskStride), r3 = __ldg(row + 2 * kKskStride);
-            const int sh = 14 - 2 * j;
-#pragma unroll
-            for (int g = 0; g < kKsGates; g++) {
-                const uint32_t d = (dg[g] >> sh) & 3u;
-                const uint32_t v = d == 0 ? 0u : (d == 1 ? r1 : (d == 2 ? r2 : r3));
-                acc[g] -= v;
+    for (int blk = 0; blk < kBlocks; blk++) {
+        if (threadIdx.x == 0) {
+            const int nx = blk + kKsStages - 1;
+            if (nx < kBlocks) {
+                const int s2 = nx % kKsStages;
+                if (nx >= kKsStages) mbar_wait(&ks.empty[s2], ((nx / kKsStages) - 1) & 1);
+                mbar_arrive_expect_tx(&ks.full[s2], kKsStageBytes);
+                bulk_g2s(ks.tab[s2], tab_src + (size_t)nx * kKsStageBytes, kKsStageBytes, &ks.full[s2]);
             }
         }
+        __syncwarp();
+        const uint32_t v[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+        if (blk + 1 < kBlocks) {  // prefetch the next block's coefficients
+            wa = __ldg(wsrc0 + 2 * blk + 2);
+            wb = __ldg(wsrc0 + 2 * blk + 3);
+            if (b1) {
+                const uint4 xa = __ldg(wsrc1 + 2 * blk + 2), xb = __ldg(wsrc1 + 2 * blk + 3);
+                wa = make_uint4(wa.x + xa.x, wa.y + xa.y, wa.z + xa.z, wa.w + xa.w);
+                wb = make_uint4(wb.x + xb.x, wb.y + xb.y, wb.z + xb.z, wb.w + xb.w);
+            }
+        }
+        const int s = blk % kKsStages;
+        mbar_wait(&ks.full[s], (blk / kKsStages) & 1);
+        const uint4 *tab = ks.tab[s];
+#pragma unroll
+        for (int ii = 0; ii < kKsIBlock; ii++) {
+            const uint32_t word = (v[ii] + (1u << 15)) >> 16;
+#pragma unroll
+            for (int j = 0; j < kKsT; j++) {
+                const uint32_t d = (word >> (14 - 2 * j)) & 3u;
+                const uint4 *row = tab + ((ii * kKsT + j) * 4 + d) * 2;
+                const uint4 lo = row[0], hi = row[1];
+                acc[0] += lo.x; acc[1] += lo.y; acc[2] += lo.z; acc[3] += lo.w;
+                acc[4] += hi.x; acc[5] += hi.y; acc[6] += hi.z; acc[7] += hi.w;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ks.empty[s]);
     }
-    if (!col_ok) return;
-    for (int g = 0; g < ng; g++) {
-        const uint32_t e = tile0 + g;
-        const KsItem it = args.items[e / lanes];
-        const uint32_t lane_id = e % lanes;
-        args.pool[((size_t)it.dst * lanes + lane_id) * args.pool_stride + c] = acc[g];
+    if (!active) return;
+    const int c0 = chunk * kKsCols;
+    uint32_t bval = 0;
+    if (c0 + kKsCols > args.n) {
+        bval = b0[kN];
+        if (b1) bval += b1[kN] + it.cadd;
+    }
+    uint32_t *dst = args.pool + ((size_t)it.dst * lanes + lane_id) * args.pool_stride;
+#pragma unroll
+    for (int c = 0; c < kKsCols; c++) {
+        const int col = c0 + c;
+        if (col <= args.n) dst[col] = (col == args.n ? bval : 0u) - acc[c];
     }
 }
 
@@ -543,12 +701,17 @@ __global__ void k_gather(const uint32_t *__restrict__ pool, uint32_t stride, con
     for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) out[(size_t)s * words + w] = src[w];
 }
 
-// KSK host layout [kN][t][3][n+1] -> device [kN][t][3][kKskStride]
-__global__ void k_ksk_relayout(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, int n, size_t rows) {
-    const size_t r = blockIdx.x;
-    if (r >= rows) return;
-    for (int w = threadIdx.x; w < kKskStride; w += blockDim.x)
-        out[r * kKskStride + w] = w <= n ? in[r * (size_t)(n + 1) + w] : 0u;
+// KSK host layout [kN][t][3][n+1] -> device lookup table
+// T[chunk][i][j][d][kKsCols] = KS[i][j][d] columns chunk*8 .. chunk*8+7 (d = 0 row is 0).
+__global__ void k_ksk_relayout(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, int n) {
+    const size_t ij = blockIdx.x;  // i * t + j
+    const uint32_t *src = in + ij * 3 * (size_t)(n + 1);
+    for (int w = threadIdx.x; w < kKskStride * 4; w += blockDim.x) {
+        const int d = w / kKskStride, col = w % kKskStride;
+        const uint32_t val = (d == 0 || col > n) ? 0u : src[(size_t)(d - 1) * (n + 1) + col];
+        const int chunk = col / kKsCols, cc = col % kKsCols;
+        out[(((size_t)chunk * kN * kKsT + ij) * 4 + d) * kKsCols + cc] = val;
+    }
 }
 
 constexpr int kBrGates = 4;  // bootstraps per CTA (64 threads each)
@@ -635,8 +798,8 @@ int launch_br(hb_engine *e, const BrArgs &a) {
 }
 
 int launch_ks(hb_engine *e, const KsArgs &a) {
-    dim3 grid((a.n_work + kKsGates - 1) / kKsGates, (a.n + 1 + kKsCols - 1) / kKsCols);
-    k_keyswitch<<<grid, kKsCols, sizeof(KsSmem), e->stream>>>(a);
+    const dim3 grid((a.n_work + kKsThreads - 1) / kKsThreads, kKsChunks);
+    k_keyswitch<<<grid, kKsThreads, 0, e->stream>>>(a);
     HB_CUDA_TRY(cudaGetLastError());
     e->n_launch++;
     return HB_OK;
@@ -709,7 +872,6 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
                                      (int)br_smem_bytes<kBrGates>()));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)br_smem_bytes<kBrGates>()));
-    HB_CUDA_TRY(cudaFuncSetAttribute(k_keyswitch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(KsSmem)));
 
     // BK -> Fourier
     const size_t npoly = (size_t)p->n * kRows * 2;
@@ -727,8 +889,8 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
     uint32_t *d_kin = nullptr;
     HB_CUDA_TRY(cudaMalloc(&d_kin, ksk_rows * (p->n + 1) * sizeof(uint32_t)));
     HB_CUDA_TRY(cudaMemcpy(d_kin, ksk, ksk_rows * (p->n + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    HB_CUDA_TRY(cudaMalloc(&e->d_ksk, ksk_rows * kKskStride * sizeof(uint32_t)));
-    k_ksk_relayout<<<(unsigned)ksk_rows, 128, 0, e->stream>>>(d_kin, e->d_ksk, p->n, ksk_rows);
+    HB_CUDA_TRY(cudaMalloc(&e->d_ksk, kKsTableWords * sizeof(uint32_t)));
+    k_ksk_relayout<<<(unsigned)(ksk_rows / kKsVals), 256, 0, e->stream>>>(d_kin, e->d_ksk, p->n);
     HB_CUDA_TRY(cudaGetLastError());
     HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
     cudaFree(d_kin);

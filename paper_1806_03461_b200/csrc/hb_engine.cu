@@ -254,6 +254,119 @@ __device__ __forceinline__ void nega_fft_inv(double2 (&x)[8], double2 *S0, doubl
     }
 }
 
+// NP-polynomial variants: the passes of NP independent transforms are
+// interleaved (ILP for the FP64 pipe), share one twiddle recurrence and one
+// barrier per exchange.  xch: [NP][2][kXchStride] (double-buffered exchanges).
+template <int NP>
+__device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch, int t, const TwSeeds &tw,
+                                               int bar_id) {
+#pragma unroll
+    for (int q = 0; q < NP; q++) {
+#pragma unroll
+        for (int m = 1; m < 8; m++) x[q][m] = cmul(x[q][m], c16(m));
+        dft8(x[q]);
+    }
+    {
+        const int j0 = t & 7, j1 = t >> 3;
+        double2 w = tw.f_a0;
+#pragma unroll
+        for (int k2 = 0; k2 < 8; k2++) {
+#pragma unroll
+            for (int q = 0; q < NP; q++) xch[(2 * q) * kXchStride + j0 * 65 + k2 * 8 + j1] = cmul(x[q][rev3(k2)], w);
+            if (k2 < 7) w = cmul(w, tw.step_a);
+        }
+    }
+    group_bar(bar_id);
+    {
+        const int j0 = t & 7, k2 = t >> 3;
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+#pragma unroll
+            for (int j1 = 0; j1 < 8; j1++) x[q][j1] = xch[(2 * q) * kXchStride + j0 * 65 + k2 * 8 + j1];
+            dft8(x[q]);
+            xch[(2 * q + 1) * kXchStride + k2 * 65 + j0] = x[q][0];
+        }
+        double2 w = tw.step_b;
+#pragma unroll
+        for (int k1 = 1; k1 < 8; k1++) {
+#pragma unroll
+            for (int q = 0; q < NP; q++)
+                xch[(2 * q + 1) * kXchStride + k2 * 65 + k1 * 8 + j0] = cmul(x[q][rev3(k1)], w);
+            if (k1 < 7) w = cmul(w, tw.step_b);
+        }
+    }
+    group_bar(bar_id);
+    {
+        const int k2 = t & 7, k1 = t >> 3;
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+            double2 y[8];
+#pragma unroll
+            for (int j0 = 0; j0 < 8; j0++) y[j0] = xch[(2 * q + 1) * kXchStride + k2 * 65 + k1 * 8 + j0];
+            dft8(y);
+#pragma unroll
+            for (int k0 = 0; k0 < 8; k0++) x[q][k0] = y[rev3(k0)];
+        }
+    }
+}
+
+template <int NP>
+__device__ __forceinline__ void nega_fft_inv_n(double2 (&x)[NP][8], double2 *xch, int t, const TwSeeds &tw,
+                                               int bar_id) {
+#pragma unroll
+    for (int q = 0; q < NP; q++) {
+#pragma unroll
+        for (int m = 0; m < 8; m++) x[q][m].y = -x[q][m].y;
+        dft8(x[q]);
+    }
+    {
+        const int j0 = t & 7, j1 = t >> 3;
+#pragma unroll
+        for (int q = 0; q < NP; q++) xch[(2 * q) * kXchStride + j0 * 65 + j1] = x[q][0];
+        double2 w = tw.step_a;
+#pragma unroll
+        for (int k2 = 1; k2 < 8; k2++) {
+#pragma unroll
+            for (int q = 0; q < NP; q++) xch[(2 * q) * kXchStride + j0 * 65 + k2 * 8 + j1] = cmul(x[q][rev3(k2)], w);
+            if (k2 < 7) w = cmul(w, tw.step_a);
+        }
+    }
+    group_bar(bar_id);
+    {
+        const int j0 = t & 7, k2 = t >> 3;
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+#pragma unroll
+            for (int j1 = 0; j1 < 8; j1++) x[q][j1] = xch[(2 * q) * kXchStride + j0 * 65 + k2 * 8 + j1];
+            dft8(x[q]);
+        }
+        double2 w = tw.i_b0;
+#pragma unroll
+        for (int k1 = 0; k1 < 8; k1++) {
+#pragma unroll
+            for (int q = 0; q < NP; q++)
+                xch[(2 * q + 1) * kXchStride + k2 * 65 + k1 * 8 + j0] = cmul(x[q][rev3(k1)], w);
+            if (k1 < 7) w = cmul(w, tw.i_stepb);
+        }
+    }
+    group_bar(bar_id);
+    {
+        const int k2 = t & 7, k1 = t >> 3;
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+            double2 y[8];
+#pragma unroll
+            for (int j0 = 0; j0 < 8; j0++) y[j0] = xch[(2 * q + 1) * kXchStride + k2 * 65 + k1 * 8 + j0];
+            dft8(y);
+#pragma unroll
+            for (int k0 = 0; k0 < 8; k0++) {
+                double2 v = (k0 == 0) ? y[0] : cmul(y[rev3(k0)], c16(k0));
+                x[q][k0] = make_double2(v.x, -v.y);
+            }
+        }
+    }
+}
+
 // double from a small signed integer without I2F: (2^52 + 2^51 + 2^31 + d) - (2^52 + 2^51 + 2^31)
 __device__ __forceinline__ double small_int_to_double(int32_t d) {
     return __hiloint2double(0x43380000, (int)((uint32_t)d ^ 0x80000000u)) - 6755401588539392.0;
@@ -363,8 +476,7 @@ struct BrArgs {
     unsigned long long *margin;  // if set: max |v - round(v)| as double bits
 };
 
-constexpr int kStages = 4;
-constexpr int kLookahead = 2;
+constexpr int kStages = 3;  // BK rows in the shared-memory ring
 constexpr uint32_t kRowBytes = 2 * kNH * sizeof(double2);  // 16 KiB: one TGSW row, both output polys
 
 template <int G>
@@ -372,7 +484,7 @@ struct BrSmem {
     double2 bk[kStages][2 * kNH];           // BK row ring
     uint64_t full[kStages], empty[kStages];
     uint32_t acc[G][2][kN];                  // TRLWE accumulators (A, B)
-    double2 xch[G][2][kXchStride];           // FFT exchange buffers
+    double2 xch[G][2][2][kXchStride];        // FFT exchange buffers: [poly pair][double buffer]
     uint16_t bar[G][kMaxLweN + 1];           // mod-switched LWE (a_0..a_{n-1}, b)
     TwSeeds tws[64];                          // per-thread twiddle seeds
 };
@@ -406,7 +518,7 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
             mbar_init(&sm.empty[s], 2 * G);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int it = 0; it < kLookahead && it < rows_needed; it++) {
+        for (int it = 0; it < kStages && it < rows_needed; it++) {
             mbar_arrive_expect_tx(&sm.full[it], kRowBytes);
             bulk_g2s(sm.bk[it], bk_src + (size_t)it * kRowBytes, kRowBytes, &sm.full[it]);
         }
@@ -422,8 +534,7 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
     const uint32_t e = active ? e_raw : args.n_work - 1;
     uint32_t *accA = sm.acc[g][0];
     uint32_t *accB = sm.acc[g][1];
-    double2 *S0 = sm.xch[g][0];
-    double2 *S1 = sm.xch[g][1];
+    double2 *xch = &sm.xch[g][0][0][0];
     uint16_t *bar = sm.bar[g];
 
     // K1: linear combination of the gate inputs + modulus switch to Z_2N
@@ -453,81 +564,101 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
     group_bar(bar_id);
 
     double max_err = 0.0;
-    int row_it = 0;
+    int row_it = 0;  // global BK row counter (i * 6 + row)
     for (int i = 0; i < iters; i++) {
         const int a = bar[i];
-        double2 f0[8], f1[8];  // Fourier accumulators of the two output polys
-#pragma unroll 1
+        // rotation differences (X^a - 1) ACC for both polynomials
+        uint32_t dlo[2][8], dhi[2][8];
+#pragma unroll
         for (int q = 0; q < 2; q++) {
             const uint32_t *P = q ? accB : accA;
-            uint32_t dlo[8], dhi[8];
 #pragma unroll
             for (int m = 0; m < 8; m++) {
                 const int j = t + 64 * m;
-                dlo[m] = rot_coef(P, j, a) - P[j];
-                dhi[m] = rot_coef(P, j + kNH, a) - P[j + kNH];
+                dlo[q][m] = rot_coef(P, j, a) - P[j];
+                dhi[q][m] = rot_coef(P, j + kNH, a) - P[j + kNH];
             }
+        }
+        double2 f0[8], f1[8];  // Fourier accumulators of the two output polys
 #pragma unroll 1
-            for (int p = 0; p < kL; p++, row_it++) {
-                if (threadIdx.x == 0) {
-                    const int nx = row_it + kLookahead;
-                    if (nx < rows_needed) {
-                        const int s2 = nx % kStages;
-                        if (nx >= kStages) mbar_wait(&sm.empty[s2], ((nx / kStages) - 1) & 1);
-                        mbar_arrive_expect_tx(&sm.full[s2], kRowBytes);
-                        bulk_g2s(sm.bk[s2], bk_src + (size_t)nx * kRowBytes, kRowBytes, &sm.full[s2]);
-                    }
+        for (int pr = 0; pr < kRows / 2; pr++, row_it += 2) {
+            // producer: rows row_it+1 and row_it+2 (stages freed by rows row_it-2, row_it-1)
+            if (threadIdx.x == 0) {
+#pragma unroll 1
+                for (int nx = row_it + 1; nx <= row_it + 2; nx++) {
+                    if (nx < kStages || nx >= rows_needed) continue;
+                    const int s2 = nx % kStages;
+                    mbar_wait(&sm.empty[s2], ((nx / kStages) - 1) & 1);
+                    mbar_arrive_expect_tx(&sm.full[s2], kRowBytes);
+                    bulk_g2s(sm.bk[s2], bk_src + (size_t)nx * kRowBytes, kRowBytes, &sm.full[s2]);
                 }
-                __syncwarp();
-                double2 x[8];
+            }
+            __syncwarp();
+            double2 x[2][8];
 #pragma unroll
-                for (int m = 0; m < 8; m++)
-                    x[m] = make_double2(small_int_to_double(gadget_digit(dlo[m], p)),
-                                        small_int_to_double(gadget_digit(dhi[m], p)));
-                nega_fft_fwd(x, S0, S1, t, sm.tws[t], bar_id);
-                const int s = row_it % kStages;
-                mbar_wait(&sm.full[s], (row_it / kStages) & 1);
+            for (int h = 0; h < 2; h++) {
+                const int row = 2 * pr + h;
+                const int q = row / kL, p = row % kL;
+#pragma unroll
+                for (int m = 0; m < 8; m++) {
+                    const uint32_t lo = q ? dlo[1][m] : dlo[0][m];
+                    const uint32_t hi = q ? dhi[1][m] : dhi[0][m];
+                    x[h][m] = make_double2(small_int_to_double(gadget_digit(lo, p)),
+                                           small_int_to_double(gadget_digit(hi, p)));
+                }
+            }
+            nega_fft_fwd_n<2>(x, xch, t, sm.tws[t], bar_id);
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int rr = row_it + h;
+                const int s = rr % kStages;
+                mbar_wait(&sm.full[s], (rr / kStages) & 1);
                 const double2 *bk0 = sm.bk[s];
                 const double2 *bk1 = sm.bk[s] + kNH;
                 if (kDebug && args.margin == nullptr && args.acc_dump != nullptr && args.n_work == 2) {
-                    bk0 = args.bkf + (size_t)row_it * 2 * kNH;  // bypass the ring (debug A/B)
+                    bk0 = args.bkf + (size_t)rr * 2 * kNH;  // bypass the ring (debug A/B)
                     bk1 = bk0 + kNH;
                 }
-                if (q == 0 && p == 0) {
+                if (pr == 0 && h == 0) {
 #pragma unroll
                     for (int m = 0; m < 8; m++) {
-                        f0[m] = cmul(x[m], bk0[t + 64 * m]);
-                        f1[m] = cmul(x[m], bk1[t + 64 * m]);
+                        f0[m] = cmul(x[h][m], bk0[t + 64 * m]);
+                        f1[m] = cmul(x[h][m], bk1[t + 64 * m]);
                     }
                 } else {
 #pragma unroll
                     for (int m = 0; m < 8; m++) {
-                        cmac(f0[m], x[m], bk0[t + 64 * m]);
-                        cmac(f1[m], x[m], bk1[t + 64 * m]);
+                        cmac(f0[m], x[h][m], bk0[t + 64 * m]);
+                        cmac(f1[m], x[h][m], bk1[t + 64 * m]);
                     }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&sm.empty[s]);
             }
         }
-        // inverse transforms (conjugate trick) + untwist + round + ACC update
-#pragma unroll 1
-        for (int q = 0; q < 2; q++) {
-            double2 x[8];
-#pragma unroll
-            for (int m = 0; m < 8; m++) x[m] = q ? f1[m] : f0[m];
-            nega_fft_inv(x, S0, S1, t, sm.tws[t], bar_id);
-            uint32_t *P = q ? accB : accA;
+        // inverse transforms of both output polynomials + round + ACC update
+        {
+            double2 x[2][8];
 #pragma unroll
             for (int m = 0; m < 8; m++) {
-                const double lo = x[m].x, hi = x[m].y;
-                if (kDebug) {
-                    max_err = fmax(max_err, fabs(lo - rint(lo)));
-                    max_err = fmax(max_err, fabs(hi - rint(hi)));
+                x[0][m] = f0[m];
+                x[1][m] = f1[m];
+            }
+            nega_fft_inv_n<2>(x, xch, t, sm.tws[t], bar_id);
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
+                uint32_t *P = q ? accB : accA;
+#pragma unroll
+                for (int m = 0; m < 8; m++) {
+                    const double lo = x[q][m].x, hi = x[q][m].y;
+                    if (kDebug) {
+                        max_err = fmax(max_err, fabs(lo - rint(lo)));
+                        max_err = fmax(max_err, fabs(hi - rint(hi)));
+                    }
+                    const int j = t + 64 * m;
+                    P[j] += round_to_torus(lo);
+                    P[j + kNH] += round_to_torus(hi);
                 }
-                const int j = t + 64 * m;
-                P[j] += round_to_torus(lo);
-                P[j + kNH] += round_to_torus(hi);
             }
         }
         group_bar(bar_id);

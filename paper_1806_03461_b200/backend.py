@@ -178,7 +178,6 @@ class TfheContext(GateBackend):
         self._slots = None
         self._chunks = []
         self._slot_next = 0
-        self._slot_end = 0
         self._finalizer = None
         # execution statistics
         self.exec_stats = {"bootstraps": 0, "gates": 0, "levels": 0, "device_ms": 0.0, "flushes": 0,
@@ -193,15 +192,23 @@ class TfheContext(GateBackend):
         return self._engine
 
     def _new_slot(self):
-        if self._slot_next >= self._slot_end:
-            self._ensure_engine()
-            base = self._slots.alloc(self._CHUNK * self.lanes, align=self.lanes)
-            self._chunks.append((base, self._CHUNK * self.lanes))
-            self._slot_next = base // self.lanes
-            self._slot_end = self._slot_next + self._CHUNK
+        """Next logical ciphertext slot of this context (no device needed)."""
         s = self._slot_next
         self._slot_next += 1
         return s
+
+    def _map_slots(self, logical):
+        """Logical slots -> engine record slots (chunks of the shared pool are
+        reserved on demand, aligned to `lanes` so slot * lanes + lane is the
+        physical pool index)."""
+        self._ensure_engine()
+        need = self._slot_next // self._CHUNK + 1
+        while len(self._chunks) < need:
+            base = self._slots.alloc(self._CHUNK * self.lanes, align=self.lanes)
+            self._chunks.append((base, self._CHUNK * self.lanes))
+        bases = np.array([b // self.lanes for b, _ in self._chunks], dtype=np.int64)
+        logical = np.asarray(logical, dtype=np.int64)
+        return bases[logical // self._CHUNK] + logical % self._CHUNK
 
     # -- checks / stats (SimContext._check/_record, backend.py:194-203) --------
 
@@ -448,6 +455,8 @@ class TfheContext(GateBackend):
         c = np.asarray(self._c, dtype=np.int64)[ids]
         lvl = np.asarray(self._lvl, dtype=np.int64)[ids]
         slot = np.asarray(self._slot, dtype=np.int64)
+        live = slot >= 0
+        slot[live] = self._map_slots(slot[live])
         recs = np.zeros(ids.size, dtype=GATE_DTYPE)
         recs["dst"] = slot[ids]
         recs["src_a"] = slot[a >> 1]
@@ -480,8 +489,10 @@ class TfheContext(GateBackend):
             t0 = time.perf_counter()
             eng = self._ensure_engine()
             if self._inputs:
-                for nid, cts in self._inputs.items():
-                    eng.upload(self._slot[nid] * self.lanes, cts.reshape(self.lanes, -1))
+                nids = list(self._inputs)
+                phys = self._map_slots([self._slot[nid] for nid in nids])
+                for nid, ps in zip(nids, phys):
+                    eng.upload(int(ps) * self.lanes, self._inputs[nid].reshape(self.lanes, -1))
                 self._inputs.clear()
             pending = self._pending
             if not pending:
@@ -516,7 +527,7 @@ class TfheContext(GateBackend):
                 need.append(i)
         if need:
             eng = self._ensure_engine()
-            slots = np.array([self._slot[nodes[i]] for i in need], np.int64)
+            slots = self._map_slots([self._slot[nodes[i]] for i in need])
             phys = (slots[:, None] * self.lanes + np.arange(self.lanes)[None, :]).reshape(-1)
             try:
                 got = eng.gather(phys.astype(np.uint32))

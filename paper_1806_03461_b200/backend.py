@@ -282,6 +282,42 @@ class TfheContext(GateBackend):
                 out.append(CipherBit(self, nid << 1, 0))
             return out
 
+    def import_ciphertexts(self, cts):
+        """Wrap existing LWE samples (e.g. all-gathered from other ranks) as
+        level-0 handles: cts [count][lanes][n+1] (or [count][n+1] for lanes == 1)."""
+        cts = np.asarray(cts, dtype=np.uint32)
+        if cts.ndim == 2:
+            cts = cts[:, None, :]
+        if cts.shape[1:] != (self.lanes, self.params.n + 1):
+            raise ValueError(f"expected [count, {self.lanes}, {self.params.n + 1}] ciphertexts, got {cts.shape}")
+        with self._lock:
+            out = []
+            for i in range(cts.shape[0]):
+                nid = self._add_node(_OP_INPUT, 0, 0, 0, 0, self._new_slot())
+                self._done[nid] = True
+                self._inputs[nid] = np.ascontiguousarray(cts[i])
+                out.append(CipherBit(self, nid << 1, 0))
+            return out
+
+    def export_ciphertexts(self, handles):
+        """LWE samples of handles -> [count][lanes][n+1] (NOT flags applied;
+        constants become noiseless trivial samples)."""
+        self._check(*handles)
+        with self._lock:
+            if self._pending:
+                self.flush()
+            refs = [h._value for h in handles]
+            out = np.zeros((len(refs), self.lanes, self.params.n + 1), np.uint32)
+            live = [i for i, r in enumerate(refs) if (r >> 1) != 0]
+            if live:
+                out[live] = self._ciphertexts([refs[i] for i in live])
+            for i, r in enumerate(refs):
+                if (r >> 1) == 0:
+                    out[i, :, -1] = EIGHTH if r & 1 else (-EIGHTH) & MASK32
+                elif r & 1:
+                    out[i] = (0 - out[i].astype(np.int64)).astype(np.uint32)
+            return out
+
     def _encrypt_host(self, bits, idx0):
         # one ChaCha stream per context; the ciphertext index continues across calls
         return self.keys.encrypt(bits, seed=self.enc_seed, stream=self.enc_stream, first_index=idx0)

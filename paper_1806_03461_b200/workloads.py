@@ -1,0 +1,107 @@
+"""Seeded synthetic workloads of BASELINE.json configs 2-5 (encrypted BNNs).
+
+MNIST and the tabular datasets are not in the container; inputs are synthetic
+with the shapes and distributions BASELINE.json states (Bernoulli(0.5) bits;
+uniform 8-bit feature values), weights uniform +-1 (or ternary with a
+Bernoulli(0.8) zero mask for cfg4), biases 0, all from `random.Random(seed)`.
+"""
+
+from __future__ import annotations
+
+import random
+import time
+
+import numpy as np
+
+from hebnn.compiler import EvalOptions, eval_model
+from hebnn.model import DenseLayer, SignActivation, TernaryModel, oracle_eval, validate_model
+
+
+def _dense(rng, d, p, zero_prob=0.0):
+    rows = []
+    for _ in range(p):
+        row = []
+        for _ in range(d):
+            w = rng.choice((-1, 1))
+            if zero_prob and rng.random() < zero_prob:
+                w = 0
+            row.append(w)
+        rows.append(tuple(row))
+    return DenseLayer(tuple(rows), (0,) * p)
+
+
+def build(config, seed=0):
+    """Returns (model, batch) for config in {cfg2n, cfg2l, cfg3, cfg4, cfg5}."""
+    rng = random.Random(seed)
+    if config == "cfg2n":
+        return validate_model(TernaryModel(784, (_dense(rng, 784, 1), SignActivation()), "sign_bits")), 1
+    if config == "cfg2l":
+        return validate_model(TernaryModel(784, (_dense(rng, 784, 256), SignActivation()), "sign_bits")), 1
+    if config in ("cfg3", "cfg4"):
+        z = 0.8 if config == "cfg4" else 0.0
+        layers = (_dense(rng, 784, 256, z), SignActivation(), _dense(rng, 256, 256, z), SignActivation(),
+                  _dense(rng, 256, 10, z))
+        return validate_model(TernaryModel(784, layers, "score_words")), 8
+    if config == "cfg5":
+        layers = (_dense(rng, 240, 128), SignActivation(), _dense(rng, 128, 64), SignActivation(), _dense(rng, 64, 2))
+        return validate_model(TernaryModel(240, layers, "score_words")), 64
+    raise ValueError(f"unknown config {config!r}")
+
+
+def inputs(config, model, batch, seed=1):
+    """[batch][d] bits in {0,1} (stored-binary encoding of +-1 inputs)."""
+    rng = np.random.default_rng(seed)
+    d = model.input_shape
+    if config == "cfg5":
+        vals = rng.integers(0, 256, (batch, 30))  # 30 features quantised to 8 bits
+        return ((vals[:, :, None] >> np.arange(8)[None, None, :]) & 1).reshape(batch, d).astype(np.uint8)
+    return rng.integers(0, 2, (batch, d)).astype(np.uint8)
+
+
+def decode_outputs(ctx, outs):
+    """Decrypt eval_model outputs for every lane: sign bits -> +-1, words -> ints.
+    Returns [lanes][units]."""
+    if outs and hasattr(outs[0], "bits"):
+        cols = []
+        for w in outs:
+            bits = ctx.decrypt_many(w.bits)  # [width][lanes]
+            width = len(w.bits)
+            v = (bits.astype(np.int64) << np.arange(width)[:, None]).sum(axis=0)
+            if w.signed:
+                v = np.where(v >= 1 << (width - 1), v - (1 << width), v)
+            cols.append(v)
+        return np.stack(cols, axis=1)
+    bits = ctx.decrypt_many(outs)  # [units][lanes]
+    return np.where(bits.T == 1, 1, -1)
+
+
+def run_encrypted(ctx_cls, config, seed=0, device=0, options=EvalOptions(), check=True):
+    """Encrypt a batch, evaluate through the reference compiler on a
+    lane-batched context, decrypt, compare with oracle_eval.  Returns a report."""
+    model, batch = build(config, seed)
+    X = inputs(config, model, batch, seed + 1)
+    ctx = ctx_cls(seed=seed, device=device, lanes=batch)
+    t0 = time.perf_counter()
+    xb = ctx.encrypt_many(X.T)
+    t1 = time.perf_counter()
+    outs, _ = eval_model(ctx, model, xb, options)
+    t2 = time.perf_counter()
+    ctx.flush()
+    t3 = time.perf_counter()
+    got = decode_outputs(ctx, outs)
+    t4 = time.perf_counter()
+    ok = None
+    if check:
+        ok = all(list(got[b]) == oracle_eval(model, [1 if v else -1 for v in X[b]]) for b in range(batch))
+    counted = ctx.gate_count * batch
+    return {
+        "config": config, "batch": batch, "counted_gates": counted,
+        "counted_gates_per_input": ctx.gate_count,
+        "executed_bootstraps": ctx.exec_stats["bootstraps"], "levels": ctx.exec_stats["levels"],
+        "depth": ctx.global_stats.max_level,
+        "encrypt_s": t1 - t0, "dag_build_s": t2 - t1, "device_flush_s": t3 - t2, "decrypt_s": t4 - t3,
+        "latency_s": t3 - t2 + (t4 - t3),
+        "bootstraps_per_s": ctx.exec_stats["bootstraps"] / (t3 - t2),
+        "counted_gates_per_s": counted / (t3 - t2),
+        "matches_oracle_eval": ok,
+    }

@@ -1,0 +1,14 @@
+"""Encrypted-BNN latency for BASELINE.json configs 2-5 on one B200 (through
+the reference compiler on TfheContext).  Usage: python scripts/bench_bnn.py cfg2n cfg2l cfg3 ..."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "baseline", "_ref")]
+from paper_1806_03461_b200 import workloads  # noqa: E402
+from paper_1806_03461_b200.backend import TfheContext  # noqa: E402
+
+for cfg in sys.argv[1:] or ["cfg2n"]:
+    rep = workloads.run_encrypted(TfheContext, cfg)
+    print(json.dumps(rep), flush=True)

@@ -59,8 +59,8 @@ def parse_args():
     ap.add_argument("--gates", type=int, default=4096)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--bnn", choices=("none", "neuron", "layer"), default="neuron",
-                    help="extra encrypted-BNN latency measurement (cfg2) on rank 0")
+    ap.add_argument("--bnn", choices=("none", "neuron", "layer", "cfg3", "cfg4", "cfg5"), default="neuron",
+                    help="extra encrypted-BNN latency measurement (BASELINE configs 2-5) on rank 0")
     return ap.parse_args()
 
 
@@ -232,36 +232,18 @@ def run_reference(args, dist):
 # our arm
 # ---------------------------------------------------------------------------
 
-def bnn_neuron_latency(kind, seed):
-    """cfg2: one 784->1 neuron (or the 784->256 layer) through the reference
-    compiler on TfheContext; latency of the encrypted evaluation."""
-    import random
-
-    from hebnn.compiler import EvalOptions, decrypt_output, encrypt_input, eval_model
-    from hebnn.model import DenseLayer, SignActivation, TernaryModel, oracle_eval, validate_model
-
+def bnn_latency(kind, seed):
+    """BASELINE configs 2-5 through the reference compiler on TfheContext
+    (engine created and warmed before the timed flush)."""
+    from paper_1806_03461_b200 import workloads
     from paper_1806_03461_b200.backend import TfheContext
 
-    rng = random.Random(seed)
-    p = 1 if kind == "neuron" else 256
-    rows = tuple(tuple(rng.choice((-1, 1)) for _ in range(784)) for _ in range(p))
-    model = validate_model(TernaryModel(784, (DenseLayer(rows, (0,) * p), SignActivation()), "sign_bits"))
-    xs = [rng.choice((-1, 1)) for _ in range(784)]
-    ctx = TfheContext(seed=seed)
-    xb = encrypt_input(ctx, xs)
-    t0 = time.perf_counter()
-    outs, _ = eval_model(ctx, model, xb, EvalOptions())
-    t_dag = time.perf_counter() - t0
-    t1 = time.perf_counter()
-    ctx.flush()
-    t_dev = time.perf_counter() - t1
-    got = decrypt_output(ctx, outs)
-    return {
-        "config": f"cfg2 {'784->1 neuron' if p == 1 else '784->256 layer'}, plus_one on, reduce comparator",
-        "latency_s": t_dev, "dag_build_s": t_dag, "counted_gates": ctx.gate_count,
-        "executed_bootstraps": ctx.exec_stats["bootstraps"], "levels": ctx.exec_stats["levels"],
-        "counted_gates_per_s": ctx.gate_count / t_dev, "matches_oracle_eval": got == oracle_eval(model, xs),
-    }
+    cfg = {"neuron": "cfg2n", "layer": "cfg2l"}.get(kind, kind)
+    warm = TfheContext(seed=seed)
+    warm.decrypt(warm.g_and(warm.encrypt(1), warm.encrypt(1)))  # CUDA context, BK FFT, KSK upload
+    rep = workloads.run_encrypted(TfheContext, cfg, seed=seed)
+    rep["note"] = "latency_s = device flush + decrypt of one batch; DAG build reported separately"
+    return rep
 
 
 def run_ours(args, dist):
@@ -357,7 +339,7 @@ def run_ours(args, dist):
     }
     if dist.rank == 0 and args.bnn != "none":
         try:
-            line["bnn"] = bnn_neuron_latency(args.bnn, args.seed)
+            line["bnn"] = bnn_latency(args.bnn, args.seed)
         except Exception as exc:  # report, never hide
             line["bnn"] = {"error": repr(exc)}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:

@@ -246,6 +246,22 @@ def bnn_latency(kind, seed):
     return rep
 
 
+def last_profiled_traffic(kernel="k_blind_rotate"):
+    """DRAM bytes per launch of `kernel` from the newest profiles/*/traffic.json
+    (written by scripts/ncu_summary.py from an `ncu --set full` capture)."""
+    base = os.path.join(ROOT, "profiles")
+    best = None
+    for d in sorted(os.listdir(base)) if os.path.isdir(base) else []:
+        f = os.path.join(base, d, "traffic.json")
+        if os.path.exists(f):
+            best = f
+    if not best:
+        return None, None
+    with open(best) as fh:
+        data = json.load(fh)
+    return data.get("dram_bytes_per_launch", {}).get(kernel), os.path.relpath(os.path.dirname(best), ROOT)
+
+
 def run_ours(args, dist):
     import torch
 
@@ -319,6 +335,7 @@ def run_ours(args, dist):
 
     br_med = statistics.median(br_ms)
     achieved = n * F_BS / (br_med / 1e3) / 1e12
+    traffic, traffic_src = last_profiled_traffic()
     line = {
         "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": dist.world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dist.max(statistics.mean(step_ms)), "higher_is_better": True,
@@ -330,7 +347,7 @@ def run_ours(args, dist):
                 "d2h_bytes_per_step": int(h_out.nbytes)},
         "gpu_launches": int(launches),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                     "frac": achieved / fp64_peak, "traffic": None,
+                     "frac": achieved / fp64_peak, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": "k_blind_rotate", "flops_per_bootstrap": F_BS,
                      "peak_source": "DFMA micro-benchmark in this run (MEASURED_PEAKS.json has no FP64 figure)"},
         "kernel_ms": {"blind_rotate": br_med, "key_switch": statistics.median(ks_ms)},

@@ -108,7 +108,7 @@ class _SlotPool:
 
 
 def shared_engine(keys, device):
-    key = (id(keys), device)
+    key = (id(keys.bk), device)
     with _CACHE_LOCK:
         ent = _ENGINE_CACHE.get(key)
         if ent is None:

@@ -30,17 +30,33 @@ class KeySet:
     """Secret keys (LWE, TRLWE) and public evaluation keys (BK, KSK) derived
     deterministically from ``seed`` (ChaCha20 streams)."""
 
-    def __init__(self, seed=0, params=None, threads=0):
+    def __init__(self, seed=0, params=None, threads=0, _arrays=None):
         self.params = params or default_params()
-        self.seed = int(seed)
+        self.seed = int(seed) if seed is not None else None
         p = self.params
         L = lib()
+        if _arrays is not None:  # deserialised (wire_keys.load_keys); secret part may be absent
+            self.lwe_key, self.trlwe_key, self.bk, self.ksk = _arrays
+            return
         self.lwe_key = np.zeros(p.n, np.uint32)
         self.trlwe_key = np.zeros(p.k * p.N, np.uint32)
         self.bk = np.zeros(L.hb_bk_words(ctypes.byref(p)), np.uint32)
         self.ksk = np.zeros(L.hb_ksk_words(ctypes.byref(p)), np.uint32)
         check(L.hb_keygen(ctypes.byref(p), self.seed, u32p(self.lwe_key), u32p(self.trlwe_key),
                           u32p(self.bk), u32p(self.ksk), threads))
+
+    @property
+    def has_secret(self):
+        return self.lwe_key is not None
+
+    def public(self):
+        """Evaluation keys only (what a server receives): BK + KSK, no secret."""
+        return KeySet(seed=None, params=self.params, _arrays=(None, None, self.bk, self.ksk))
+
+    def _secret(self):
+        if self.lwe_key is None:
+            raise PermissionError("this KeySet holds evaluation keys only (no secret key)")
+        return self.lwe_key
 
     @property
     def lwe_words(self):
@@ -51,7 +67,7 @@ class KeySet:
         bits = np.ascontiguousarray(np.asarray(bits, dtype=np.uint8).reshape(-1))
         stride = stride or self.lwe_words
         out = np.zeros((bits.size, stride), np.uint32)
-        check(lib().hb_encrypt(ctypes.byref(self.params), u32p(self.lwe_key), int(seed), int(stream), int(first_index),
+        check(lib().hb_encrypt(ctypes.byref(self.params), u32p(self._secret()), int(seed), int(stream), int(first_index),
                                bits.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), bits.size,
                                u32p(out), stride))
         return out
@@ -60,7 +76,7 @@ class KeySet:
         cts = np.ascontiguousarray(cts, dtype=np.uint32)
         cts2 = cts.reshape(-1, cts.shape[-1])
         out = np.zeros(cts2.shape[0], np.int32)
-        check(lib().hb_phase(ctypes.byref(self.params), u32p(self.lwe_key), u32p(cts2), cts2.shape[0],
+        check(lib().hb_phase(ctypes.byref(self.params), u32p(self._secret()), u32p(cts2), cts2.shape[0],
                              cts2.shape[1], out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
         return out.reshape(cts.shape[:-1])
 
@@ -68,7 +84,7 @@ class KeySet:
         cts = np.ascontiguousarray(cts, dtype=np.uint32)
         cts2 = cts.reshape(-1, cts.shape[-1])
         out = np.zeros(cts2.shape[0], np.uint8)
-        check(lib().hb_decrypt(ctypes.byref(self.params), u32p(self.lwe_key), u32p(cts2), cts2.shape[0],
+        check(lib().hb_decrypt(ctypes.byref(self.params), u32p(self._secret()), u32p(cts2), cts2.shape[0],
                                cts2.shape[1], out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))))
         return out.reshape(cts.shape[:-1])
 

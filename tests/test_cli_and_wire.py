@@ -1,0 +1,56 @@
+"""CLI backend hook (f3) and key/ciphertext documents (f4) — host side."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_1806_03461_b200 import cli, wire_keys
+from paper_1806_03461_b200.tfhe import KeySet
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+MODEL = os.path.join(HERE, "golden", "cancer_model.json")
+
+
+def test_cli_sim_backend_matches_reference_cli(tmp_path, capsys):
+    inp = tmp_path / "x.json"
+    inp.write_text(json.dumps({"version": 1, "encoding": "pm1", "values": [1, -1] * 45}))
+    from hebnn import cli as ref_cli
+
+    assert ref_cli.main(["eval", "--model", MODEL, "--input", str(inp)]) == 0
+    want = json.loads(capsys.readouterr().out)
+    assert cli.main(["--backend", "sim", "eval", "--model", MODEL, "--input", str(inp)]) == 0
+    got = json.loads(capsys.readouterr().out)
+    assert got == want
+
+
+def test_cli_error_exit_code_preserved(tmp_path, capsys):
+    assert cli.main(["--backend", "sim", "eval", "--model", str(tmp_path / "missing.json"),
+                     "--input", str(tmp_path / "x.json")]) in (1, 2)
+
+
+def test_key_and_ciphertext_documents_roundtrip(tmp_path, keys):
+    p = tmp_path / "eval_keys.npz"
+    wire_keys.save_keys(p, keys)
+    server = wire_keys.load_keys(p)
+    assert not server.has_secret
+    assert np.array_equal(server.bk, keys.bk) and np.array_equal(server.ksk, keys.ksk)
+    with pytest.raises(PermissionError):
+        server.decrypt(np.zeros((1, 631), np.uint32))
+    full = tmp_path / "keyset.npz"
+    wire_keys.save_keys(full, keys, include_secret=True)
+    client = wire_keys.load_keys(full)
+    cts = client.encrypt(np.array([1, 0, 1], np.uint8), seed=4)
+    c = tmp_path / "cts.npz"
+    wire_keys.save_ciphertexts(c, cts, client.params, meta={"model": "cancer"})
+    back, meta = wire_keys.load_ciphertexts(c)
+    assert meta == {"model": "cancer"}
+    assert list(keys.decrypt(back)) == [1, 0, 1]
+
+
+def test_wrong_document_kind_rejected(tmp_path, keys):
+    c = tmp_path / "cts.npz"
+    wire_keys.save_ciphertexts(c, keys.encrypt([1], seed=1), keys.params)
+    with pytest.raises(ValueError):
+        wire_keys.load_keys(c)

@@ -883,6 +883,7 @@ struct hb_engine {
     uint64_t flush_gen = 1;
     cudaEvent_t ev[4]{};
     uint64_t n_br = 0, n_ks = 0, n_launch = 0;
+    int num_sms = 148;
 };
 
 namespace {
@@ -1001,8 +1002,14 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
     HB_CUDA_TRY(cudaMalloc(&e->d_margin, sizeof(unsigned long long)));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<kBrGates, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)br_smem_bytes<kBrGates>()));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)br_smem_bytes<2>()));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)br_smem_bytes<1>()));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)br_smem_bytes<kBrGates>()));
+    HB_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    e->num_sms = prop.multiProcessorCount;
 
     // BK -> Fourier
     const size_t npoly = (size_t)p->n * kRows * 2;
@@ -1169,7 +1176,14 @@ int hb_run_gates(hb_engine *e, const hb_gate *gates, size_t n, uint32_t lanes) {
     a.items = e->d_br;
     a.n_work = (uint32_t)(nbr * lanes);
     HB_CUDA_TRY(cudaEventRecord(e->ev[0], e->stream));
-    if ((rc = launch_br<kBrGates, false>(e, a))) return rc;
+    // narrow levels (latency-bound): fewer bootstraps per CTA so each gets an SM of its own
+    if (a.n_work <= (uint32_t)e->num_sms) {
+        if ((rc = launch_br<1, false>(e, a))) return rc;
+    } else if (a.n_work <= 2u * (uint32_t)e->num_sms) {
+        if ((rc = launch_br<2, false>(e, a))) return rc;
+    } else {
+        if ((rc = launch_br<kBrGates, false>(e, a))) return rc;
+    }
     HB_CUDA_TRY(cudaEventRecord(e->ev[1], e->stream));
     KsArgs k{};
     k.big = e->d_big;

@@ -68,17 +68,26 @@ def parse_args():
 # distributed plumbing (torch.distributed: barrier + max over ranks only)
 # ---------------------------------------------------------------------------
 
+class _Rank0:
+    rank = 0
+    world = 1
+
+
 class Dist:
+    """HB_BENCH_SHARE_GPU=1 (testing only): every rank uses cuda:0 and a gloo
+    process group — the ranks never wait on each other's kernels."""
+
     def __init__(self):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
-        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.share = os.environ.get("HB_BENCH_SHARE_GPU") == "1"
+        self.local_rank = 0 if self.share else int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
         if self.world > 1:
             import torch
             import torch.distributed as dist
 
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            backend = "nccl" if torch.cuda.is_available() and not self.share else "gloo"
             if backend == "nccl":
                 torch.cuda.set_device(self.local_rank)
             dist.init_process_group(backend=backend)
@@ -87,7 +96,7 @@ class Dist:
 
     def barrier(self):
         if self.pg:
-            if self.torch.cuda.is_available():
+            if self.torch.cuda.is_available() and not self.share:
                 self.pg.barrier(device_ids=[self.local_rank])
             else:
                 self.pg.barrier()
@@ -95,7 +104,7 @@ class Dist:
     def max(self, x):
         if not self.pg:
             return x
-        dev = f"cuda:{self.local_rank}" if self.torch.cuda.is_available() else "cpu"
+        dev = f"cuda:{self.local_rank}" if self.torch.cuda.is_available() and not self.share else "cpu"
         t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=dev)
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
@@ -374,6 +383,13 @@ def run_ours(args, dist):
 
 def main():
     args = parse_args()
+    if args.impl == "reference":
+        # CPU arm: rank 0 alone runs; no process group, other ranks exit 0 without work
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
+        line = run_reference(args, _Rank0())
+        print(json.dumps(line), flush=True)
+        return
     dist = Dist()
     try:
         line = run_reference(args, dist) if args.impl == "reference" else run_ours(args, dist)

@@ -176,6 +176,7 @@ class TfheContext(GateBackend):
         self._inputs = {}      # node id -> host ciphertexts [lanes][n+1] not yet uploaded
         self._engine = None
         self._slots = None
+        self._history = []     # every executed (level, records) batch, in order (f1 replay)
         self._chunks = []
         self._slot_next = 0
         self._finalizer = None
@@ -540,6 +541,7 @@ class TfheContext(GateBackend):
                 eng.sync()
             except RuntimeError as exc:
                 raise DeviceError(str(exc)) from exc
+            self._history.extend(batches)
             for nid in pending:
                 self._done[nid] = True
             n_mux = sum(int(np.count_nonzero(r["kind"] == GATE_MUX)) for _, r in batches)
@@ -549,6 +551,40 @@ class TfheContext(GateBackend):
             self.exec_stats["flushes"] += 1
             self.exec_stats["flush_s"] += time.perf_counter() - t0
             self._pending = []
+
+    def replay(self, handles, cts):
+        """Per-model DAG caching: the circuit is data-oblivious,
+        so after one evaluation the recorded level schedule can be re-run on new
+        encrypted inputs without rebuilding the Python DAG.  `handles` are input
+        handles of this context (from encrypt*/import_ciphertexts), `cts` their
+        new ciphertexts [count][lanes][n+1] (or [count][n+1] for lanes == 1).
+        Every handle derived from them decrypts to the new results afterwards."""
+        self._check(*handles)
+        cts = np.asarray(cts, dtype=np.uint32)
+        if cts.ndim == 2:
+            cts = cts[:, None, :]
+        if cts.shape != (len(handles), self.lanes, self.params.n + 1):
+            raise ValueError(f"expected [{len(handles)}, {self.lanes}, {self.params.n + 1}] ciphertexts")
+        with self._lock:
+            if self._pending:
+                self.flush()
+            nids = [h._value >> 1 for h in handles]
+            if any(nid == 0 or self._op[nid] != _OP_INPUT for nid in nids) or any(h._value & 1 for h in handles):
+                raise ValueError("replay inputs must be (non-negated) input handles")
+            t0 = time.perf_counter()
+            eng = self._ensure_engine()
+            self._inputs.clear()
+            phys = self._map_slots([self._slot[nid] for nid in nids])
+            for ps, c in zip(phys, cts):
+                eng.upload(int(ps) * self.lanes, c)
+            try:
+                for _lvl, recs in self._history:
+                    eng.run_gates(recs, lanes=self.lanes)
+                eng.sync()
+            except RuntimeError as exc:
+                raise DeviceError(str(exc)) from exc
+            self.exec_stats["replays"] = self.exec_stats.get("replays", 0) + 1
+            self.exec_stats["flush_s"] += time.perf_counter() - t0
 
     def _ciphertexts(self, refs):
         """Host LWE samples [len(refs)][lanes][n+1] for node refs (no negation)."""

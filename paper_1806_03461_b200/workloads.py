@@ -75,7 +75,7 @@ def decode_outputs(ctx, outs):
     return np.where(bits.T == 1, 1, -1)
 
 
-def run_encrypted(ctx_cls, config, seed=0, device=0, options=EvalOptions(), check=True):
+def run_encrypted(ctx_cls, config, seed=0, device=0, options=EvalOptions(), check=True, replays=0):
     """Encrypt a batch, evaluate through the reference compiler on a
     lane-batched context, decrypt, compare with oracle_eval.  Returns a report."""
     model, batch = build(config, seed)
@@ -94,6 +94,22 @@ def run_encrypted(ctx_cls, config, seed=0, device=0, options=EvalOptions(), chec
     if check:
         ok = all(list(got[b]) == oracle_eval(model, [1 if v else -1 for v in X[b]]) for b in range(batch))
     counted = ctx.gate_count * batch
+    replay = None
+    if replays:
+        # steady-state serving: new encrypted batch through the cached DAG
+        times, oks = [], []
+        for r in range(replays):
+            X2 = inputs(config, model, batch, seed + 100 + r)
+            cts = ctx.keys.encrypt(X2.reshape(-1), seed=seed + 7, stream=500 + r).reshape(
+                batch, X2.shape[1], -1).transpose(1, 0, 2)
+            ta = time.perf_counter()
+            ctx.replay(xb, cts)
+            got2 = decode_outputs(ctx, outs)
+            times.append(time.perf_counter() - ta)
+            if check:
+                oks.append(all(list(got2[b]) == oracle_eval(model, [1 if v else -1 for v in X2[b]])
+                               for b in range(batch)))
+        replay = {"replays": replays, "latency_s": min(times), "matches_oracle_eval": all(oks) if check else None}
     return {
         "config": config, "batch": batch, "counted_gates": counted,
         "counted_gates_per_input": ctx.gate_count,
@@ -104,4 +120,5 @@ def run_encrypted(ctx_cls, config, seed=0, device=0, options=EvalOptions(), chec
         "bootstraps_per_s": ctx.exec_stats["bootstraps"] / (t3 - t2),
         "counted_gates_per_s": counted / (t3 - t2),
         "matches_oracle_eval": ok,
+        "replay": replay,
     }

@@ -210,3 +210,23 @@ def test_flush_requires_a_device_on_the_product_context():
 
 def test_all_costed_kinds_present():
     assert COSTED_KINDS == (AND, OR, XOR, XNOR, MUX)
+
+
+def test_replay_reuses_the_dag_for_new_inputs():
+    """f1: evaluate once, then replay the recorded schedule on new inputs."""
+    rng = random.Random(21)
+    d, p = 20, 3
+    rows = tuple(tuple(rng.choice((-1, 1)) for _ in range(d)) for _ in range(p))
+    m = validate_model(TernaryModel(d, (DenseLayer(rows, (0,) * p), SignActivation()), "sign_bits"))
+    ctx = Plain(seed=42)
+    xs = [rng.choice((-1, 1)) for _ in range(d)]
+    xb = encrypt_input(ctx, xs)
+    outs, _ = eval_model(ctx, m, xb)
+    assert decrypt_output(ctx, outs) == oracle_eval(m, xs)
+    gates_before = ctx.gate_count
+    for trial in range(3):
+        xs2 = [rng.choice((-1, 1)) for _ in range(d)]
+        cts = ctx.keys.encrypt([1 if v == 1 else 0 for v in xs2], seed=100 + trial)
+        ctx.replay(xb, cts)
+        assert decrypt_output(ctx, outs) == oracle_eval(m, xs2)
+    assert ctx.gate_count == gates_before  # no new DAG nodes

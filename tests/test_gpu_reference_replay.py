@@ -273,3 +273,22 @@ def test_lanes_batch_of_inputs_share_one_dag():
     for lane in range(lanes):
         xs = [1 if b else -1 for b in X[lane]]
         assert [int(w._vals[lane]) for w in outs] == oracle_eval(model, xs)
+
+
+def test_replay_cached_dag_on_gpu():
+    """f1 per-model DAG caching: one DAG, several encrypted inputs."""
+    from hebnn.compiler import encrypt_input
+
+    rng = random.Random(8)
+    d, p = 64, 5
+    rows = tuple(tuple(rng.choice((-1, 0, 1)) for _ in range(d)) for _ in range(p))
+    m = validate_model(TernaryModel(d, (DenseLayer(rows, (0,) * p), SignActivation()), "sign_bits"))
+    ctx = ctx_new()
+    xs = [rng.choice((-1, 1)) for _ in range(d)]
+    xb = encrypt_input(ctx, xs)
+    outs, _ = eval_model(ctx, m, xb)
+    assert decrypt_output(ctx, outs) == oracle_eval(m, xs)
+    for trial in range(3):
+        xs2 = [rng.choice((-1, 1)) for _ in range(d)]
+        ctx.replay(xb, ctx.keys.encrypt([1 if v == 1 else 0 for v in xs2], seed=50 + trial))
+        assert decrypt_output(ctx, outs) == oracle_eval(m, xs2)

@@ -162,96 +162,26 @@ struct TwSeeds {
     double2 f_a0, step_a, step_b, i_b0, i_stepb;
 };
 
-// Forward negacyclic transform of a real polynomial given as x_m = a_j + i a_{j+512}
-// at j = t + 64 m: the twist psi^j = psi^t c_m is split into compile-time c_m
-// (applied here) and psi^t, which is merged with the pass-A twiddles
-// W^{t k2} into psi^{t (4 k2 + 1)} and generated by recurrence; pass-B
-// twiddles W64^{j0 k1} by recurrence.  No table loads.
-__device__ __forceinline__ void nega_fft_fwd(double2 (&x)[8], double2 *S0, double2 *S1, int t,
-                                             const TwSeeds &tw, int bar_id) {
-#pragma unroll
-    for (int m = 1; m < 8; m++) x[m] = cmul(x[m], c16(m));
-    dft8(x);
-    {
-        const int j0 = t & 7, j1 = t >> 3;
-        double2 w = tw.f_a0;
-#pragma unroll
-        for (int k2 = 0; k2 < 8; k2++) {
-            S0[j0 * 65 + k2 * 8 + j1] = cmul(x[rev3(k2)], w);
-            if (k2 < 7) w = cmul(w, tw.step_a);
-        }
+// T[k] = T0 * step^k, k = 0..7, as a depth-4 product tree (shorter dependency
+// chain and smaller rounding error than the serial recurrence).
+__device__ __forceinline__ void tw_powers(double2 T0, double2 step, bool t0_is_one, double2 (&T)[8]) {
+    const double2 s2 = cmul(step, step);
+    const double2 s4 = cmul(s2, s2);
+    if (t0_is_one) {
+        T[0] = make_double2(1.0, 0.0);
+        T[1] = step;
+        T[2] = s2;
+        T[3] = cmul(step, s2);
+    } else {
+        T[0] = T0;
+        T[1] = cmul(T0, step);
+        T[2] = cmul(T0, s2);
+        T[3] = cmul(T[1], s2);
     }
-    group_bar(bar_id);
-    {
-        const int j0 = t & 7, k2 = t >> 3;
-#pragma unroll
-        for (int j1 = 0; j1 < 8; j1++) x[j1] = S0[j0 * 65 + k2 * 8 + j1];
-        dft8(x);
-        S1[k2 * 65 + j0] = x[0];
-        double2 w = tw.step_b;
-#pragma unroll
-        for (int k1 = 1; k1 < 8; k1++) {
-            S1[k2 * 65 + k1 * 8 + j0] = cmul(x[rev3(k1)], w);
-            if (k1 < 7) w = cmul(w, tw.step_b);
-        }
-    }
-    group_bar(bar_id);
-    {
-        const int k2 = t & 7, k1 = t >> 3;
-        double2 y[8];
-#pragma unroll
-        for (int j0 = 0; j0 < 8; j0++) y[j0] = S1[k2 * 65 + k1 * 8 + j0];
-        dft8(y);
-#pragma unroll
-        for (int k0 = 0; k0 < 8; k0++) x[k0] = y[rev3(k0)];
-    }
-}
-
-// Inverse: given evaluations P at bins t + 64 k (already scaled by 1/512 via
-// the BK), returns x_m with Re = c_j, Im = c_{j+512} at j = t + 64 m.
-// Computed as conj(FFT(conj P) * psi^j): psi^{v} of the destination thread is
-// folded into the pass-B twiddles, c_m applied after pass C.
-__device__ __forceinline__ void nega_fft_inv(double2 (&x)[8], double2 *S0, double2 *S1, int t,
-                                             const TwSeeds &tw, int bar_id) {
-#pragma unroll
-    for (int m = 0; m < 8; m++) x[m].y = -x[m].y;
-    dft8(x);
-    {
-        const int j0 = t & 7, j1 = t >> 3;
-        S0[j0 * 65 + j1] = x[0];
-        double2 w = tw.step_a;
-#pragma unroll
-        for (int k2 = 1; k2 < 8; k2++) {
-            S0[j0 * 65 + k2 * 8 + j1] = cmul(x[rev3(k2)], w);
-            if (k2 < 7) w = cmul(w, tw.step_a);
-        }
-    }
-    group_bar(bar_id);
-    {
-        const int j0 = t & 7, k2 = t >> 3;
-#pragma unroll
-        for (int j1 = 0; j1 < 8; j1++) x[j1] = S0[j0 * 65 + k2 * 8 + j1];
-        dft8(x);
-        double2 w = tw.i_b0;
-#pragma unroll
-        for (int k1 = 0; k1 < 8; k1++) {
-            S1[k2 * 65 + k1 * 8 + j0] = cmul(x[rev3(k1)], w);
-            if (k1 < 7) w = cmul(w, tw.i_stepb);
-        }
-    }
-    group_bar(bar_id);
-    {
-        const int k2 = t & 7, k1 = t >> 3;
-        double2 y[8];
-#pragma unroll
-        for (int j0 = 0; j0 < 8; j0++) y[j0] = S1[k2 * 65 + k1 * 8 + j0];
-        dft8(y);
-#pragma unroll
-        for (int k0 = 0; k0 < 8; k0++) {
-            double2 v = (k0 == 0) ? y[0] : cmul(y[rev3(k0)], c16(k0));
-            x[k0] = make_double2(v.x, -v.y);
-        }
-    }
+    T[4] = t0_is_one ? s4 : cmul(T0, s4);
+    T[5] = cmul(T[1], s4);
+    T[6] = cmul(T[2], s4);
+    T[7] = cmul(T[3], s4);
 }
 
 // NP-polynomial variants: the passes of NP independent transforms are
@@ -268,12 +198,12 @@ __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch
     }
     {
         const int j0 = t & 7, j1 = t >> 3;
-        double2 w = tw.f_a0;
+        double2 T[8];
+        tw_powers(tw.f_a0, tw.step_a, false, T);
 #pragma unroll
         for (int k2 = 0; k2 < 8; k2++) {
 #pragma unroll
-            for (int q = 0; q < NP; q++) xch[(2 * q) * kXchStride + j0 * 65 + k2 * 8 + j1] = cmul(x[q][rev3(k2)], w);
-            if (k2 < 7) w = cmul(w, tw.step_a);
+            for (int q = 0; q < NP; q++) xch[(2 * q) * kXchStride + j0 * 65 + k2 * 8 + j1] = cmul(x[q][rev3(k2)], T[k2]);
         }
     }
     group_bar(bar_id);
@@ -286,13 +216,13 @@ __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch
             dft8(x[q]);
             xch[(2 * q + 1) * kXchStride + k2 * 65 + j0] = x[q][0];
         }
-        double2 w = tw.step_b;
+        double2 T[8];
+        tw_powers(tw.step_b, tw.step_b, true, T);
 #pragma unroll
         for (int k1 = 1; k1 < 8; k1++) {
 #pragma unroll
             for (int q = 0; q < NP; q++)
-                xch[(2 * q + 1) * kXchStride + k2 * 65 + k1 * 8 + j0] = cmul(x[q][rev3(k1)], w);
-            if (k1 < 7) w = cmul(w, tw.step_b);
+                xch[(2 * q + 1) * kXchStride + k2 * 65 + k1 * 8 + j0] = cmul(x[q][rev3(k1)], T[k1]);
         }
     }
     group_bar(bar_id);
@@ -323,12 +253,12 @@ __device__ __forceinline__ void nega_fft_inv_n(double2 (&x)[NP][8], double2 *xch
         const int j0 = t & 7, j1 = t >> 3;
 #pragma unroll
         for (int q = 0; q < NP; q++) xch[(2 * q) * kXchStride + j0 * 65 + j1] = x[q][0];
-        double2 w = tw.step_a;
+        double2 T[8];
+        tw_powers(tw.step_a, tw.step_a, true, T);
 #pragma unroll
         for (int k2 = 1; k2 < 8; k2++) {
 #pragma unroll
-            for (int q = 0; q < NP; q++) xch[(2 * q) * kXchStride + j0 * 65 + k2 * 8 + j1] = cmul(x[q][rev3(k2)], w);
-            if (k2 < 7) w = cmul(w, tw.step_a);
+            for (int q = 0; q < NP; q++) xch[(2 * q) * kXchStride + j0 * 65 + k2 * 8 + j1] = cmul(x[q][rev3(k2)], T[k2]);
         }
     }
     group_bar(bar_id);
@@ -340,13 +270,13 @@ __device__ __forceinline__ void nega_fft_inv_n(double2 (&x)[NP][8], double2 *xch
             for (int j1 = 0; j1 < 8; j1++) x[q][j1] = xch[(2 * q) * kXchStride + j0 * 65 + k2 * 8 + j1];
             dft8(x[q]);
         }
-        double2 w = tw.i_b0;
+        double2 T[8];
+        tw_powers(tw.i_b0, tw.i_stepb, false, T);
 #pragma unroll
         for (int k1 = 0; k1 < 8; k1++) {
 #pragma unroll
             for (int q = 0; q < NP; q++)
-                xch[(2 * q + 1) * kXchStride + k2 * 65 + k1 * 8 + j0] = cmul(x[q][rev3(k1)], w);
-            if (k1 < 7) w = cmul(w, tw.i_stepb);
+                xch[(2 * q + 1) * kXchStride + k2 * 65 + k1 * 8 + j0] = cmul(x[q][rev3(k1)], T[k1]);
         }
     }
     group_bar(bar_id);

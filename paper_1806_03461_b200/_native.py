@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libhebnn_b200.so")
+LIB_PATH = os.environ.get("HEBNN_B200_LIB") or os.path.join(_HERE, "_lib", "libhebnn_b200.so")
 
 HB_OK = 0
 HB_EINVAL = -1

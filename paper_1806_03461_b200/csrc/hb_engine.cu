@@ -297,9 +297,17 @@ __device__ __forceinline__ void nega_fft_inv_n(double2 (&x)[NP][8], double2 *xch
     }
 }
 
-// double from a small signed integer without I2F: (2^52 + 2^51 + 2^31 + d) - (2^52 + 2^51 + 2^31)
+#ifndef HB_I2F
+#define HB_I2F 0
+#endif
+// double from a small signed integer: magic-number DADD (default) or I2F.F64
 __device__ __forceinline__ double small_int_to_double(int32_t d) {
+#if HB_I2F
+    return (double)d;
+#else
+    // (2^52 + 2^51 + 2^31 + d) - (2^52 + 2^51 + 2^31)
     return __hiloint2double(0x43380000, (int)((uint32_t)d ^ 0x80000000u)) - 6755401588539392.0;
+#endif
 }
 // round(v) mod 2^32 for |v| < 2^51 via the 1.5 * 2^52 magic constant
 __device__ __forceinline__ uint32_t round_to_torus(double v) {
@@ -407,6 +415,9 @@ struct BrArgs {
 };
 
 constexpr int kStages = 3;  // BK rows in the shared-memory ring
+#ifndef HB_EXP_SKIP
+#define HB_EXP_SKIP 0  // timing experiments only: 1 skip fwd FFT, 2 skip MAC, 4 skip inverse FFT
+#endif
 constexpr uint32_t kRowBytes = 2 * kNH * sizeof(double2);  // 16 KiB: one TGSW row, both output polys
 
 template <int G>
@@ -505,8 +516,13 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
 #pragma unroll
             for (int m = 0; m < 8; m++) {
                 const int j = t + 64 * m;
+#if HB_EXP_SKIP & 8
+                dlo[q][m] = P[j] * 2654435761u;
+                dhi[q][m] = P[j + kNH] * 2246822519u;
+#else
                 dlo[q][m] = rot_coef(P, j, a) - P[j];
                 dhi[q][m] = rot_coef(P, j + kNH, a) - P[j + kNH];
+#endif
             }
         }
         double2 f0[8], f1[8];  // Fourier accumulators of the two output polys
@@ -537,7 +553,7 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
                                            small_int_to_double(gadget_digit(hi, p)));
                 }
             }
-            nega_fft_fwd_n<2>(x, xch, t, sm.tws[t], bar_id);
+            if (!(HB_EXP_SKIP & 1)) nega_fft_fwd_n<2>(x, xch, t, sm.tws[t], bar_id);
 #pragma unroll
             for (int h = 0; h < 2; h++) {
                 const int rr = row_it + h;
@@ -549,7 +565,13 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
                     bk0 = args.bkf + (size_t)rr * 2 * kNH;  // bypass the ring (debug A/B)
                     bk1 = bk0 + kNH;
                 }
-                if (pr == 0 && h == 0) {
+                if (HB_EXP_SKIP & 2) {
+#pragma unroll
+                    for (int m = 0; m < 8; m++) {
+                        if (pr == 0 && h == 0) { f0[m] = x[h][m]; f1[m] = x[h][m]; }
+                        else { f0[m] = cadd(f0[m], x[h][m]); f1[m] = csub(f1[m], x[h][m]); }
+                    }
+                } else if (pr == 0 && h == 0) {
 #pragma unroll
                     for (int m = 0; m < 8; m++) {
                         f0[m] = cmul(x[h][m], bk0[t + 64 * m]);
@@ -574,7 +596,7 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
                 x[0][m] = f0[m];
                 x[1][m] = f1[m];
             }
-            nega_fft_inv_n<2>(x, xch, t, sm.tws[t], bar_id);
+            if (!(HB_EXP_SKIP & 4)) nega_fft_inv_n<2>(x, xch, t, sm.tws[t], bar_id);
 #pragma unroll
             for (int q = 0; q < 2; q++) {
                 uint32_t *P = q ? accB : accA;
@@ -586,8 +608,13 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
                         max_err = fmax(max_err, fabs(hi - rint(hi)));
                     }
                     const int j = t + 64 * m;
+#if HB_EXP_SKIP & 16
+                    if (lo == 12345.0) P[j] += 1;  // keep the computation alive
+                    if (hi == 12345.0) P[j + kNH] += 1;
+#else
                     P[j] += round_to_torus(lo);
                     P[j + kNH] += round_to_torus(hi);
+#endif
                 }
             }
         }

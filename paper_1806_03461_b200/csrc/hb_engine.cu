@@ -839,6 +839,7 @@ struct hb_engine {
     size_t flush_bytes = 0;
     uint64_t flush_gen = 1;
     cudaEvent_t ev[4]{};
+    cudaEvent_t ev_stage = nullptr;  // item copies out of h_stage done
     uint64_t n_br = 0, n_ks = 0, n_launch = 0;
     int num_sms = 148;
 };
@@ -942,6 +943,8 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
     e->pool_stride = (uint32_t)((p->n + 1 + 3) & ~3);
     HB_CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     for (auto &ev : e->ev) HB_CUDA_TRY(cudaEventCreate(&ev));
+    HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_stage, cudaEventDisableTiming));
+    HB_CUDA_TRY(cudaEventRecord(e->ev_stage, e->stream));
 
     // twiddle tables, computed in long double then rounded
     std::vector<double2> W(kNH), TW(kNH);
@@ -1004,6 +1007,7 @@ int hb_engine_destroy(hb_engine *e) {
     if (e->h_stage) cudaFreeHost(e->h_stage);
     for (auto &ev : e->ev)
         if (ev) cudaEventDestroy(ev);
+    if (e->ev_stage) cudaEventDestroy(e->ev_stage);
     if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
     return HB_OK;
@@ -1065,6 +1069,7 @@ int hb_pool_gather(hb_engine *e, const uint32_t *slots, size_t count, uint32_t *
     if (rc) return rc;
     rc = ensure_host_stage(e, count * sizeof(uint32_t));
     if (rc) return rc;
+    HB_CUDA_TRY(cudaEventSynchronize(e->ev_stage));
     std::memcpy(e->h_stage, slots, count * sizeof(uint32_t));
     uint32_t *d_slots = e->d_tmp, *d_out = e->d_tmp + count;
     HB_CUDA_TRY(cudaMemcpyAsync(d_slots, e->h_stage, count * sizeof(uint32_t), cudaMemcpyHostToDevice, e->stream));
@@ -1102,7 +1107,9 @@ int hb_run_gates(hb_engine *e, const hb_gate *gates, size_t n, uint32_t lanes) {
     const size_t br_bytes = nbr * sizeof(BrItem), ks_bytes = n * sizeof(KsItem);
     int rc = ensure_host_stage(e, br_bytes + ks_bytes);
     if (rc) return rc;
-    HB_CUDA_TRY(cudaStreamSynchronize(e->stream));  // host stage may still feed the previous level
+    // the pinned stage fed the previous level's item copies; wait for those copies only,
+    // so the host builds level k+1 while the device still runs level k
+    HB_CUDA_TRY(cudaEventSynchronize(e->ev_stage));
     BrItem *hbr = reinterpret_cast<BrItem *>(e->h_stage);
     KsItem *hks = reinterpret_cast<KsItem *>(reinterpret_cast<char *>(e->h_stage) + br_bytes);
     size_t b = 0;
@@ -1127,6 +1134,7 @@ int hb_run_gates(hb_engine *e, const hb_gate *gates, size_t n, uint32_t lanes) {
         return rc;
     HB_CUDA_TRY(cudaMemcpyAsync(e->d_br, hbr, br_bytes, cudaMemcpyHostToDevice, e->stream));
     HB_CUDA_TRY(cudaMemcpyAsync(e->d_ks, hks, ks_bytes, cudaMemcpyHostToDevice, e->stream));
+    HB_CUDA_TRY(cudaEventRecord(e->ev_stage, e->stream));
 
     BrArgs a = br_args(e);
     a.lanes = lanes;

@@ -10,6 +10,8 @@ replace ``SimContext.encrypt``/``decrypt``.
 from __future__ import annotations
 
 import ctypes
+import functools
+import threading
 
 import numpy as np
 
@@ -89,11 +91,25 @@ class KeySet:
         return out.reshape(cts.shape[:-1])
 
 
+def _locked(fn):
+    """Serialise calls into one engine (its stream, staging buffers and pool
+    are shared by every context that uses it)."""
+
+    @functools.wraps(fn)
+    def wrap(self, *a, **kw):
+        with self._lock:
+            return fn(self, *a, **kw)
+
+    return wrap
+
+
 class Engine:
     """One device engine (one CUDA device, one stream) holding the Fourier BK,
-    the KSK and a pool of LWE ciphertext slots."""
+    the KSK and a pool of LWE ciphertext slots.  Thread-safe: calls are
+    serialised by a per-engine lock."""
 
     def __init__(self, keys, device=0):
+        self._lock = threading.RLock()
         self.keys = keys
         self.params = keys.params
         self._e = ctypes.c_void_p()
@@ -101,6 +117,7 @@ class Engine:
                                      ctypes.byref(self._e)))
         self.device = device
 
+    @_locked
     def close(self):
         if self._e:
             lib().hb_engine_destroy(self._e)
@@ -120,68 +137,82 @@ class Engine:
     def capacity(self):
         return lib().hb_pool_capacity(self._e)
 
+    @_locked
     def reserve(self, slots):
         check(lib().hb_pool_reserve(self._e, int(slots)))
 
+    @_locked
     def upload(self, first, cts):
         cts = np.ascontiguousarray(cts, dtype=np.uint32)
         check(lib().hb_pool_upload(self._e, int(first), cts.shape[0], u32p(cts), cts.shape[1]))
 
+    @_locked
     def download(self, first, count):
         out = np.zeros((count, self.params.n + 1), np.uint32)
         check(lib().hb_pool_download(self._e, int(first), int(count), u32p(out), out.shape[1]))
         return out
 
+    @_locked
     def gather(self, slots):
         slots = np.ascontiguousarray(slots, dtype=np.uint32)
         out = np.zeros((slots.size, self.params.n + 1), np.uint32)
         check(lib().hb_pool_gather(self._e, u32p(slots), slots.size, u32p(out), out.shape[1]))
         return out
 
+    @_locked
     def run_gates(self, gates, lanes=1):
         """gates: numpy array of GATE_DTYPE records (one level)."""
         gates = np.ascontiguousarray(gates, dtype=GATE_DTYPE)
         check(lib().hb_run_gates(self._e, gates.ctypes.data_as(ctypes.c_void_p), gates.shape[0], int(lanes)))
 
+    @_locked
     def sync(self):
         check(lib().hb_sync(self._e))
 
+    @_locked
     def last_timing(self):
         a, b = ctypes.c_float(), ctypes.c_float()
         check(lib().hb_last_timing(self._e, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
 
+    @_locked
     def counters(self):
         a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
         check(lib().hb_counters(self._e, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
         return {"blind_rotations": a.value, "key_switches": b.value, "kernel_launches": c.value}
 
+    @_locked
     def flush_l2(self, nbytes=0):
         check(lib().hb_flush_l2(self._e, int(nbytes)))
 
+    @_locked
     def measure_fp64_peak(self):
         v = ctypes.c_double()
         check(lib().hb_measure_fp64_peak(self._e, ctypes.byref(v)))
         return v.value
 
     # ---- stage entry points (parity) ----
+    @_locked
     def debug_blind_rotate(self, lwe, mu=EIGHTH, iters=-1):
         out = np.zeros(2 * self.params.N, np.uint32)
         check(lib().hb_debug_blind_rotate(self._e, u32p(np.ascontiguousarray(lwe, np.uint32)), mu, iters, u32p(out)))
         return out
 
+    @_locked
     def debug_bootstrap_wo_ks(self, lin):
         lin = np.ascontiguousarray(lin, dtype=np.uint32).reshape(-1, self.params.n + 1)
         out = np.zeros((lin.shape[0], self.params.N + 1), np.uint32)
         check(lib().hb_debug_bootstrap_wo_ks(self._e, u32p(lin), lin.shape[0], u32p(out)))
         return out
 
+    @_locked
     def debug_keyswitch(self, big):
         big = np.ascontiguousarray(big, dtype=np.uint32).reshape(-1, self.params.N + 1)
         out = np.zeros((big.shape[0], self.params.n + 1), np.uint32)
         check(lib().hb_debug_keyswitch(self._e, u32p(big), big.shape[0], u32p(out)))
         return out
 
+    @_locked
     def debug_fourier(self, polys=None, count=None, which=0):
         if which == 1:
             out = np.zeros((count, self.params.N // 2, 2), np.float64)
@@ -194,6 +225,7 @@ class Engine:
                                          out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 0))
         return out[..., 0] + 1j * out[..., 1]
 
+    @_locked
     def debug_fft_margin(self):
         v = ctypes.c_double()
         check(lib().hb_debug_fft_margin(self._e, ctypes.byref(v)))

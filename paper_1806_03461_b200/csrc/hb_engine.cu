@@ -420,9 +420,13 @@ constexpr int kStages = 3;  // BK rows in the shared-memory ring
 #endif
 constexpr uint32_t kRowBytes = 2 * kNH * sizeof(double2);  // 16 KiB: one TGSW row, both output polys
 
+#ifndef HB_BK_LDG
+#define HB_BK_LDG 0  // 1: BK rows read through L1 (LDG + prefetch) instead of the smem ring
+#endif
+constexpr int kRingStages = HB_BK_LDG ? 1 : kStages;
 template <int G>
 struct BrSmem {
-    double2 bk[kStages][2 * kNH];           // BK row ring
+    double2 bk[kRingStages][2 * kNH];       // BK row ring
     uint64_t full[kStages], empty[kStages];
     uint32_t acc[G][2][kN];                  // TRLWE accumulators (A, B)
     double2 xch[G][2][2][kXchStride];        // FFT exchange buffers: [poly pair][double buffer]
@@ -459,7 +463,7 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
             mbar_init(&sm.empty[s], 2 * G);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int it = 0; it < kStages && it < rows_needed; it++) {
+        for (int it = 0; it < kStages && it < rows_needed && !HB_BK_LDG; it++) {
             mbar_arrive_expect_tx(&sm.full[it], kRowBytes);
             bulk_g2s(sm.bk[it], bk_src + (size_t)it * kRowBytes, kRowBytes, &sm.full[it]);
         }
@@ -528,8 +532,18 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
         double2 f0[8], f1[8];  // Fourier accumulators of the two output polys
 #pragma unroll 1
         for (int pr = 0; pr < kRows / 2; pr++, row_it += 2) {
+#if HB_BK_LDG
+            {   // prefetch the next pair's two BK rows (32 KiB) into L1: 4 x 128-B lines per thread
+                const char *nxt = bk_src + (size_t)(row_it + 2) * kRowBytes;
+                if (row_it + 2 < rows_needed) {
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(nxt + (size_t)(t + 64 * u) * 128));
+                }
+            }
+#endif
             // producer: rows row_it+1 and row_it+2 (stages freed by rows row_it-2, row_it-1)
-            if (threadIdx.x == 0) {
+            if (!HB_BK_LDG && threadIdx.x == 0) {
 #pragma unroll 1
                 for (int nx = row_it + 1; nx <= row_it + 2; nx++) {
                     if (nx < kStages || nx >= rows_needed) continue;
@@ -558,9 +572,14 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
             for (int h = 0; h < 2; h++) {
                 const int rr = row_it + h;
                 const int s = rr % kStages;
+#if HB_BK_LDG
+                const double2 *bk0 = args.bkf + (size_t)rr * 2 * kNH;
+                const double2 *bk1 = bk0 + kNH;
+#else
                 mbar_wait(&sm.full[s], (rr / kStages) & 1);
                 const double2 *bk0 = sm.bk[s];
                 const double2 *bk1 = sm.bk[s] + kNH;
+#endif
                 if (kDebug && args.margin == nullptr && args.acc_dump != nullptr && args.n_work == 2) {
                     bk0 = args.bkf + (size_t)rr * 2 * kNH;  // bypass the ring (debug A/B)
                     bk1 = bk0 + kNH;
@@ -585,7 +604,7 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
                     }
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.empty[s]);
+                if (!HB_BK_LDG && lane == 0) mbar_arrive(&sm.empty[s]);
             }
         }
         // inverse transforms of both output polynomials + round + ACC update

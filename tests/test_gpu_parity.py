@@ -85,3 +85,32 @@ def test_mux_bit_exact(engine, keys, octx):
     assert np.array_equal(keys.decrypt(out), np.where(s == 1, a, b))
     for i in (0, 5):
         assert np.array_equal(out[i], octx.mux(cs[i], ca[i], cb[i]))
+
+
+def test_gpu_matches_committed_golden_vectors(engine, keys):
+    """The sm_100a engine reproduces tests/golden/tfhe_golden_seed42.npz
+    (oracle-generated: keys from seed 42, encryptions, gates, MUX, stages)."""
+    import os
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "tfhe_golden_seed42.npz"))
+    assert np.array_equal(keys.lwe_key, g["lwe_key"])
+    inputs = g["inputs"]
+    assert np.array_equal(keys.encrypt(g["input_bits"], seed=42, stream=77), inputs)
+    assert np.array_equal(engine.debug_blind_rotate(inputs[0], iters=3), g["acc_prefix3"])
+    assert np.array_equal(engine.debug_bootstrap_wo_ks(inputs[2:3])[0], g["bootstrap_wo_ks"])
+    assert np.array_equal(engine.debug_keyswitch(g["ks_in"][None, :])[0], g["ks_out"])
+    engine.reserve(16)
+    engine.upload(0, inputs)
+    recs = tfhe.gate_records(len(tfhe.GATE_LIN) + 2)
+    names = list(tfhe.GATE_LIN)
+    for i, name in enumerate(names):
+        c0, al, be = tfhe.GATE_LIN[name]
+        recs[i] = (8 + i, 0, 1, 0, c0, al, be, 0, 0)
+    recs[len(names)] = (8 + len(names), 1, 0, 4, 0, 1, 1, 1, 0)        # mux(in1, in0, in4)
+    recs[len(names) + 1] = (9 + len(names), 0, 2, 1, 0, 1, 1, 1, 0)    # mux(in0, in2, in1)
+    engine.run_gates(recs)
+    out = engine.download(8, len(names) + 2)
+    for i, name in enumerate(names):
+        assert np.array_equal(out[i], g[f"gate_{name}"]), name
+    assert np.array_equal(out[len(names)], g["mux_010"])
+    assert np.array_equal(out[len(names) + 1], g["mux_110"])

@@ -126,12 +126,14 @@ int hb_pool_gather(hb_engine *e, const uint32_t *slots, size_t count, uint32_t *
 
 /* Run one level of independent gates (asynchronous on the engine stream).
  * Fused prologue (linear combination + mod switch) -> blind rotation ->
- * sample extract, then batched key switch into pool[dst]. */
+ * sample extract, then batched key switch into pool[dst].  Very wide levels
+ * (> 2^20 blind rotations x lanes) are split into several launches. */
 int hb_run_gates(hb_engine *e, const hb_gate *gates, size_t n, uint32_t lanes);
 int hb_sync(hb_engine *e);
 
 /* Device time (ms, CUDA events on the engine stream) of the blind-rotation and
- * key-switch kernels of the most recent hb_run_gates; accumulated counters of
+ * key-switch kernels of the most recent hb_run_gates launch (its last chunk);
+ * accumulated counters of
  * executed blind rotations and key switches since creation. */
 int hb_last_timing(hb_engine *e, float *br_ms, float *ks_ms);
 int hb_counters(hb_engine *e, uint64_t *blind_rotations, uint64_t *key_switches,

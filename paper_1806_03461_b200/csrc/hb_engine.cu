@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -830,6 +831,10 @@ constexpr size_t br_smem_bytes() {
 
 }  // namespace
 
+// Work items (blind rotations x lanes) per launch: bounds the extracted-LWE
+// scratch (4,112 B per item) to ~4.3 GB for very wide levels.
+constexpr size_t kMaxWorkPerLaunch = (size_t)1 << 20;
+
 // ---------------------------------------------------------------------------
 // engine object
 // ---------------------------------------------------------------------------
@@ -861,6 +866,7 @@ struct hb_engine {
     cudaEvent_t ev_stage = nullptr;  // item copies out of h_stage done
     uint64_t n_br = 0, n_ks = 0, n_launch = 0;
     int num_sms = 148;
+    size_t max_work = kMaxWorkPerLaunch;  // HEBNN_B200_MAX_WORK overrides (tests)
 };
 
 namespace {
@@ -989,6 +995,7 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
                                      (int)br_smem_bytes<kBrGates>()));
     HB_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
     e->num_sms = prop.multiProcessorCount;
+    if (const char *mw = std::getenv("HEBNN_B200_MAX_WORK")) e->max_work = std::max<size_t>(2, std::strtoull(mw, nullptr, 10));
 
     // BK -> Fourier
     const size_t npoly = (size_t)p->n * kRows * 2;
@@ -1101,6 +1108,8 @@ int hb_pool_gather(hb_engine *e, const uint32_t *slots, size_t count, uint32_t *
     return HB_OK;
 }
 
+static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_t lanes);
+
 int hb_run_gates(hb_engine *e, const hb_gate *gates, size_t n, uint32_t lanes) {
     if (!e || (n && !gates) || lanes == 0) {
         set_error("hb_run_gates: bad arguments");
@@ -1108,6 +1117,16 @@ int hb_run_gates(hb_engine *e, const hb_gate *gates, size_t n, uint32_t lanes) {
     }
     if (!n) return HB_OK;
     HB_CUDA_TRY(cudaSetDevice(e->device));
+    // gates of one level are independent: split very wide levels into chunks
+    const size_t per_chunk = std::max<size_t>(1, e->max_work / (2 * (size_t)lanes));
+    for (size_t off = 0; off < n; off += per_chunk) {
+        const int rc = run_gates_chunk(e, gates + off, std::min(per_chunk, n - off), lanes);
+        if (rc) return rc;
+    }
+    return HB_OK;
+}
+
+static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_t lanes) {
     // expand records into blind-rotation and key-switch work items
     size_t nbr = 0;
     for (size_t i = 0; i < n; i++) {

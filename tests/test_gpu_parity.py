@@ -114,3 +114,43 @@ def test_gpu_matches_committed_golden_vectors(engine, keys):
         assert np.array_equal(out[i], g[f"gate_{name}"]), name
     assert np.array_equal(out[len(names)], g["mux_010"])
     assert np.array_equal(out[len(names) + 1], g["mux_110"])
+
+
+def test_wide_level_split_into_chunks_is_identical(keys):
+    """hb_run_gates splits levels wider than the work limit into several
+    launches; the result must not depend on the split."""
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import os, sys, numpy as np
+sys.path.insert(0, os.getcwd())
+from paper_1806_03461_b200 import tfhe
+keys = tfhe.KeySet(seed=42)
+eng = tfhe.Engine(keys)
+n = 300
+rng = np.random.default_rng(4)
+eng.reserve(3 * n)
+eng.upload(0, keys.encrypt(rng.integers(0, 2, 2 * n).astype(np.uint8), seed=6, stream=1))
+recs = tfhe.gate_records(n)
+recs["dst"], recs["src_a"], recs["src_b"] = np.arange(2 * n, 3 * n), np.arange(n), np.arange(n, 2 * n)
+recs["kind"] = np.where(np.arange(n) % 3 == 0, 1, 0)
+recs["src_c"] = (np.arange(n) + 7) % n
+recs["c0"], recs["alpha"], recs["beta"] = tfhe.GATE_LIN["XOR"][0], 2, 2
+recs["alpha"][recs["kind"] == 1] = 1
+recs["beta"][recs["kind"] == 1] = 1
+recs["c0"][recs["kind"] == 1] = 0
+eng.run_gates(recs)
+np.save(sys.argv[1], eng.download(2 * n, n))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for mw in ("0", "64"):
+        path = f"/tmp/hb_chunk_{mw}.npy"
+        env = dict(os.environ)
+        if mw != "0":
+            env["HEBNN_B200_MAX_WORK"] = mw
+        subprocess.run([sys.executable, "-c", code, path], check=True, cwd=root, env=env)
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])

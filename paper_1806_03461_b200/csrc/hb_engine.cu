@@ -416,6 +416,10 @@ struct BrArgs {
 };
 
 constexpr int kStages = 3;  // BK rows in the shared-memory ring
+#ifndef HB_PAIR_UNROLL
+#define HB_PAIR_UNROLL 1
+#endif
+constexpr int kPairUnroll = HB_PAIR_UNROLL;
 #ifndef HB_EXP_SKIP
 #define HB_EXP_SKIP 0  // timing experiments only: 1 skip fwd FFT, 2 skip MAC, 4 skip inverse FFT
 #endif
@@ -531,7 +535,7 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
             }
         }
         double2 f0[8], f1[8];  // Fourier accumulators of the two output polys
-#pragma unroll 1
+#pragma unroll kPairUnroll
         for (int pr = 0; pr < kRows / 2; pr++, row_it += 2) {
 #if HB_BK_LDG
             {   // prefetch the next pair's two BK rows (32 KiB) into L1: 4 x 128-B lines per thread

@@ -417,7 +417,7 @@ struct BrArgs {
 
 constexpr int kStages = 3;  // BK rows in the shared-memory ring
 #ifndef HB_PAIR_UNROLL
-#define HB_PAIR_UNROLL 1
+#define HB_PAIR_UNROLL 3  // fully unrolled pair loop: rows (q, p) become compile-time
 #endif
 constexpr int kPairUnroll = HB_PAIR_UNROLL;
 #ifndef HB_EXP_SKIP

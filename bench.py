@@ -216,7 +216,7 @@ def run_reference(args, dist):
     if dist.rank != 0:
         return None
     threads = os.cpu_count() or 1
-    sample = 2 * threads
+    sample = 8 * threads  # ~1.3 s of wall time per step (~20 core-seconds)
     step, ok = cpu_nand_sample(args.seed, sample, threads)
     for _ in range(args.warmup):
         step()
@@ -370,7 +370,7 @@ def run_ours(args, dist):
             line["bnn"] = {"error": repr(exc)}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        sample = 2 * threads
+        sample = 8 * threads  # ~20 core-seconds of exact CGGI on the host
         step, ok = cpu_nand_sample(args.seed, sample, threads)
         dt = step()
         line["cpu_baseline"] = {"value": sample / dt, "unit": "gates/s", "cores": threads, "kind": "port",

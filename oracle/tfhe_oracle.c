@@ -156,26 +156,28 @@ void or_negacyclic_mul_schoolbook(int32_t N, const int32_t *a, const uint32_t *b
 #define GL_EPS 0xFFFFFFFFull
 
 static inline uint64_t gl_reduce128(unsigned __int128 x) {
-    uint64_t lo = (uint64_t)x, hi = (uint64_t)(x >> 64);
-    uint64_t hh = hi >> 32, hl = hi & GL_EPS;
+    /* branch-free Goldilocks reduction: 2^64 = 2^32 - 1, 2^96 = -1 (mod p) */
+    const uint64_t lo = (uint64_t)x, hi = (uint64_t)(x >> 64);
+    const uint64_t hh = hi >> 32, hl = hi & GL_EPS;
     uint64_t t0 = lo - hh;
-    if (lo < hh) t0 -= GL_EPS;
-    uint64_t t1 = hl * GL_EPS;
+    t0 -= (0 - (uint64_t)(lo < hh)) & GL_EPS;
+    const uint64_t t1 = hl * GL_EPS;
     uint64_t r = t0 + t1;
-    if (r < t1) r += GL_EPS;
-    if (r >= GL_P) r -= GL_P;
+    r += (0 - (uint64_t)(r < t1)) & GL_EPS;
+    r -= (0 - (uint64_t)(r >= GL_P)) & GL_P;
     return r;
 }
 static inline uint64_t gl_mul(uint64_t a, uint64_t b) {
     return gl_reduce128((unsigned __int128)a * b);
 }
 static inline uint64_t gl_add(uint64_t a, uint64_t b) {
-    uint64_t r = a + b;
-    if (r < a || r >= GL_P) r -= GL_P;
-    return r;
+    const uint64_t r = a + b;
+    const uint64_t over = (uint64_t)(r < a) | (uint64_t)(r >= GL_P);
+    return r - ((0 - over) & GL_P);
 }
 static inline uint64_t gl_sub(uint64_t a, uint64_t b) {
-    return a >= b ? a - b : a + (GL_P - b);
+    const uint64_t r = a - b;
+    return r + ((0 - (uint64_t)(a < b)) & GL_P);
 }
 static uint64_t gl_pow(uint64_t b, uint64_t e) {
     uint64_t r = 1;
@@ -202,6 +204,7 @@ typedef struct {
     uint64_t *w;             /* omega^j bit-reversed table for CT butterflies */
     uint64_t *winv;
     int *rev;                /* bit-reversal permutation */
+    uint64_t *ws, *wsinv;    /* per-stage contiguous twiddles: stage len -> [len/2] at offset len/2 - 1 */
 } ntt_plan;
 
 static int bitrev(int x, int bits) {
@@ -240,27 +243,41 @@ static void ntt_plan_init(ntt_plan *pl, int N) {
         x = gl_mul(x, omega);
         y = gl_mul(y, omega_inv);
     }
+    pl->ws = malloc(sizeof(uint64_t) * N);
+    pl->wsinv = malloc(sizeof(uint64_t) * N);
+    for (int len = 2; len <= N; len <<= 1) {
+        const int half = len >> 1, step = N / len;
+        for (int j = 0; j < half; j++) {
+            pl->ws[half - 1 + j] = pl->w[j * step];
+            pl->wsinv[half - 1 + j] = pl->winv[j * step];
+        }
+    }
 }
 
 static void ntt_plan_free(ntt_plan *pl) {
     free(pl->psi_pows); free(pl->psi_inv_pows); free(pl->w); free(pl->winv); free(pl->rev);
+    free(pl->ws); free(pl->wsinv);
 }
 
-/* in-place cyclic NTT, natural-order input -> natural-order output */
+/* in-place cyclic NTT, natural-order input -> natural-order output
+ * (bit reversal, then radix-2 Cooley-Tukey with contiguous per-stage twiddles) */
 static void ntt_core(const ntt_plan *pl, uint64_t *a, const uint64_t *w) {
-    int N = pl->N;
+    const int N = pl->N;
+    const uint64_t *stage_w = (w == pl->w) ? pl->ws : pl->wsinv;
     for (int i = 0; i < N; i++) {
         int j = pl->rev[i];
         if (j > i) { uint64_t t = a[i]; a[i] = a[j]; a[j] = t; }
     }
     for (int len = 2; len <= N; len <<= 1) {
-        int half = len >> 1, step = N / len;
+        const int half = len >> 1;
+        const uint64_t *ww = stage_w + half - 1;
         for (int s = 0; s < N; s += len) {
+            uint64_t *lo = a + s, *hi = a + s + half;
             for (int j = 0; j < half; j++) {
-                uint64_t u = a[s + j];
-                uint64_t v = gl_mul(a[s + j + half], w[j * step]);
-                a[s + j] = gl_add(u, v);
-                a[s + j + half] = gl_sub(u, v);
+                const uint64_t u = lo[j];
+                const uint64_t v = gl_mul(hi[j], ww[j]);
+                lo[j] = gl_add(u, v);
+                hi[j] = gl_sub(u, v);
             }
         }
     }
@@ -457,13 +474,16 @@ void or_modswitch(const or_ctx *c, const uint32_t *lwe, uint32_t *out) {
     for (int i = 0; i <= c->p.n; i++) out[i] = mod_switch(lwe[i], c->p.N);
 }
 
-/* gadget decomposition digit pp of x, in [-Bg/2, Bg/2) */
-static inline int32_t decomp_digit(uint32_t x, int pp, int bg_bits, int l) {
-    uint32_t half = 1u << (bg_bits - 1);
+/* gadget decomposition offset sum_q Bg/2 * 2^(32-(q+1)bg_bits) (tfhe tGswTorus32PolynomialDecompH) */
+static inline uint32_t decomp_offset(int bg_bits, int l) {
+    const uint32_t half = 1u << (bg_bits - 1);
     uint32_t offset = 0;
     for (int q = 0; q < l; q++) offset += half << (32 - (q + 1) * bg_bits);
-    uint32_t buf = x + offset;
-    return (int32_t)((buf >> (32 - (pp + 1) * bg_bits)) & ((1u << bg_bits) - 1)) - (int32_t)half;
+    return offset;
+}
+/* gadget decomposition digit pp of x (buf = x + offset), in [-Bg/2, Bg/2) */
+static inline int32_t decomp_digit(uint32_t buf, int pp, int bg_bits) {
+    return (int32_t)((buf >> (32 - (pp + 1) * bg_bits)) & ((1u << bg_bits) - 1)) - (int32_t)(1u << (bg_bits - 1));
 }
 
 /* ACC <- ACC + BK_i [x] ((X^a - 1) ACC), exact (CGGI CMux step) */
@@ -475,9 +495,10 @@ static void cmux_step(const or_ctx *c, int i, int a, uint32_t *acc, uint32_t *ro
         for (int j = 0; j < N; j++) rot[(size_t)q * N + j] -= acc[(size_t)q * N + j];
     }
     memset(sum, 0, sizeof(uint64_t) * (size_t)kp1 * N);
+    const uint32_t offset = decomp_offset(c->p.bg_bits, l);
     for (int row = 0; row < rows; row++) {
         int q = row / l, pp = row % l;
-        for (int j = 0; j < N; j++) dig[j] = decomp_digit(rot[(size_t)q * N + j], pp, c->p.bg_bits, l);
+        for (int j = 0; j < N; j++) dig[j] = decomp_digit(rot[(size_t)q * N + j] + offset, pp, c->p.bg_bits);
         ntt_forward_i64(&c->pl, dig, dig_ntt);
         const uint64_t *bkrow = c->bk_ntt + (((size_t)i * rows + row) * kp1) * N;
         for (int o = 0; o < kp1; o++)

@@ -13,6 +13,7 @@
 //                     tile of gates
 //   k_gather          pool slots -> contiguous buffer for download
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1123,10 +1124,15 @@ int hb_run_gates(hb_engine *e, const hb_gate *gates, size_t n, uint32_t lanes) {
     HB_CUDA_TRY(cudaSetDevice(e->device));
     // gates of one level are independent: split very wide levels into chunks
     const size_t per_chunk = std::max<size_t>(1, e->max_work / (2 * (size_t)lanes));
+    nvtxRangePushA("hb_run_gates");  // NVTX range per level (visible in nsys timelines)
     for (size_t off = 0; off < n; off += per_chunk) {
         const int rc = run_gates_chunk(e, gates + off, std::min(per_chunk, n - off), lanes);
-        if (rc) return rc;
+        if (rc) {
+            nvtxRangePop();
+            return rc;
+        }
     }
+    nvtxRangePop();
     return HB_OK;
 }
 

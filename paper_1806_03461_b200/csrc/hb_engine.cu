@@ -47,6 +47,11 @@ namespace {
 // ---------------------------------------------------------------------------
 
 constexpr int kXchStride = 520;  // double2 per exchange buffer (65-padded layout)
+#ifndef HB_EXP_SKIP
+// timing experiments only (results wrong): 1 skip fwd FFT, 2 skip MAC, 4 skip inverse FFT,
+// 8 skip rotation, 16 skip ACC update, 32/64 replace the 2nd/1st FFT barrier by __syncwarp
+#define HB_EXP_SKIP 0
+#endif
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -208,7 +213,7 @@ __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch
             for (int q = 0; q < NP; q++) xch[(2 * q) * kXchStride + j0 * 65 + k2 * 8 + j1] = cmul(x[q][rev3(k2)], T[k2]);
         }
     }
-    group_bar(bar_id);
+    if (HB_EXP_SKIP & 64) __syncwarp(); else group_bar(bar_id);
     {
         const int j0 = t & 7, k2 = t >> 3;
 #pragma unroll
@@ -227,7 +232,7 @@ __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch
                 xch[(2 * q + 1) * kXchStride + k2 * 65 + k1 * 8 + j0] = cmul(x[q][rev3(k1)], T[k1]);
         }
     }
-    group_bar(bar_id);
+    if (HB_EXP_SKIP & 32) __syncwarp(); else group_bar(bar_id);
     {
         const int k2 = t & 7, k1 = t >> 3;
 #pragma unroll
@@ -263,7 +268,7 @@ __device__ __forceinline__ void nega_fft_inv_n(double2 (&x)[NP][8], double2 *xch
             for (int q = 0; q < NP; q++) xch[(2 * q) * kXchStride + j0 * 65 + k2 * 8 + j1] = cmul(x[q][rev3(k2)], T[k2]);
         }
     }
-    group_bar(bar_id);
+    if (HB_EXP_SKIP & 64) __syncwarp(); else group_bar(bar_id);
     {
         const int j0 = t & 7, k2 = t >> 3;
 #pragma unroll
@@ -281,7 +286,7 @@ __device__ __forceinline__ void nega_fft_inv_n(double2 (&x)[NP][8], double2 *xch
                 xch[(2 * q + 1) * kXchStride + k2 * 65 + k1 * 8 + j0] = cmul(x[q][rev3(k1)], T[k1]);
         }
     }
-    group_bar(bar_id);
+    if (HB_EXP_SKIP & 32) __syncwarp(); else group_bar(bar_id);
     {
         const int k2 = t & 7, k1 = t >> 3;
 #pragma unroll
@@ -421,9 +426,7 @@ constexpr int kStages = 3;  // BK rows in the shared-memory ring
 #define HB_PAIR_UNROLL 3  // fully unrolled pair loop: rows (q, p) become compile-time
 #endif
 constexpr int kPairUnroll = HB_PAIR_UNROLL;
-#ifndef HB_EXP_SKIP
-#define HB_EXP_SKIP 0  // timing experiments only: 1 skip fwd FFT, 2 skip MAC, 4 skip inverse FFT
-#endif
+
 constexpr uint32_t kRowBytes = 2 * kNH * sizeof(double2);  // 16 KiB: one TGSW row, both output polys
 
 #ifndef HB_BK_LDG

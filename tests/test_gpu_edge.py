@@ -1,0 +1,81 @@
+"""Edge cases of the engine and the drop-in on the GPU: invalid records,
+empty levels, pool growth preserving contents, native MUX across lanes,
+NOT priced as XNOR, concurrent contexts sharing one engine."""
+
+import threading
+
+import numpy as np
+import pytest
+
+from hebnn import backend as ref_backend
+from paper_1806_03461_b200 import tfhe
+from paper_1806_03461_b200.backend import TfheContext
+
+pytestmark = pytest.mark.gpu
+
+
+def test_invalid_records_are_value_errors(engine, keys):
+    engine.reserve(8)
+    recs = tfhe.gate_records(1)
+    recs[0] = (2, 0, 1, 0, 0, 1, 1, 7, 0)  # unknown kind
+    with pytest.raises(ValueError, match="kind"):
+        engine.run_gates(recs)
+    recs[0] = (10 ** 9, 0, 1, 0, 0, 1, 1, 0, 0)  # slot beyond capacity
+    with pytest.raises(ValueError, match="capacity"):
+        engine.run_gates(recs)
+    engine.run_gates(tfhe.gate_records(0))  # empty level is a no-op
+    engine.sync()
+
+
+def test_pool_growth_preserves_contents(keys):
+    eng = tfhe.Engine(keys)
+    cts = keys.encrypt(np.array([1, 0, 1], np.uint8), seed=3)
+    eng.reserve(3)
+    eng.upload(0, cts)
+    eng.reserve(200_000)  # grow: old slots copied into the new allocation
+    assert eng.capacity >= 200_000
+    assert np.array_equal(eng.download(0, 3), cts)
+    eng.close()
+
+
+def test_native_mux_across_lanes():
+    lanes = 8
+    ctx = TfheContext(seed=42, lanes=lanes)
+    rng = np.random.default_rng(1)
+    S, A, B = (rng.integers(0, 2, lanes) for _ in range(3))
+    s, a, b = (ctx.encrypt_lanes(v) for v in (S, A, B))
+    m = ctx.g_mux(s, a, ctx.g_not(b))
+    assert list(ctx.decrypt(m)) == list(np.where(S == 1, A, 1 - B))
+    assert ctx.exec_stats["bootstraps"] == 2 * lanes  # one native MUX = 2 blind rotations per lane
+
+
+def test_not_priced_as_xnor_on_gpu(monkeypatch):
+    monkeypatch.setattr(ref_backend, "NOT_IS_FREE", False)
+    ctx = TfheContext(seed=42)
+    a = ctx.encrypt(1)
+    na = ctx.g_not(a)
+    assert ctx.global_stats.counts["XNOR"] == 1
+    assert ctx.decrypt(na) == 0 and ctx.decrypt(ctx.g_not(na)) == 1
+
+
+def test_concurrent_contexts_share_one_engine():
+    errors = []
+
+    def work(seed):
+        try:
+            ctx = TfheContext(seed=42)
+            rng = np.random.default_rng(seed)
+            bits = rng.integers(0, 2, (16, 2))
+            outs = [ctx.g_xor(ctx.encrypt(int(x)), ctx.encrypt(int(y))) for x, y in bits]
+            got = ctx.decrypt_many(outs)[:, 0]
+            if list(got) != list(bits[:, 0] ^ bits[:, 1]):
+                errors.append(seed)
+        except Exception as exc:  # pragma: no cover - reported below
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert errors == []

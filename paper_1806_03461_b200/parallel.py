@@ -20,10 +20,36 @@ from hebnn.compiler import EvalOptions, eval_model
 from hebnn.model import BatchNorm, ConvLayer, DenseLayer, SignActivation, TernaryModel, model_blocks
 
 
-def partition(count, world):
-    """Contiguous near-equal split of `count` output units over `world` ranks."""
-    bounds = [round(r * count / world) for r in range(world + 1)]
-    return [(bounds[r], bounds[r + 1]) for r in range(world)]
+def partition(count, world, costs=None):
+    """Contiguous split of `count` output units over `world` ranks: equal unit
+    counts, or — with per-unit `costs` (e.g. gates per neuron) — equal cost
+    (cfg4's ternary rows have very different DAG sizes)."""
+    if costs is None:
+        bounds = [round(r * count / world) for r in range(world + 1)]
+        return [(bounds[r], bounds[r + 1]) for r in range(world)]
+    costs = [max(0.0, float(c)) for c in costs]
+    total = sum(costs) or 1.0
+    bounds, acc, r = [0], 0.0, 1
+    for i, c in enumerate(costs):
+        acc += c
+        while r < world and acc >= r * total / world:
+            bounds.append(i + 1)
+            r += 1
+    while len(bounds) < world + 1:
+        bounds.append(count)
+    bounds[-1] = count
+    return [(bounds[k], max(bounds[k], bounds[k + 1])) for k in range(world)]
+
+
+def unit_costs(block, options=EvalOptions()):
+    """Predicted encrypted additions per output unit (compiler.plan_row), a
+    proxy for its gate count."""
+    from hebnn.compiler import plan_row
+    from hebnn.model import flat_filter
+
+    lin = block.linear
+    rows = lin.weights if isinstance(lin, DenseLayer) else [tuple(flat_filter(f)) for f in lin.filters]
+    return [plan_row(r, None, options).predicted_adds + 1 for r in rows]
 
 
 def _sub_block_model(block, lo, hi, output_mode, is_last):
@@ -67,10 +93,11 @@ class OutPEvaluator:
     list[np.ndarray]` (see `TorchComm`).
     """
 
-    def __init__(self, ctx_factory, comm, options=EvalOptions()):
+    def __init__(self, ctx_factory, comm, options=EvalOptions(), balance="gates"):
         self.ctx_factory = ctx_factory
         self.comm = comm
         self.options = options
+        self.balance = balance  # "gates" (predicted cost) or "units"
         self.stats = []
 
     def run(self, model, input_cts):
@@ -83,7 +110,8 @@ class OutPEvaluator:
         result = None
         for bi, block in enumerate(blocks):
             is_last = bi == len(blocks) - 1
-            lo, hi = partition(_units(block), self.comm.world)[self.comm.rank]
+            costs = unit_costs(block, self.options) if self.balance == "gates" else None
+            lo, hi = partition(_units(block), self.comm.world, costs)[self.comm.rank]
             ctx = self.ctx_factory()
             x = ctx.import_ciphertexts(cts)
             outs = []

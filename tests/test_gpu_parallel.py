@@ -69,4 +69,4 @@ def test_outp_two_ranks_on_gpu():
         assert p.exitcode == 0
     assert res[0][0] and res[1][0]
     assert res[0][1] == res[1][1]
-    assert res[0][2][0] == (0, 4) and res[1][2][0] == (4, 9)
+    assert res[0][2][0][0] == 0 and res[0][2][0][1] == res[1][2][0][0] and res[1][2][0][1] == 9

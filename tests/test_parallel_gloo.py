@@ -78,5 +78,17 @@ def test_outp_two_ranks_gloo(world):
     for rank in range(world):
         for mode, (ok, got, units) in res[rank].items():
             assert ok, (rank, mode, got)
-            assert units[0] == [(0, 4), (4, 7)][rank]  # 7 hidden units split 4 / 3
+            assert units[0][0] <= units[0][1]
     assert {m: v[1] for m, v in res[0].items()} == {m: v[1] for m, v in res[1].items()}
+
+
+def test_partition_balances_cost():
+    from paper_1806_03461_b200.parallel import partition
+
+    assert partition(7, 2) == [(0, 4), (4, 7)]
+    # one expensive unit first: cost-balanced split puts it alone
+    parts = partition(5, 2, costs=[10, 1, 1, 1, 1])
+    assert parts == [(0, 1), (1, 5)]
+    parts = partition(10, 4, costs=[1] * 10)
+    assert sum(h - l for l, h in parts) == 10 and all(h >= l for l, h in parts)
+    assert partition(2, 4, costs=[1, 1])[-1][1] == 2

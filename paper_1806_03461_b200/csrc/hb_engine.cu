@@ -667,6 +667,168 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
 }
 
 // ---------------------------------------------------------------------------
+// Latency mode (narrow levels): one bootstrap per CTA, three 64-thread groups.
+// Group r takes TGSW rows 2r, 2r+1 of every CMux step (one dual forward FFT +
+// MAC into a partial Fourier accumulator); groups 0/1 then sum the three
+// partials of output polynomial 0/1, run its inverse FFT and update ACC.  The
+// per-step critical path is one dual FFT instead of three.  Each group's two
+// BK rows (32 KiB) arrive by cp.async.bulk into its own buffer, issued as soon
+// as the previous step's partials have been consumed.  Bit-identical to the
+// throughput kernel (different FP64 summation order; every rounding exact).
+// ---------------------------------------------------------------------------
+struct BrLatSmem {
+    double2 bk[3][2][2 * kNH];               // per group: 2 rows x 2 output polys (32 KiB); reused for partials
+    uint64_t full[3];
+    uint32_t acc[2][kN];
+    double2 xch[3][2][2][kXchStride];        // per group dual-FFT exchange buffers
+    uint16_t bar[kMaxLweN + 1];
+    TwSeeds tws[64];
+};
+
+template <bool kDebug>
+__global__ void __launch_bounds__(192, 1) k_blind_rotate_lat(const BrArgs args) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    BrLatSmem &sm = *reinterpret_cast<BrLatSmem *>(smem_raw);
+    const int warp = threadIdx.x >> 5;
+    const int grp = warp >> 1;          // 0..2
+    const int t = threadIdx.x & 63;
+    const int bar_id = 1 + grp;
+    const int n = args.n;
+    const int iters = min(n, args.iters);
+    const char *bk_src = reinterpret_cast<const char *>(args.bkf);
+    const uint32_t e = blockIdx.x;      // one bootstrap per CTA (grid == n_work)
+    uint32_t *accA = sm.acc[0];
+    uint32_t *accB = sm.acc[1];
+    double2 *xch = &sm.xch[grp][0][0][0];
+
+    if (threadIdx.x < 64) {
+        TwSeeds ts;
+        ts.f_a0 = args.TW[t];
+        ts.step_a = args.W[t];
+        ts.step_b = args.W[8 * (t & 7)];
+        ts.i_b0 = args.TW[t >> 3];
+        ts.i_stepb = args.TW[32 * (t & 7) + 8];
+        sm.tws[t] = ts;
+    }
+    // this group's rows of step 0
+    if (t == 0) {
+        mbar_init(&sm.full[grp], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (iters > 0) {
+            mbar_arrive_expect_tx(&sm.full[grp], 2 * kRowBytes);
+            bulk_g2s(sm.bk[grp], bk_src + (size_t)(2 * grp) * kRowBytes, 2 * kRowBytes, &sm.full[grp]);
+        }
+    }
+    {   // K1: linear combination + modulus switch (all 192 threads)
+        const uint32_t lanes = args.lanes;
+        const BrItem it = args.items[e / lanes];
+        const uint32_t lane_id = e % lanes;
+        const int alpha = (int8_t)(it.coef & 0xFF), beta = (int8_t)((it.coef >> 8) & 0xFF);
+        const uint32_t *A = args.pool + ((size_t)it.src_a * lanes + lane_id) * args.pool_stride;
+        const uint32_t *B = args.pool + ((size_t)it.src_b * lanes + lane_id) * args.pool_stride;
+        for (int c = threadIdx.x; c <= n; c += 192) {
+            uint32_t v = (uint32_t)alpha * __ldg(&A[c]);
+            if (beta) v += (uint32_t)beta * __ldg(&B[c]);
+            if (c == n) v += it.c0;
+            sm.bar[c] = (uint16_t)(((v + (1u << 20)) >> 21) & (2 * kN - 1));
+        }
+    }
+    __syncthreads();
+    {
+        const int barb = sm.bar[n];
+        for (int i = threadIdx.x; i < kN; i += 192) {
+            accA[i] = 0;
+            accB[i] = (((i + barb) & kN) ? 0u - args.mu : args.mu);
+        }
+    }
+    __syncthreads();
+
+    double max_err = 0.0;
+    for (int i = 0; i < iters; i++) {
+        const int a = sm.bar[i];
+        // digits of this group's two rows: row = 2 grp + h, q = row / 3, p = row % 3
+        double2 x[2][8];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int row = 2 * grp + h;
+            const int q = row / kL, p = row % kL;
+            const uint32_t *P = q ? accB : accA;
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                const int j = t + 64 * m;
+                const uint32_t lo = rot_coef(P, j, a) - P[j];
+                const uint32_t hi = rot_coef(P, j + kNH, a) - P[j + kNH];
+                x[h][m] = make_double2(small_int_to_double(gadget_digit(lo, p)),
+                                       small_int_to_double(gadget_digit(hi, p)));
+            }
+        }
+        nega_fft_fwd_n<2>(x, xch, t, sm.tws[t], bar_id);
+        mbar_wait(&sm.full[grp], i & 1);
+        double2 f0[8], f1[8];
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+            const double2 *b0 = sm.bk[grp][0], *b1 = sm.bk[grp][1];
+            f0[m] = cmul(x[0][m], b0[t + 64 * m]);
+            f1[m] = cmul(x[0][m], b0[kNH + t + 64 * m]);
+            cmac(f0[m], x[1][m], b1[t + 64 * m]);
+            cmac(f1[m], x[1][m], b1[kNH + t + 64 * m]);
+        }
+        group_bar(bar_id);  // all MAC reads of this group's BK buffer done
+        // partials overwrite the (consumed) BK buffer: [0][.] = output poly 0, [1][.] = output poly 1
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+            sm.bk[grp][0][t + 64 * m] = f0[m];
+            sm.bk[grp][1][t + 64 * m] = f1[m];
+        }
+        __syncthreads();
+        if (grp < 2) {
+            // group o sums the three partials of output polynomial o, inverse FFT, ACC update
+            double2 y[1][8];
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                const int k = t + 64 * m;
+                y[0][m] = cadd(cadd(sm.bk[0][grp][k], sm.bk[1][grp][k]), sm.bk[2][grp][k]);
+            }
+            nega_fft_inv_n<1>(y, xch, t, sm.tws[t], bar_id);
+            uint32_t *P = grp ? accB : accA;
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                const double lo = y[0][m].x, hi = y[0][m].y;
+                if (kDebug) {
+                    max_err = fmax(max_err, fabs(lo - rint(lo)));
+                    max_err = fmax(max_err, fabs(hi - rint(hi)));
+                }
+                const int j = t + 64 * m;
+                P[j] += round_to_torus(lo);
+                P[j + kNH] += round_to_torus(hi);
+            }
+        }
+        __syncthreads();  // partials consumed, ACC updated
+        if (t == 0 && i + 1 < iters) {  // next step's rows for this group
+            // generic-proxy reads/writes of this buffer (MAC, partials) before the async-proxy refill
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive_expect_tx(&sm.full[grp], 2 * kRowBytes);
+            bulk_g2s(sm.bk[grp], bk_src + (size_t)((i + 1) * kRows + 2 * grp) * kRowBytes, 2 * kRowBytes,
+                     &sm.full[grp]);
+        }
+    }
+
+    if (kDebug && args.margin) atomicMax(args.margin, (unsigned long long)__double_as_longlong(max_err));
+    if (kDebug && args.acc_dump) {
+        uint32_t *dst = args.acc_dump + (size_t)e * 2 * kN;
+        for (int c = threadIdx.x; c < 2 * kN; c += 192) dst[c] = (c < kN) ? accA[c] : accB[c - kN];
+    }
+    uint32_t *out = args.big + (size_t)e * kBigStride;
+    for (int c = threadIdx.x; c <= kN; c += 192) {
+        uint32_t v;
+        if (c == 0) v = accA[0];
+        else if (c < kN) v = 0u - accA[kN - c];
+        else v = accB[0];
+        out[c] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K4: batched key switch.  For coefficient i the CGGI digits are the eight
 // base-4 digits of w_i = (a'_i + 2^15) >> 16.  The device KSK is laid out as a
 // lookup table per 8-column chunk, T[chunk][i][j][d][8] with T[..][0][..] = 0,
@@ -875,6 +1037,7 @@ struct hb_engine {
     uint64_t n_br = 0, n_ks = 0, n_launch = 0;
     int num_sms = 148;
     size_t max_work = kMaxWorkPerLaunch;  // HEBNN_B200_MAX_WORK overrides (tests)
+    bool latency_mode = true;             // HEBNN_B200_LATENCY_MODE=0 disables (A/B tests)
 };
 
 namespace {
@@ -915,6 +1078,14 @@ int launch_br(hb_engine *e, const BrArgs &a) {
     const size_t smem = br_smem_bytes<G>();
     const unsigned grid = (a.n_work + G - 1) / G;
     k_blind_rotate<G, kDebug><<<grid, 64 * G, smem, e->stream>>>(a);
+    HB_CUDA_TRY(cudaGetLastError());
+    e->n_launch++;
+    return HB_OK;
+}
+
+template <bool kDebug>
+int launch_br_lat(hb_engine *e, const BrArgs &a) {
+    k_blind_rotate_lat<kDebug><<<a.n_work, 192, sizeof(BrLatSmem), e->stream>>>(a);
     HB_CUDA_TRY(cudaGetLastError());
     e->n_launch++;
     return HB_OK;
@@ -1001,9 +1172,14 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
                                      (int)br_smem_bytes<1>()));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)br_smem_bytes<kBrGates>()));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_lat<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrLatSmem)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_lat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrLatSmem)));
     HB_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
     e->num_sms = prop.multiProcessorCount;
     if (const char *mw = std::getenv("HEBNN_B200_MAX_WORK")) e->max_work = std::max<size_t>(2, std::strtoull(mw, nullptr, 10));
+    if (const char *lm = std::getenv("HEBNN_B200_LATENCY_MODE")) e->latency_mode = std::atoi(lm) != 0;
 
     // BK -> Fourier
     const size_t npoly = (size_t)p->n * kRows * 2;
@@ -1192,8 +1368,11 @@ static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_
     a.items = e->d_br;
     a.n_work = (uint32_t)(nbr * lanes);
     HB_CUDA_TRY(cudaEventRecord(e->ev[0], e->stream));
-    // narrow levels (latency-bound): fewer bootstraps per CTA so each gets an SM of its own
-    if (a.n_work <= (uint32_t)e->num_sms) {
+    // narrow levels (latency-bound): one bootstrap per CTA split over three
+    // thread groups (latency mode), or fewer bootstraps per CTA
+    if (a.n_work <= (uint32_t)e->num_sms && e->latency_mode) {
+        if ((rc = launch_br_lat<false>(e, a))) return rc;
+    } else if (a.n_work <= (uint32_t)e->num_sms) {
         if ((rc = launch_br<1, false>(e, a))) return rc;
     } else if (a.n_work <= 2u * (uint32_t)e->num_sms) {
         if ((rc = launch_br<2, false>(e, a))) return rc;

@@ -485,33 +485,43 @@ class TfheContext(GateBackend):
     def _build_schedule(self, pending):
         if not pending:
             return []
-        ids = np.asarray(pending, dtype=np.int64)
-        op = np.asarray(self._op, dtype=np.int8)[ids]
-        a = np.asarray(self._a, dtype=np.int64)[ids]
-        b = np.asarray(self._b, dtype=np.int64)[ids]
-        c = np.asarray(self._c, dtype=np.int64)[ids]
-        lvl = np.asarray(self._lvl, dtype=np.int64)[ids]
-        slot = np.asarray(self._slot, dtype=np.int64)
-        live = slot >= 0
-        slot[live] = self._map_slots(slot[live])
-        recs = np.zeros(ids.size, dtype=GATE_DTYPE)
-        recs["dst"] = slot[ids]
-        recs["src_a"] = slot[a >> 1]
-        recs["src_b"] = slot[b >> 1]
+        if 8 * len(pending) < len(self._op):
+            # small flush on a large DAG: gather only what the pending nodes touch
+            op = np.fromiter((self._op[i] for i in pending), np.int8, len(pending))
+            a = np.fromiter((self._a[i] for i in pending), np.int64, len(pending))
+            b = np.fromiter((self._b[i] for i in pending), np.int64, len(pending))
+            c = np.fromiter((self._c[i] for i in pending), np.int64, len(pending))
+            lvl = np.fromiter((self._lvl[i] for i in pending), np.int64, len(pending))
+            sl = self._slot
+            dst = np.fromiter((sl[i] for i in pending), np.int64, len(pending))
+            s_a = np.fromiter((sl[r >> 1] for r in a.tolist()), np.int64, len(pending))
+            s_b = np.fromiter((sl[r >> 1] for r in b.tolist()), np.int64, len(pending))
+            s_c = np.fromiter((sl[r >> 1] for r in c.tolist()), np.int64, len(pending))
+        else:
+            ids = np.asarray(pending, dtype=np.int64)
+            op = np.asarray(self._op, dtype=np.int8)[ids]
+            a = np.asarray(self._a, dtype=np.int64)[ids]
+            b = np.asarray(self._b, dtype=np.int64)[ids]
+            c = np.asarray(self._c, dtype=np.int64)[ids]
+            lvl = np.asarray(self._lvl, dtype=np.int64)[ids]
+            slot = np.asarray(self._slot, dtype=np.int64)
+            dst, s_a, s_b, s_c = slot[ids], slot[a >> 1], slot[b >> 1], slot[c >> 1]
         is_and = op == _OP_AND
         is_xor = op == _OP_XOR
         is_mux = op == _OP_MUX
+        recs = np.zeros(op.size, dtype=GATE_DTYPE)
+        recs["dst"] = self._map_slots(dst)
+        recs["src_a"] = self._map_slots(s_a)
+        recs["src_b"] = self._map_slots(s_b)
+        # MUX records: src_a = selector, src_b = a, src_c = b (refs a/b/c of the node)
+        recs["src_c"] = np.where(is_mux, self._map_slots(np.where(s_c >= 0, s_c, 0)), 0)
         sa = 1 - 2 * (a & 1)
         sb = 1 - 2 * (b & 1)
         recs["kind"] = np.where(is_mux, GATE_MUX, GATE_LIN2)
         recs["c0"] = np.where(is_and, _C_AND, np.where(is_xor, _C_XOR, 0)).astype(np.uint32)
-        # AND: signs of the refs; XOR: 2, 2; MUX: S = src_a (positive), alpha/beta = signs of a / b
+        # AND: signs of the refs; XOR: 2, 2; MUX: selector positive, alpha/beta = signs of a / b
         recs["alpha"] = np.where(is_and, sa, np.where(is_xor, 2, sb))
         recs["beta"] = np.where(is_and, sb, np.where(is_xor, 2, 1 - 2 * (c & 1)))
-        recs["src_c"] = np.where(is_mux, slot[c >> 1], 0)
-        # MUX records: src_a = selector, src_b = a, src_c = b
-        recs["src_a"] = np.where(is_mux, slot[a >> 1], recs["src_a"])
-        recs["src_b"] = np.where(is_mux, slot[b >> 1], recs["src_b"])
         order = np.argsort(lvl, kind="stable")
         lvl_sorted = lvl[order]
         bounds = np.flatnonzero(np.diff(lvl_sorted)) + 1

@@ -328,19 +328,30 @@ def run_ours(args, dist):
     total_s = dist.max(sum(step_ms) / 1e3)
     value = n * dist.world * args.steps / total_s
 
-    # e2e through the C ABI with host buffers
+    # e2e through the C ABI with host buffers: every step uploads its inputs from
+    # pinned memory and downloads its outputs; the copies run on the engine's
+    # copy streams, overlapping the neighbouring steps' compute (two slot
+    # regions, double-buffered host staging)
     dist.barrier()
-    e2e_times = []
-    for _ in range(args.steps):
-        eng.sync()
-        t0 = time.perf_counter()
-        eng.upload(0, h_in)
-        eng.run_gates(recs)
-        tfhe.lib().hb_pool_download(eng._e, 2 * n, n, tfhe.u32p(h_out), words)
-        e2e_times.append(time.perf_counter() - t0)
-    e2e_total = dist.max(sum(e2e_times))
+    eng.reserve(6 * n)
+    h_in2 = [h_in, torch.empty((2 * n, words), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)]
+    h_in2[1][:] = h_in
+    h_out2 = [h_out, torch.empty((n, words), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)]
+    recs2 = [recs, recs.copy()]
+    for f in ("dst", "src_a", "src_b"):
+        recs2[1][f] = recs[f] + 3 * n
+    eng.sync()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        r = k % 2
+        eng.upload_async(3 * n * r, h_in2[r])
+        eng.run_gates(recs2[r])
+        eng.download_async(3 * n * r + 2 * n, h_out2[r])
+    eng.sync()
+    e2e_total = dist.max(time.perf_counter() - t0)
     e2e_value = n * dist.world * args.steps / e2e_total
-    correct &= bool(np.array_equal(keys.decrypt(h_out), 1 - (a & b)))
+    correct &= bool(np.array_equal(keys.decrypt(h_out2[0]), 1 - (a & b)))
+    correct &= bool(np.array_equal(keys.decrypt(h_out2[1]), 1 - (a & b))) or args.steps < 2
 
     br_med = statistics.median(br_ms)
     achieved = n * F_BS / (br_med / 1e3) / 1e12
@@ -353,7 +364,8 @@ def run_ours(args, dist):
         "config": {"workload": WORKLOAD, "gates_per_gpu": n, "parallelism": f"replicated keys, {dist.world} GPU(s)",
                    "l2": "flushed (256 MiB write) before every timed step", "inputs": "resident in HBM"},
         "e2e": {"value": e2e_value, "unit": "gates/s", "h2d_bytes_per_step": int(h_in.nbytes + recs.nbytes),
-                "d2h_bytes_per_step": int(h_out.nbytes)},
+                "d2h_bytes_per_step": int(h_out.nbytes),
+                "note": "C ABI, pinned host buffers, H2D/D2H on copy streams overlapping neighbouring steps"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic, "traffic_source": traffic_src,

@@ -120,6 +120,16 @@ int hb_pool_upload(hb_engine *e, size_t first_slot, size_t count, const uint32_t
                    size_t host_stride);
 int hb_pool_download(hb_engine *e, size_t first_slot, size_t count, uint32_t *host,
                      size_t host_stride);
+/* Asynchronous variants on the engine's copy streams (overlap transfers with
+ * compute; host buffers must be pinned and stay valid until hb_sync).  An
+ * async upload may overlap the most recently issued level but waits for every
+ * earlier one (double-buffered slot regions); the next hb_run_gates waits for
+ * the last async upload; an async download waits for every level issued
+ * before it. */
+int hb_pool_upload_async(hb_engine *e, size_t first_slot, size_t count, const uint32_t *host,
+                         size_t host_stride);
+int hb_pool_download_async(hb_engine *e, size_t first_slot, size_t count, uint32_t *host,
+                           size_t host_stride);
 /* scattered slots -> host (gathered on the device, one copy) */
 int hb_pool_gather(hb_engine *e, const uint32_t *slots, size_t count, uint32_t *host,
                    size_t host_stride);
@@ -129,7 +139,7 @@ int hb_pool_gather(hb_engine *e, const uint32_t *slots, size_t count, uint32_t *
  * sample extract, then batched key switch into pool[dst].  Very wide levels
  * (> 2^20 blind rotations x lanes) are split into several launches. */
 int hb_run_gates(hb_engine *e, const hb_gate *gates, size_t n, uint32_t lanes);
-int hb_sync(hb_engine *e);
+int hb_sync(hb_engine *e);  /* compute and copy streams */
 
 /* Device time (ms, CUDA events on the engine stream) of the blind-rotation and
  * key-switch kernels of the most recent hb_run_gates launch (its last chunk);

@@ -1012,6 +1012,12 @@ struct hb_engine {
     int device = 0;
     hb_params p{};
     cudaStream_t stream = nullptr;
+    cudaStream_t h2d_stream = nullptr;    // async uploads overlapping the compute stream
+    cudaStream_t d2h_stream = nullptr;    // async downloads
+    cudaEvent_t ev_upload = nullptr;      // last async upload (the next level waits on it)
+    cudaEvent_t ev_compute = nullptr;     // compute point an async download waits on
+    cudaEvent_t ev_prev_level = nullptr;  // compute stream before the most recent level
+    bool pending_upload = false;
     double2 *d_W = nullptr, *d_TW = nullptr;
     double2 *d_bkf = nullptr;
     uint32_t *d_ksk = nullptr;
@@ -1148,6 +1154,12 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
     HB_CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     for (auto &ev : e->ev) HB_CUDA_TRY(cudaEventCreate(&ev));
     HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_stage, cudaEventDisableTiming));
+    HB_CUDA_TRY(cudaStreamCreateWithFlags(&e->h2d_stream, cudaStreamNonBlocking));
+    HB_CUDA_TRY(cudaStreamCreateWithFlags(&e->d2h_stream, cudaStreamNonBlocking));
+    HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_upload, cudaEventDisableTiming));
+    HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_compute, cudaEventDisableTiming));
+    HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_prev_level, cudaEventDisableTiming));
+    HB_CUDA_TRY(cudaEventRecord(e->ev_prev_level, e->stream));
     HB_CUDA_TRY(cudaEventRecord(e->ev_stage, e->stream));
 
     // twiddle tables, computed in long double then rounded
@@ -1218,6 +1230,13 @@ int hb_engine_destroy(hb_engine *e) {
     for (auto &ev : e->ev)
         if (ev) cudaEventDestroy(ev);
     if (e->ev_stage) cudaEventDestroy(e->ev_stage);
+    for (cudaStream_t st : {e->h2d_stream, e->d2h_stream})
+        if (st) {
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
+        }
+    for (cudaEvent_t ev : {e->ev_upload, e->ev_compute, e->ev_prev_level})
+        if (ev) cudaEventDestroy(ev);
     if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
     return HB_OK;
@@ -1362,6 +1381,11 @@ static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_
     HB_CUDA_TRY(cudaMemcpyAsync(e->d_br, hbr, br_bytes, cudaMemcpyHostToDevice, e->stream));
     HB_CUDA_TRY(cudaMemcpyAsync(e->d_ks, hks, ks_bytes, cudaMemcpyHostToDevice, e->stream));
     HB_CUDA_TRY(cudaEventRecord(e->ev_stage, e->stream));
+    HB_CUDA_TRY(cudaEventRecord(e->ev_prev_level, e->stream));  // "everything before this level"
+    if (e->pending_upload) {  // inputs staged by hb_pool_upload_async
+        HB_CUDA_TRY(cudaStreamWaitEvent(e->stream, e->ev_upload, 0));
+        e->pending_upload = false;
+    }
 
     BrArgs a = br_args(e);
     a.lanes = lanes;
@@ -1400,6 +1424,39 @@ int hb_sync(hb_engine *e) {
     if (!e) return HB_EINVAL;
     HB_CUDA_TRY(cudaSetDevice(e->device));
     HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    HB_CUDA_TRY(cudaStreamSynchronize(e->h2d_stream));
+    HB_CUDA_TRY(cudaStreamSynchronize(e->d2h_stream));
+    return HB_OK;
+}
+
+int hb_pool_upload_async(hb_engine *e, size_t first, size_t count, const uint32_t *host, size_t host_stride) {
+    if (!e || (count && !host) || host_stride < (size_t)e->p.n + 1 || first + count > e->pool_cap) {
+        set_error("hb_pool_upload_async: bad arguments or slot range beyond capacity");
+        return HB_EINVAL;
+    }
+    if (!count) return HB_OK;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    // may overlap the most recently issued level, never an earlier one (double buffering)
+    HB_CUDA_TRY(cudaStreamWaitEvent(e->h2d_stream, e->ev_prev_level, 0));
+    HB_CUDA_TRY(cudaMemcpy2DAsync(e->d_pool + first * e->pool_stride, e->pool_stride * 4, host, host_stride * 4,
+                                  (size_t)(e->p.n + 1) * 4, count, cudaMemcpyHostToDevice, e->h2d_stream));
+    HB_CUDA_TRY(cudaEventRecord(e->ev_upload, e->h2d_stream));
+    e->pending_upload = true;
+    return HB_OK;
+}
+
+int hb_pool_download_async(hb_engine *e, size_t first, size_t count, uint32_t *host, size_t host_stride) {
+    if (!e || (count && !host) || host_stride < (size_t)e->p.n + 1 || first + count > e->pool_cap) {
+        set_error("hb_pool_download_async: bad arguments or slot range beyond capacity");
+        return HB_EINVAL;
+    }
+    if (!count) return HB_OK;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    // everything issued so far on the compute stream (the levels producing these slots)
+    HB_CUDA_TRY(cudaEventRecord(e->ev_compute, e->stream));
+    HB_CUDA_TRY(cudaStreamWaitEvent(e->d2h_stream, e->ev_compute, 0));
+    HB_CUDA_TRY(cudaMemcpy2DAsync(host, host_stride * 4, e->d_pool + first * e->pool_stride, e->pool_stride * 4,
+                                  (size_t)(e->p.n + 1) * 4, count, cudaMemcpyDeviceToHost, e->d2h_stream));
     return HB_OK;
 }
 

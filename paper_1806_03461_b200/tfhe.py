@@ -153,6 +153,16 @@ class Engine:
         return out
 
     @_locked
+    def upload_async(self, first, cts):
+        """Pinned host array -> pool on the copy stream (returns immediately)."""
+        check(lib().hb_pool_upload_async(self._e, int(first), cts.shape[0], u32p(cts), cts.shape[1]))
+
+    @_locked
+    def download_async(self, first, out):
+        """Pool -> pinned host array `out` [count][>=n+1] after all issued levels."""
+        check(lib().hb_pool_download_async(self._e, int(first), out.shape[0], u32p(out), out.shape[1]))
+
+    @_locked
     def gather(self, slots):
         slots = np.ascontiguousarray(slots, dtype=np.uint32)
         out = np.zeros((slots.size, self.params.n + 1), np.uint32)

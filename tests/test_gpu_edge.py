@@ -79,3 +79,36 @@ def test_concurrent_contexts_share_one_engine():
     for t in threads:
         t.join()
     assert errors == []
+
+
+def test_async_double_buffered_transfers(keys):
+    """hb_pool_upload_async / hb_pool_download_async overlapping consecutive
+    levels on two slot regions give the same results as synchronous copies."""
+    import torch
+
+    eng = tfhe.Engine(keys)
+    n, words = 64, keys.params.n + 1
+    rng = np.random.default_rng(9)
+    steps = 5
+    bits = [rng.integers(0, 2, 2 * n).astype(np.uint8) for _ in range(steps)]
+    h_in = [torch.empty((2 * n, words), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32) for _ in range(steps)]
+    h_out = [torch.empty((n, words), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32) for _ in range(steps)]
+    for k in range(steps):
+        h_in[k][:] = keys.encrypt(bits[k], seed=20 + k)
+    eng.reserve(6 * n)
+    c0, al, be = tfhe.GATE_LIN["XOR"]
+    recs = []
+    for r in range(2):
+        rc = tfhe.gate_records(n)
+        rc["dst"], rc["src_a"], rc["src_b"] = 3 * n * r + 2 * n + np.arange(n), 3 * n * r + np.arange(n), 3 * n * r + n + np.arange(n)
+        rc["c0"], rc["alpha"], rc["beta"] = c0, al, be
+        recs.append(rc)
+    for k in range(steps):
+        r = k % 2
+        eng.upload_async(3 * n * r, h_in[k])
+        eng.run_gates(recs[r])
+        eng.download_async(3 * n * r + 2 * n, h_out[k])
+    eng.sync()
+    for k in range(steps):
+        assert np.array_equal(keys.decrypt(h_out[k]), bits[k][:n] ^ bits[k][n:]), k
+    eng.close()

@@ -252,6 +252,7 @@ def bnn_latency(kind, seed):
     warm.decrypt(warm.g_and(warm.encrypt(1), warm.encrypt(1)))  # CUDA context, BK FFT, KSK upload
     rep = workloads.run_encrypted(TfheContext, cfg, seed=seed)
     rep["note"] = "latency_s = device flush + decrypt of one batch; DAG build reported separately"
+    rep["reference_cpu"] = workloads.run_sim_reference(cfg, seed=seed)
     return rep
 
 
@@ -389,6 +390,8 @@ def run_ours(args, dist):
                                 "sample": f"{sample} NAND gates on {threads} threads ({cpu_model()}), "
                                           f"{dt:.1f} s; exact-integer CGGI oracle (reference has no crypto)",
                                 "correct": ok()}
+        step1, _ = cpu_nand_sample(args.seed + 1, 8, 1)
+        line["cpu_baseline"]["single_thread_value"] = 8 / step1()
     eng.close()
     return line
 

@@ -75,6 +75,23 @@ def decode_outputs(ctx, outs):
     return np.where(bits.T == 1, 1, -1)
 
 
+def run_sim_reference(config, seed=0, options=EvalOptions()):
+    """The reference's own CPU path for the same workload: SimContext +
+    eval_model (plaintext gate simulation, backend.py:162-237 and
+    compiler.py eval_model), one input.  Reported beside the encrypted run."""
+    from hebnn.backend import SimContext
+
+    model, batch = build(config, seed)
+    X = inputs(config, model, batch, seed + 1)
+    ctx = SimContext()
+    t0 = time.perf_counter()
+    xs = [ctx.encrypt(int(v)) for v in X[0]]
+    outs, _ = eval_model(ctx, model, xs, options)
+    dt = time.perf_counter() - t0
+    return {"kind": "reference SimContext (plaintext, 1 thread)", "inputs": 1, "seconds_per_input": dt,
+            "counted_gates_per_input": ctx.gate_count, "counted_gates_per_s": ctx.gate_count / dt}
+
+
 def run_encrypted(ctx_cls, config, seed=0, device=0, options=EvalOptions(), check=True, replays=0):
     """Encrypt a batch, evaluate through the reference compiler on a
     lane-batched context, decrypt, compare with oracle_eval.  Returns a report."""

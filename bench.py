@@ -357,6 +357,9 @@ def run_ours(args, dist):
     br_med = statistics.median(br_ms)
     achieved = n * F_BS / (br_med / 1e3) / 1e12
     traffic, traffic_src = last_profiled_traffic()
+    # nominal FP64 peak: 64 DFMA lanes per SM x 2 flops x max SM clock
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    nominal = sms * 128 * clk["sm_max_mhz"] * 1e6 / 1e12 if clk.get("sm_max_mhz") else None
     line = {
         "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": dist.world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dist.max(statistics.mean(step_ms)), "higher_is_better": True,
@@ -371,7 +374,8 @@ def run_ours(args, dist):
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": "k_blind_rotate", "flops_per_bootstrap": F_BS,
-                     "peak_source": "DFMA micro-benchmark in this run (MEASURED_PEAKS.json has no FP64 figure)"},
+                     "peak_source": "DFMA micro-benchmark in this run (MEASURED_PEAKS.json has no FP64 figure)",
+                     "peak_nominal": nominal, "frac_of_nominal": (achieved / nominal) if nominal else None},
         "kernel_ms": {"blind_rotate": br_med, "key_switch": statistics.median(ks_ms)},
         "clocks": clk,
         "correct": correct,

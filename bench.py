@@ -351,6 +351,15 @@ def run_ours(args, dist):
     eng.sync()
     e2e_total = dist.max(time.perf_counter() - t0)
     e2e_value = n * dist.world * args.steps / e2e_total
+    # the same without overlap: blocking upload -> gates -> blocking download per step
+    dist.barrier()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        eng.upload(0, h_in)
+        eng.run_gates(recs)
+        eng.download(2 * n, n, out=h_out)
+    e2e_serial = n * dist.world * args.steps / dist.max(time.perf_counter() - t0)
+    correct &= bool(np.array_equal(keys.decrypt(h_out), 1 - (a & b)))
     correct &= bool(np.array_equal(keys.decrypt(h_out2[0]), 1 - (a & b)))
     correct &= bool(np.array_equal(keys.decrypt(h_out2[1]), 1 - (a & b))) or args.steps < 2
 
@@ -369,7 +378,9 @@ def run_ours(args, dist):
                    "l2": "flushed (256 MiB write) before every timed step", "inputs": "resident in HBM"},
         "e2e": {"value": e2e_value, "unit": "gates/s", "h2d_bytes_per_step": int(h_in.nbytes + recs.nbytes),
                 "d2h_bytes_per_step": int(h_out.nbytes),
-                "note": "C ABI, pinned host buffers, H2D/D2H on copy streams overlapping neighbouring steps"},
+                "serial_value": e2e_serial,
+                "note": "C ABI, pinned host buffers, H2D/D2H on copy streams overlapping neighbouring steps; "
+                        "serial_value: blocking copies, no overlap"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic, "traffic_source": traffic_src,

@@ -147,8 +147,13 @@ class Engine:
         check(lib().hb_pool_upload(self._e, int(first), cts.shape[0], u32p(cts), cts.shape[1]))
 
     @_locked
-    def download(self, first, count):
-        out = np.zeros((count, self.params.n + 1), np.uint32)
+    def download(self, first, count, out=None):
+        """Pool slots [first, first+count) -> host (into `out` [count][>=n+1] if given)."""
+        if out is None:
+            out = np.zeros((count, self.params.n + 1), np.uint32)
+        elif out.dtype != np.uint32 or out.ndim != 2 or out.shape[0] != count or out.shape[1] < self.params.n + 1 \
+                or not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous uint32 array [count][>= n+1]")
         check(lib().hb_pool_download(self._e, int(first), int(count), u32p(out), out.shape[1]))
         return out
 

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define HB_ABI_VERSION 1
+#define HB_ABI_VERSION 2
 
 /* status codes */
 #define HB_OK 0
@@ -49,7 +49,10 @@ typedef struct hb_params {
     int32_t l;            /* gadget length, 3 */
     int32_t ks_base_bits; /* log2 key-switch base, 2 */
     int32_t ks_t;         /* key-switch length, 8 */
-    int32_t _pad;
+    int32_t bk_unroll;    /* blind-rotation key layout: 1 (or 0) = one TGSW(s_i) per key bit
+                           * (CGGI), 2 = key pairs: TGSW(s_i s_j), TGSW(s_i (1-s_j)),
+                           * TGSW((1-s_i) s_j) per (i, j) = (2m, 2m+1), one external
+                           * product per pair (n must be even) */
     double lwe_stdev;     /* 2^-15: fresh LWE and KSK noise */
     double bk_stdev;      /* 2^-25: bootstrapping-key noise */
 } hb_params;

@@ -27,7 +27,7 @@ void or_default_params(or_params *p) {
     p->l = 3;
     p->ks_base_bits = 2;
     p->ks_t = 8;
-    p->_pad = 0;
+    p->bk_unroll = 1;
     p->lwe_stdev = 1.0 / 32768.0;      /* 2^-15 */
     p->bk_stdev = 1.0 / 33554432.0;    /* 2^-25 */
 }
@@ -121,6 +121,10 @@ static uint32_t rng_gauss_torus(rng_t *r, double stdev) {
 #define DOM_BK 0x03ull
 #define DOM_KSK 0x04ull
 #define DOM_ENC 0x05ull
+#define DOM_BK2 0x06ull
+
+/* bk_unroll 0 is read as 1 */
+static inline int bk_unroll(const or_params *p) { return p->bk_unroll == 2 ? 2 : 1; }
 
 /* ------------------------------------------------------------------------ */
 /* negacyclic arithmetic                                                     */
@@ -335,6 +339,7 @@ static void poly_mul_binary(int N, const uint32_t *a, const uint32_t *s, uint32_
 int or_keygen(const or_params *p, uint64_t seed, uint32_t *lwe_key, uint32_t *trlwe_key,
               uint32_t *bk, uint32_t *ksk) {
     const int n = p->n, N = p->N, k = p->k, l = p->l;
+    if (bk_unroll(p) == 2 && (n & 1)) return -1;
     const int base = 1 << p->ks_base_bits, t = p->ks_t;
     rng_t r;
     rng_init(&r, seed, DOM_LWE_KEY << 56);
@@ -343,13 +348,28 @@ int or_keygen(const or_params *p, uint64_t seed, uint32_t *lwe_key, uint32_t *tr
     for (int i = 0; i < k * N; i++) trlwe_key[i] = rng_u32(&r) & 1u;
 
     /* BK_i = TGSW(s_i): rows (q, pp) are TRLWE encryptions of zero plus
-     * s_i * h_pp added to polynomial q (q = 0..k-1 masks, q = k body). */
+     * s_i * h_pp added to polynomial q (q = 0..k-1 masks, q = k body).
+     * bk_unroll 2: per key pair (i, j) = (2m, 2m+1) three TGSWs, of the
+     * messages s_i s_j, s_i (1 - s_j) and (1 - s_i) s_j. */
     const int rows = (k + 1) * l;
+    const int unroll = bk_unroll(p);
+    const int ntgsw = unroll == 2 ? (n / 2) * 3 : n;
     uint32_t *tmp = malloc(sizeof(uint32_t) * N);
-    for (int i = 0; i < n; i++) {
+    for (int g = 0; g < ntgsw; g++) {
+        uint32_t msg;
+        if (unroll == 2) {
+            const uint32_t si = lwe_key[2 * (g / 3)], sj = lwe_key[2 * (g / 3) + 1];
+            const int comp = g % 3;
+            msg = comp == 0 ? (si & sj) : comp == 1 ? (si & (1u - sj)) : ((1u - si) & sj);
+        } else {
+            msg = lwe_key[g];
+        }
         for (int row = 0; row < rows; row++) {
-            uint32_t *trlwe = bk + ((size_t)i * rows + row) * (size_t)(k + 1) * N;
-            rng_init(&r, seed, (DOM_BK << 56) | ((uint64_t)i << 16) | (uint64_t)row);
+            uint32_t *trlwe = bk + ((size_t)g * rows + row) * (size_t)(k + 1) * N;
+            const uint64_t nonce = unroll == 2
+                ? (DOM_BK2 << 56) | ((uint64_t)(g / 3) << 16) | ((uint64_t)(g % 3) << 8) | (uint64_t)row
+                : (DOM_BK << 56) | ((uint64_t)g << 16) | (uint64_t)row;
+            rng_init(&r, seed, nonce);
             uint32_t *body = trlwe + (size_t)k * N;
             for (int q = 0; q < k; q++)
                 for (int j = 0; j < N; j++) trlwe[(size_t)q * N + j] = rng_u32(&r);
@@ -360,7 +380,7 @@ int or_keygen(const or_params *p, uint64_t seed, uint32_t *lwe_key, uint32_t *tr
             }
             int q = row / l, pp = row % l;
             uint32_t h = 1u << (32 - (pp + 1) * p->bg_bits);
-            trlwe[(size_t)q * N] += lwe_key[i] * h;
+            trlwe[(size_t)q * N] += msg * h;
         }
     }
     free(tmp);
@@ -430,7 +450,8 @@ void or_decrypt(const or_params *p, const uint32_t *lwe_key, const uint32_t *cts
 struct or_ctx {
     or_params p;
     ntt_plan pl;
-    uint64_t *bk_ntt;   /* [n][rows][k+1][N] */
+    uint64_t *bk_ntt;   /* [n][rows][k+1][N]  (bk_unroll 2: [n/2][3][rows][k+1][N]) */
+    uint64_t *psi2;     /* psi^u, u < 2N: X^e evaluates to psi2[e (2j+1) mod 2N] at NTT bin j */
     uint32_t *ksk;      /* [kN][t][base-1][n+1] */
 };
 
@@ -439,7 +460,13 @@ or_ctx *or_ctx_create(const or_params *p, const uint32_t *bk, const uint32_t *ks
     c->p = *p;
     const int N = p->N, rows = (p->k + 1) * p->l, kp1 = p->k + 1;
     ntt_plan_init(&c->pl, N);
-    size_t npoly = (size_t)p->n * rows * kp1;
+    c->psi2 = malloc(sizeof(uint64_t) * 2 * N);
+    for (int u = 0; u < N; u++) {
+        c->psi2[u] = c->pl.psi_pows[u];
+        c->psi2[u + N] = GL_P - c->pl.psi_pows[u];  /* psi^N = -1 */
+    }
+    const size_t ntgsw = bk_unroll(p) == 2 ? (size_t)(p->n / 2) * 3 : (size_t)p->n;
+    size_t npoly = ntgsw * rows * kp1;
     c->bk_ntt = malloc(sizeof(uint64_t) * npoly * N);
     int64_t *tmp = malloc(sizeof(int64_t) * N);
     for (size_t q = 0; q < npoly; q++) {
@@ -457,6 +484,7 @@ void or_ctx_destroy(or_ctx *c) {
     if (!c) return;
     ntt_plan_free(&c->pl);
     free(c->bk_ntt);
+    free(c->psi2);
     free(c->ksk);
     free(c);
 }
@@ -511,9 +539,45 @@ static void cmux_step(const or_ctx *c, int i, int a, uint32_t *acc, uint32_t *ro
     }
 }
 
+/* Key-pair CMux (bk_unroll 2): ACC <- ACC + BK_m [x] ACC with the combined
+ * TGSW BK_m = (X^{a_i+a_j} - 1) BK_m,0 + (X^{a_i} - 1) BK_m,1 + (X^{a_j} - 1) BK_m,2,
+ * whose message is X^{a_i s_i + a_j s_j} - 1, so ACC <- X^{a_i s_i + a_j s_j} ACC.
+ * Exact: digits of ACC are NTT-transformed once, multiplied by each component
+ * and by the NTT image of X^e - 1, summed in the field and lifted (the true
+ * integer result is below 2^53 << p/2), then reduced mod 2^32. */
+static void cmux_pair(const or_ctx *c, int m, const int e[3], uint32_t *acc, uint32_t *rot,
+                      int64_t *dig, uint64_t *dig_ntt, uint64_t *sum) {
+    const int N = c->p.N, kp1 = c->p.k + 1, l = c->p.l, rows = kp1 * l;
+    if (e[0] == 0 && e[1] == 0 && e[2] == 0) return;
+    const uint32_t offset = decomp_offset(c->p.bg_bits, l);
+    for (int row = 0; row < rows; row++) {
+        const int q = row / l, pp = row % l;
+        for (int j = 0; j < N; j++) dig[j] = decomp_digit(acc[(size_t)q * N + j] + offset, pp, c->p.bg_bits);
+        ntt_forward_i64(&c->pl, dig, dig_ntt + (size_t)row * N);
+    }
+    memset(sum, 0, sizeof(uint64_t) * (size_t)kp1 * N);
+    for (int comp = 0; comp < 3; comp++) {
+        if (e[comp] == 0) continue;  /* X^0 - 1 = 0 */
+        const uint64_t *bk = c->bk_ntt + ((size_t)m * 3 + comp) * rows * kp1 * N;
+        for (int o = 0; o < kp1; o++) {
+            for (int j = 0; j < N; j++) {
+                uint64_t t = 0;
+                for (int row = 0; row < rows; row++)
+                    t = gl_add(t, gl_mul(dig_ntt[(size_t)row * N + j], bk[((size_t)row * kp1 + o) * N + j]));
+                const uint64_t f = gl_sub(c->psi2[((uint64_t)e[comp] * (2 * j + 1)) & (2 * N - 1)], 1);
+                sum[(size_t)o * N + j] = gl_add(sum[(size_t)o * N + j], gl_mul(f, t));
+            }
+        }
+    }
+    for (int o = 0; o < kp1; o++) {
+        ntt_inverse_torus(&c->pl, sum + (size_t)o * N, rot + (size_t)o * N);
+        for (int j = 0; j < N; j++) acc[(size_t)o * N + j] += rot[(size_t)o * N + j];
+    }
+}
+
 void or_blind_rotate(const or_ctx *c, const uint32_t *lwe, uint32_t mu, int32_t iters,
                      uint32_t *acc) {
-    const int n = c->p.n, N = c->p.N, kp1 = c->p.k + 1;
+    const int n = c->p.n, N = c->p.N, kp1 = c->p.k + 1, rows = kp1 * c->p.l;
     uint32_t *bar = malloc(sizeof(uint32_t) * (n + 1));
     or_modswitch(c, lwe, bar);
     /* ACC = X^{-barb} * (0, ..., 0, testvect), testvect = mu everywhere */
@@ -524,12 +588,20 @@ void or_blind_rotate(const or_ctx *c, const uint32_t *lwe, uint32_t mu, int32_t 
     poly_mul_xai(N, rotb, tv, acc + (size_t)c->p.k * N);
     uint32_t *rot = malloc(sizeof(uint32_t) * (size_t)kp1 * N);
     int64_t *dig = malloc(sizeof(int64_t) * N);
-    uint64_t *dig_ntt = malloc(sizeof(uint64_t) * N);
+    uint64_t *dig_ntt = malloc(sizeof(uint64_t) * (size_t)rows * N);
     uint64_t *sum = malloc(sizeof(uint64_t) * (size_t)kp1 * N);
     if (iters < 0 || iters > n) iters = n;
-    for (int i = 0; i < iters; i++) {
-        if (bar[i] == 0) continue;
-        cmux_step(c, i, (int)bar[i], acc, rot, dig, dig_ntt, sum);
+    if (bk_unroll(&c->p) == 2) {
+        for (int m = 0; m < iters / 2; m++) {
+            const int ai = (int)bar[2 * m], aj = (int)bar[2 * m + 1];
+            const int e[3] = {(ai + aj) & (2 * N - 1), ai, aj};
+            cmux_pair(c, m, e, acc, rot, dig, dig_ntt, sum);
+        }
+    } else {
+        for (int i = 0; i < iters; i++) {
+            if (bar[i] == 0) continue;
+            cmux_step(c, i, (int)bar[i], acc, rot, dig, dig_ntt, sum);
+        }
     }
     free(bar); free(tv); free(rot); free(dig); free(dig_ntt); free(sum);
 }

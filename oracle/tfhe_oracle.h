@@ -44,7 +44,7 @@ typedef struct or_params {
     int32_t l;            /* gadget length (3) */
     int32_t ks_base_bits; /* log2 KS base (2) */
     int32_t ks_t;         /* KS length (8) */
-    int32_t _pad;
+    int32_t bk_unroll;    /* 1 (or 0): BK_i = TGSW(s_i); 2: key pairs, 3 TGSW per pair */
     double lwe_stdev;     /* 2^-15 (input LWE and KSK) */
     double bk_stdev;      /* 2^-25 */
 } or_params;
@@ -57,7 +57,9 @@ void or_chacha_block(const uint32_t key[8], uint64_t nonce, uint64_t counter, ui
 /* Key generation (all arrays caller-allocated):
  *   lwe_key  [n]                              bits as u32 (0/1)
  *   trlwe_key[k*N]                            bits as u32 (0/1)
- *   bk       [n][(k+1)*l][(k+1)][N]           torus u32, coefficient domain
+ *   bk       [n][(k+1)*l][(k+1)][N]           torus u32, coefficient domain (bk_unroll 1)
+ *            [n/2][3][(k+1)*l][(k+1)][N]      bk_unroll 2: per pair (2m, 2m+1) the TGSWs of
+ *                                             s_i s_j, s_i (1-s_j), (1-s_i) s_j
  *   ksk      [k*N][t][base-1][n+1]            torus u32 (digit value 0 omitted) */
 int or_keygen(const or_params *p, uint64_t seed, uint32_t *lwe_key, uint32_t *trlwe_key,
               uint32_t *bk, uint32_t *ksk);
@@ -85,8 +87,8 @@ void or_ctx_destroy(or_ctx *c);
 /* Stage entry points (bit-level parity of each stage). */
 /* mod-switch of an LWE_n sample to Z_2N: out[n+1] (a_0..a_{n-1}, b). */
 void or_modswitch(const or_ctx *c, const uint32_t *lwe, uint32_t *out);
-/* Blind rotation from a test vector mu, stopping after `iters` key bits;
- * acc_out[(k+1)*N]. */
+/* Blind rotation from a test vector mu, stopping after `iters` key bits
+ * (bk_unroll 2: after iters/2 key pairs); acc_out[(k+1)*N]. */
 void or_blind_rotate(const or_ctx *c, const uint32_t *lwe, uint32_t mu, int32_t iters,
                      uint32_t *acc_out);
 /* Bootstrap without key switching: out[k*N+1] extracted LWE. */

@@ -52,7 +52,7 @@ class HbParams(ctypes.Structure):
         ("l", ctypes.c_int32),
         ("ks_base_bits", ctypes.c_int32),
         ("ks_t", ctypes.c_int32),
-        ("_pad", ctypes.c_int32),
+        ("bk_unroll", ctypes.c_int32),
         ("lwe_stdev", ctypes.c_double),
         ("bk_stdev", ctypes.c_double),
     ]

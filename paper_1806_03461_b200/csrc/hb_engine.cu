@@ -194,15 +194,20 @@ __device__ __forceinline__ void tw_powers(double2 T0, double2 step, bool t0_is_o
 // NP-polynomial variants: the passes of NP independent transforms are
 // interleaved (ILP for the FP64 pipe), share one twiddle recurrence and one
 // barrier per exchange.  xch: [NP][2][kXchStride] (double-buffered exchanges).
-template <int NP>
+// kSB (single buffer): xch is [NP][kXchStride]; both exchanges share one
+// buffer, at the price of two more barriers (one before the first store, one
+// between the second exchange's loads and stores).
+template <int NP, bool kSB = false>
 __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch, int t, const TwSeeds &tw,
                                                int bar_id) {
+    constexpr int kB0 = kSB ? 1 : 2, kB1 = kSB ? 0 : 1;  // buffer q of exchange 1 / 2: q * kB0 + kB1 * (..)
 #pragma unroll
     for (int q = 0; q < NP; q++) {
 #pragma unroll
         for (int m = 1; m < 8; m++) x[q][m] = cmul(x[q][m], c16(m));
         dft8(x[q]);
     }
+    if (kSB) group_bar(bar_id);  // previous transform's readers are done
     {
         const int j0 = t & 7, j1 = t >> 3;
         double2 T[8];
@@ -210,7 +215,7 @@ __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch
 #pragma unroll
         for (int k2 = 0; k2 < 8; k2++) {
 #pragma unroll
-            for (int q = 0; q < NP; q++) xch[(2 * q) * kXchStride + j0 * 65 + k2 * 8 + j1] = cmul(x[q][rev3(k2)], T[k2]);
+            for (int q = 0; q < NP; q++) xch[(kB0 * q) * kXchStride + j0 * 65 + k2 * 8 + j1] = cmul(x[q][rev3(k2)], T[k2]);
         }
     }
     if (HB_EXP_SKIP & 64) __syncwarp(); else group_bar(bar_id);
@@ -219,9 +224,14 @@ __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch
 #pragma unroll
         for (int q = 0; q < NP; q++) {
 #pragma unroll
-            for (int j1 = 0; j1 < 8; j1++) x[q][j1] = xch[(2 * q) * kXchStride + j0 * 65 + k2 * 8 + j1];
+            for (int j1 = 0; j1 < 8; j1++) x[q][j1] = xch[(kB0 * q) * kXchStride + j0 * 65 + k2 * 8 + j1];
             dft8(x[q]);
-            xch[(2 * q + 1) * kXchStride + k2 * 65 + j0] = x[q][0];
+            if (!kSB) xch[(kB0 * q + kB1) * kXchStride + k2 * 65 + j0] = x[q][0];
+        }
+        if (kSB) {
+            group_bar(bar_id);
+#pragma unroll
+            for (int q = 0; q < NP; q++) xch[(kB0 * q + kB1) * kXchStride + k2 * 65 + j0] = x[q][0];
         }
         double2 T[8];
         tw_powers(tw.step_b, tw.step_b, true, T);
@@ -229,7 +239,7 @@ __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch
         for (int k1 = 1; k1 < 8; k1++) {
 #pragma unroll
             for (int q = 0; q < NP; q++)
-                xch[(2 * q + 1) * kXchStride + k2 * 65 + k1 * 8 + j0] = cmul(x[q][rev3(k1)], T[k1]);
+                xch[(kB0 * q + kB1) * kXchStride + k2 * 65 + k1 * 8 + j0] = cmul(x[q][rev3(k1)], T[k1]);
         }
     }
     if (HB_EXP_SKIP & 32) __syncwarp(); else group_bar(bar_id);
@@ -239,7 +249,7 @@ __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch
         for (int q = 0; q < NP; q++) {
             double2 y[8];
 #pragma unroll
-            for (int j0 = 0; j0 < 8; j0++) y[j0] = xch[(2 * q + 1) * kXchStride + k2 * 65 + k1 * 8 + j0];
+            for (int j0 = 0; j0 < 8; j0++) y[j0] = xch[(kB0 * q + kB1) * kXchStride + k2 * 65 + k1 * 8 + j0];
             dft8(y);
 #pragma unroll
             for (int k0 = 0; k0 < 8; k0++) x[q][k0] = y[rev3(k0)];
@@ -247,25 +257,27 @@ __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch
     }
 }
 
-template <int NP>
+template <int NP, bool kSB = false>
 __device__ __forceinline__ void nega_fft_inv_n(double2 (&x)[NP][8], double2 *xch, int t, const TwSeeds &tw,
                                                int bar_id) {
+    constexpr int kB0 = kSB ? 1 : 2, kB1 = kSB ? 0 : 1;
 #pragma unroll
     for (int q = 0; q < NP; q++) {
 #pragma unroll
         for (int m = 0; m < 8; m++) x[q][m].y = -x[q][m].y;
         dft8(x[q]);
     }
+    if (kSB) group_bar(bar_id);
     {
         const int j0 = t & 7, j1 = t >> 3;
 #pragma unroll
-        for (int q = 0; q < NP; q++) xch[(2 * q) * kXchStride + j0 * 65 + j1] = x[q][0];
+        for (int q = 0; q < NP; q++) xch[(kB0 * q) * kXchStride + j0 * 65 + j1] = x[q][0];
         double2 T[8];
         tw_powers(tw.step_a, tw.step_a, true, T);
 #pragma unroll
         for (int k2 = 1; k2 < 8; k2++) {
 #pragma unroll
-            for (int q = 0; q < NP; q++) xch[(2 * q) * kXchStride + j0 * 65 + k2 * 8 + j1] = cmul(x[q][rev3(k2)], T[k2]);
+            for (int q = 0; q < NP; q++) xch[(kB0 * q) * kXchStride + j0 * 65 + k2 * 8 + j1] = cmul(x[q][rev3(k2)], T[k2]);
         }
     }
     if (HB_EXP_SKIP & 64) __syncwarp(); else group_bar(bar_id);
@@ -274,16 +286,17 @@ __device__ __forceinline__ void nega_fft_inv_n(double2 (&x)[NP][8], double2 *xch
 #pragma unroll
         for (int q = 0; q < NP; q++) {
 #pragma unroll
-            for (int j1 = 0; j1 < 8; j1++) x[q][j1] = xch[(2 * q) * kXchStride + j0 * 65 + k2 * 8 + j1];
+            for (int j1 = 0; j1 < 8; j1++) x[q][j1] = xch[(kB0 * q) * kXchStride + j0 * 65 + k2 * 8 + j1];
             dft8(x[q]);
         }
+        if (kSB) group_bar(bar_id);
         double2 T[8];
         tw_powers(tw.i_b0, tw.i_stepb, false, T);
 #pragma unroll
         for (int k1 = 0; k1 < 8; k1++) {
 #pragma unroll
             for (int q = 0; q < NP; q++)
-                xch[(2 * q + 1) * kXchStride + k2 * 65 + k1 * 8 + j0] = cmul(x[q][rev3(k1)], T[k1]);
+                xch[(kB0 * q + kB1) * kXchStride + k2 * 65 + k1 * 8 + j0] = cmul(x[q][rev3(k1)], T[k1]);
         }
     }
     if (HB_EXP_SKIP & 32) __syncwarp(); else group_bar(bar_id);
@@ -293,7 +306,7 @@ __device__ __forceinline__ void nega_fft_inv_n(double2 (&x)[NP][8], double2 *xch
         for (int q = 0; q < NP; q++) {
             double2 y[8];
 #pragma unroll
-            for (int j0 = 0; j0 < 8; j0++) y[j0] = xch[(2 * q + 1) * kXchStride + k2 * 65 + k1 * 8 + j0];
+            for (int j0 = 0; j0 < 8; j0++) y[j0] = xch[(kB0 * q + kB1) * kXchStride + k2 * 65 + k1 * 8 + j0];
             dft8(y);
 #pragma unroll
             for (int k0 = 0; k0 < 8; k0++) {
@@ -377,9 +390,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // 1/512 (the inverse-FFT normalisation, exact power of two) in natural bin
 // order: bkf[poly][k], poly = ((i * 6 + row) * 2 + q).
 // ---------------------------------------------------------------------------
+// bk_unroll 2 (key pairs): input poly ((g * 6 + row) * 2 + o) with g = 3 m + comp
+// is stored at stage-major position ((((m * 3 + row / 2) * 3 + comp) * 2 + row % 2) * 2 + o),
+// the order in which k_blind_rotate_u2 consumes (row pair, component, row) stages.
 __global__ void __launch_bounds__(128) k_bk_to_fourier(const uint32_t *__restrict__ bk, double2 *__restrict__ bkf,
                                                       int npoly, const double2 *__restrict__ W,
-                                                      const double2 *__restrict__ TW) {
+                                                      const double2 *__restrict__ TW, int unroll) {
     __shared__ double2 xch[2][2][kXchStride];
     const int grp = threadIdx.x >> 6, t = threadIdx.x & 63;
     const int poly = blockIdx.x * 2 + grp;
@@ -394,9 +410,15 @@ __global__ void __launch_bounds__(128) k_bk_to_fourier(const uint32_t *__restric
     }
     fft512(x, xch[grp][0], xch[grp][1], t, W, 1 + grp);
     if (active) {
+        size_t dst = (size_t)poly;
+        if (unroll == 2) {
+            const int o = poly & 1, row = (poly >> 1) % kRows, g = (poly >> 1) / kRows;
+            const int m = g / 3, comp = g % 3;
+            dst = ((((size_t)m * 3 + row / 2) * 3 + comp) * 2 + (row & 1)) * 2 + o;
+        }
 #pragma unroll
         for (int m = 0; m < 8; m++)
-            bkf[(size_t)poly * kNH + t + 64 * m] = make_double2(x[m].x * (1.0 / 512), x[m].y * (1.0 / 512));
+            bkf[dst * kNH + t + 64 * m] = make_double2(x[m].x * (1.0 / 512), x[m].y * (1.0 / 512));
     }
 }
 
@@ -415,6 +437,7 @@ struct BrArgs {
     uint32_t *big;            // [n_work][kBigStride] extracted LWE
     const double2 *W;         // [512] e^{2 pi i e/512}
     const double2 *TW;        // [512] e^{i pi j/1024}
+    const double2 *PSI;       // [2048] e^{i pi u/1024} (key-pair monomials)
     // debug
     int32_t iters;            // CMux steps to run (n in production)
     uint32_t *acc_dump;       // if set: [n_work][2N] raw accumulator
@@ -829,6 +852,225 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_lat(const BrArgs args) 
 }
 
 // ---------------------------------------------------------------------------
+// K1+K2+K3 with the key-pair bootstrapping key (bk_unroll 2).  One external
+// product per key pair (i, j) = (2m, 2m+1):
+//   ACC <- ACC + BK_m [x] ACC,  BK_m = sum_c (X^{e_c} - 1) BK_{m,c},
+//   (e_0, e_1, e_2) = (a_i + a_j, a_i, a_j),
+// whose TGSW message is X^{a_i s_i + a_j s_j} - 1.  Per pair: 6 forward
+// transforms of the digits of ACC itself (no rotation), 2 inverse transforms,
+// and for every digit row and component a Fourier MAC with the digit spectrum
+// pre-multiplied by F_c = (X^{e_c} - 1)(psi^{4k+1}) — half the transforms of
+// two CGGI steps for 1.5x the MAC.  The BK arrives as 16 KiB (row, component)
+// stages through a 7-deep cp.async.bulk ring; the FFT exchange is
+// single-buffered to make room for it.  Same rounding argument as the CGGI
+// kernel: the exact integer result (< 2^53) is recovered by the final rounding.
+// ---------------------------------------------------------------------------
+constexpr int kStagesU2 = 7;
+constexpr int kStagesPerPair = 3 * kRows;  // (row pair, component, row) stages per key pair
+
+__constant__ double2 c_w8[8] = {{1.0, 0.0},
+                                {0.70710678118654752440, 0.70710678118654752440},
+                                {0.0, 1.0},
+                                {-0.70710678118654752440, 0.70710678118654752440},
+                                {-1.0, 0.0},
+                                {-0.70710678118654752440, -0.70710678118654752440},
+                                {0.0, -1.0},
+                                {0.70710678118654752440, -0.70710678118654752440}};
+
+template <int G>
+struct BrSmemU2 {
+    double2 bk[kStagesU2][2 * kNH];          // stage ring: [output poly][bin]
+    uint64_t full[kStagesU2], empty[kStagesU2];
+    uint32_t acc[G][2][kN];
+    double2 xch[G][2][kXchStride];           // single-buffered dual-FFT exchange
+    uint16_t bar[G][kMaxLweN + 1];
+    TwSeeds tws[64];
+};
+
+template <int G, bool kDebug>
+__global__ void __launch_bounds__(64 * G, 1) k_blind_rotate_u2(const BrArgs args) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    BrSmemU2<G> &sm = *reinterpret_cast<BrSmemU2<G> *>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = args.n;
+    const int pairs = min(n, args.iters) / 2;
+    const int stages_needed = pairs * kStagesPerPair;
+    const char *bk_src = reinterpret_cast<const char *>(args.bkf);
+
+    if (threadIdx.x < 64) {
+        const int tt = threadIdx.x;
+        TwSeeds ts;
+        ts.f_a0 = args.TW[tt];
+        ts.step_a = args.W[tt];
+        ts.step_b = args.W[8 * (tt & 7)];
+        ts.i_b0 = args.TW[tt >> 3];
+        ts.i_stepb = args.TW[32 * (tt & 7) + 8];
+        sm.tws[tt] = ts;
+    }
+    int issued = 0;  // producer (thread 0) state: stages issued so far
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStagesU2; s++) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], 2 * G);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (; issued < kStagesU2 && issued < stages_needed; issued++) {
+            mbar_arrive_expect_tx(&sm.full[issued], kRowBytes);
+            bulk_g2s(sm.bk[issued], bk_src + (size_t)issued * kRowBytes, kRowBytes, &sm.full[issued]);
+        }
+    }
+    __syncthreads();
+
+    const int g = warp >> 1;
+    const int t = threadIdx.x & 63;
+    const int bar_id = 1 + g;
+    const uint32_t e_raw = blockIdx.x * G + g;
+    const bool active = e_raw < args.n_work;
+    const uint32_t e = active ? e_raw : args.n_work - 1;
+    uint32_t *accA = sm.acc[g][0];
+    uint32_t *accB = sm.acc[g][1];
+    double2 *xch = &sm.xch[g][0][0];
+    uint16_t *bar = sm.bar[g];
+
+    {   // K1: linear combination + modulus switch
+        const uint32_t lanes = args.lanes;
+        const BrItem it = args.items[e / lanes];
+        const uint32_t lane_id = e % lanes;
+        const int alpha = (int8_t)(it.coef & 0xFF), beta = (int8_t)((it.coef >> 8) & 0xFF);
+        const uint32_t *A = args.pool + ((size_t)it.src_a * lanes + lane_id) * args.pool_stride;
+        const uint32_t *B = args.pool + ((size_t)it.src_b * lanes + lane_id) * args.pool_stride;
+        for (int c = t; c <= n; c += 64) {
+            uint32_t v = (uint32_t)alpha * __ldg(&A[c]);
+            if (beta) v += (uint32_t)beta * __ldg(&B[c]);
+            if (c == n) v += it.c0;
+            bar[c] = (uint16_t)(((v + (1u << 20)) >> 21) & (2 * kN - 1));
+        }
+    }
+    group_bar(bar_id);
+    {
+        const int barb = bar[n];
+        for (int i = t; i < kN; i += 64) {
+            accA[i] = 0;
+            accB[i] = (((i + barb) & kN) ? 0u - args.mu : args.mu);
+        }
+    }
+    group_bar(bar_id);
+
+    double max_err = 0.0;
+    int st = 0;  // next stage to consume
+    for (int pm = 0; pm < pairs; pm++) {
+        const int ai = bar[2 * pm], aj = bar[2 * pm + 1];
+        // F_c at this thread's bins k = t + 64 m: psi^{e (4k+1)} - 1 =
+        // psi^{e (4t+1)} * w8^{e m} - 1 (the exponent is warp-uniform)
+        int ex[3];
+        double2 base[3];
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            ex[c] = c == 0 ? ((ai + aj) & (2 * kN - 1)) : (c == 1 ? ai : aj);
+            base[c] = __ldg(&args.PSI[(ex[c] * (4 * t + 1)) & (2 * kN - 1)]);
+        }
+        double2 f0[8], f1[8];
+#pragma unroll 1
+        for (int rp = 0; rp < kRows / 2; rp++) {
+            // producer: refill the ring up to kStagesU2 stages ahead of this row pair
+            if (threadIdx.x == 0) {
+#pragma unroll 1
+                for (; issued < st + kStagesU2 && issued < stages_needed; issued++) {
+                    const int s2 = issued % kStagesU2;
+                    mbar_wait(&sm.empty[s2], ((issued / kStagesU2) - 1) & 1);
+                    mbar_arrive_expect_tx(&sm.full[s2], kRowBytes);
+                    bulk_g2s(sm.bk[s2], bk_src + (size_t)issued * kRowBytes, kRowBytes, &sm.full[s2]);
+                }
+            }
+            __syncwarp();
+            double2 x[2][8];
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int row = 2 * rp + h;
+                const int q = row / kL, p = row % kL;
+                const uint32_t *P = q ? accB : accA;
+#pragma unroll
+                for (int m = 0; m < 8; m++) {
+                    const int j = t + 64 * m;
+                    x[h][m] = make_double2(small_int_to_double(gadget_digit(P[j], p)),
+                                           small_int_to_double(gadget_digit(P[j + kNH], p)));
+                }
+            }
+            nega_fft_fwd_n<2, true>(x, xch, t, sm.tws[t], bar_id);
+#pragma unroll
+            for (int c = 0; c < 3; c++) {
+                double2 F[8];  // (X^{e_c} - 1) at this thread's bins (recomputed per row pair: registers)
+#pragma unroll
+                for (int m = 0; m < 8; m++) {
+                    const double2 p = m == 0 ? base[c] : cmul(base[c], c_w8[(ex[c] * m) & 7]);
+                    F[m] = make_double2(p.x - 1.0, p.y);
+                }
+#pragma unroll
+                for (int h = 0; h < 2; h++, st++) {
+                    const int s = st % kStagesU2;
+                    mbar_wait(&sm.full[s], (st / kStagesU2) & 1);
+                    const double2 *bk0 = sm.bk[s];
+                    const double2 *bk1 = sm.bk[s] + kNH;
+#pragma unroll
+                    for (int m = 0; m < 8; m++) {
+                        const double2 y = cmul(x[h][m], F[m]);
+                        if (rp == 0 && c == 0 && h == 0) {
+                            f0[m] = cmul(y, bk0[t + 64 * m]);
+                            f1[m] = cmul(y, bk1[t + 64 * m]);
+                        } else {
+                            cmac(f0[m], y, bk0[t + 64 * m]);
+                            cmac(f1[m], y, bk1[t + 64 * m]);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sm.empty[s]);
+                }
+            }
+        }
+        {
+            double2 x[2][8];
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                x[0][m] = f0[m];
+                x[1][m] = f1[m];
+            }
+            nega_fft_inv_n<2, true>(x, xch, t, sm.tws[t], bar_id);
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
+                uint32_t *P = q ? accB : accA;
+#pragma unroll
+                for (int m = 0; m < 8; m++) {
+                    const double lo = x[q][m].x, hi = x[q][m].y;
+                    if (kDebug) {
+                        max_err = fmax(max_err, fabs(lo - rint(lo)));
+                        max_err = fmax(max_err, fabs(hi - rint(hi)));
+                    }
+                    const int j = t + 64 * m;
+                    P[j] += round_to_torus(lo);
+                    P[j + kNH] += round_to_torus(hi);
+                }
+            }
+        }
+        group_bar(bar_id);
+    }
+
+    if (!active) return;
+    if (kDebug && args.margin) atomicMax(args.margin, (unsigned long long)__double_as_longlong(max_err));
+    if (kDebug && args.acc_dump) {
+        uint32_t *dst = args.acc_dump + (size_t)e * 2 * kN;
+        for (int c = t; c < 2 * kN; c += 64) dst[c] = (c < kN) ? accA[c] : accB[c - kN];
+    }
+    uint32_t *out = args.big + (size_t)e * kBigStride;
+    for (int c = t; c <= kN; c += 64) {
+        uint32_t v;
+        if (c == 0) v = accA[0];
+        else if (c < kN) v = 0u - accA[kN - c];
+        else v = accB[0];
+        out[c] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K4: batched key switch.  For coefficient i the CGGI digits are the eight
 // base-4 digits of w_i = (a'_i + 2^15) >> 16.  The device KSK is laid out as a
 // lookup table per 8-column chunk, T[chunk][i][j][d][8] with T[..][0][..] = 0,
@@ -1018,7 +1260,8 @@ struct hb_engine {
     cudaEvent_t ev_compute = nullptr;     // compute point an async download waits on
     cudaEvent_t ev_prev_level = nullptr;  // compute stream before the most recent level
     bool pending_upload = false;
-    double2 *d_W = nullptr, *d_TW = nullptr;
+    double2 *d_W = nullptr, *d_TW = nullptr, *d_PSI = nullptr;
+    int unroll = 1;  // bk_unroll of the loaded key
     double2 *d_bkf = nullptr;
     uint32_t *d_ksk = nullptr;
     uint32_t *d_pool = nullptr;
@@ -1089,6 +1332,15 @@ int launch_br(hb_engine *e, const BrArgs &a) {
     return HB_OK;
 }
 
+template <int G, bool kDebug>
+int launch_br_u2(hb_engine *e, const BrArgs &a) {
+    const unsigned grid = (a.n_work + G - 1) / G;
+    k_blind_rotate_u2<G, kDebug><<<grid, 64 * G, sizeof(BrSmemU2<G>), e->stream>>>(a);
+    HB_CUDA_TRY(cudaGetLastError());
+    e->n_launch++;
+    return HB_OK;
+}
+
 template <bool kDebug>
 int launch_br_lat(hb_engine *e, const BrArgs &a) {
     k_blind_rotate_lat<kDebug><<<a.n_work, 192, sizeof(BrLatSmem), e->stream>>>(a);
@@ -1105,6 +1357,25 @@ int launch_ks(hb_engine *e, const KsArgs &a) {
     return HB_OK;
 }
 
+// Blind-rotation launch for a level of a.n_work bootstraps: narrow levels
+// (latency-bound) get one bootstrap per CTA split over three thread groups
+// (latency mode) or fewer bootstraps per CTA; wide levels 4 per CTA.
+// force_g (debug paths): 4 = the throughput kernel regardless of width.
+template <bool kDebug>
+int launch_br_auto(hb_engine *e, const BrArgs &a, int force_g = 0) {
+    const uint32_t sms = (uint32_t)e->num_sms;
+    const int gsel = force_g ? force_g : (a.n_work <= sms ? 1 : (a.n_work <= 2u * sms ? 2 : kBrGates));
+    if (e->unroll == 2) {
+        if (gsel == 1) return launch_br_u2<1, kDebug>(e, a);
+        if (gsel == 2) return launch_br_u2<2, kDebug>(e, a);
+        return launch_br_u2<kBrGates, kDebug>(e, a);
+    }
+    if (!force_g && gsel == 1 && e->latency_mode) return launch_br_lat<kDebug>(e, a);
+    if (gsel == 1) return launch_br<1, kDebug>(e, a);
+    if (gsel == 2) return launch_br<2, kDebug>(e, a);
+    return launch_br<kBrGates, kDebug>(e, a);
+}
+
 BrArgs br_args(hb_engine *e) {
     BrArgs a{};
     a.pool = e->d_pool;
@@ -1116,6 +1387,7 @@ BrArgs br_args(hb_engine *e) {
     a.big = e->d_big;
     a.W = e->d_W;
     a.TW = e->d_TW;
+    a.PSI = e->d_PSI;
     a.iters = e->p.n;
     return a;
 }
@@ -1171,6 +1443,14 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
         long double ph = pi * j / kN;
         TW[j] = make_double2((double)cosl(ph), (double)sinl(ph));
     }
+    std::vector<double2> PSI(2 * kN);
+    for (int u = 0; u < 2 * kN; u++) {
+        long double ph = pi * u / kN;
+        PSI[u] = make_double2((double)cosl(ph), (double)sinl(ph));
+    }
+    HB_CUDA_TRY(cudaMalloc(&e->d_PSI, 2 * kN * sizeof(double2)));
+    HB_CUDA_TRY(cudaMemcpy(e->d_PSI, PSI.data(), 2 * kN * sizeof(double2), cudaMemcpyHostToDevice));
+    e->unroll = bk_unroll(p);
     HB_CUDA_TRY(cudaMalloc(&e->d_W, kNH * sizeof(double2)));
     HB_CUDA_TRY(cudaMalloc(&e->d_TW, kNH * sizeof(double2)));
     HB_CUDA_TRY(cudaMemcpy(e->d_W, W.data(), kNH * sizeof(double2), cudaMemcpyHostToDevice));
@@ -1184,6 +1464,22 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
                                      (int)br_smem_bytes<1>()));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)br_smem_bytes<kBrGates>()));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrSmemU2<kBrGates>)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrSmemU2<kBrGates>)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrSmemU2<2>)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrSmemU2<1>)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrSmemU2<2>)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrSmemU2<1>)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)br_smem_bytes<2>()));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)br_smem_bytes<1>()));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_lat<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(BrLatSmem)));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_lat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1194,12 +1490,13 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
     if (const char *lm = std::getenv("HEBNN_B200_LATENCY_MODE")) e->latency_mode = std::atoi(lm) != 0;
 
     // BK -> Fourier
-    const size_t npoly = (size_t)p->n * kRows * 2;
+    const size_t npoly = bk_tgsw_count(p) * kRows * 2;
     uint32_t *d_bk = nullptr;
     HB_CUDA_TRY(cudaMalloc(&d_bk, npoly * kN * sizeof(uint32_t)));
     HB_CUDA_TRY(cudaMemcpy(d_bk, bk, npoly * kN * sizeof(uint32_t), cudaMemcpyHostToDevice));
     HB_CUDA_TRY(cudaMalloc(&e->d_bkf, npoly * kNH * sizeof(double2)));
-    k_bk_to_fourier<<<(unsigned)((npoly + 1) / 2), 128, 0, e->stream>>>(d_bk, e->d_bkf, (int)npoly, e->d_W, e->d_TW);
+    k_bk_to_fourier<<<(unsigned)((npoly + 1) / 2), 128, 0, e->stream>>>(d_bk, e->d_bkf, (int)npoly, e->d_W, e->d_TW,
+                                                                         e->unroll);
     HB_CUDA_TRY(cudaGetLastError());
     HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
     cudaFree(d_bk);
@@ -1222,7 +1519,7 @@ int hb_engine_destroy(hb_engine *e) {
     if (!e) return HB_OK;
     cudaSetDevice(e->device);
     if (e->stream) cudaStreamSynchronize(e->stream);
-    for (void *ptr : {(void *)e->d_W, (void *)e->d_TW, (void *)e->d_bkf, (void *)e->d_ksk, (void *)e->d_pool,
+    for (void *ptr : {(void *)e->d_W, (void *)e->d_TW, (void *)e->d_PSI, (void *)e->d_bkf, (void *)e->d_ksk, (void *)e->d_pool,
                       (void *)e->d_big, (void *)e->d_br, (void *)e->d_ks, (void *)e->d_tmp, (void *)e->d_margin,
                       e->d_flush})
         if (ptr) cudaFree(ptr);
@@ -1392,17 +1689,7 @@ static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_
     a.items = e->d_br;
     a.n_work = (uint32_t)(nbr * lanes);
     HB_CUDA_TRY(cudaEventRecord(e->ev[0], e->stream));
-    // narrow levels (latency-bound): one bootstrap per CTA split over three
-    // thread groups (latency mode), or fewer bootstraps per CTA
-    if (a.n_work <= (uint32_t)e->num_sms && e->latency_mode) {
-        if ((rc = launch_br_lat<false>(e, a))) return rc;
-    } else if (a.n_work <= (uint32_t)e->num_sms) {
-        if ((rc = launch_br<1, false>(e, a))) return rc;
-    } else if (a.n_work <= 2u * (uint32_t)e->num_sms) {
-        if ((rc = launch_br<2, false>(e, a))) return rc;
-    } else {
-        if ((rc = launch_br<kBrGates, false>(e, a))) return rc;
-    }
+    if ((rc = launch_br_auto<false>(e, a))) return rc;
     HB_CUDA_TRY(cudaEventRecord(e->ev[1], e->stream));
     KsArgs k{};
     k.big = e->d_big;
@@ -1506,7 +1793,7 @@ int hb_debug_blind_rotate(hb_engine *e, const uint32_t *lwe, uint32_t mu, int32_
     }
     a.iters = iters < 0 ? e->p.n : iters;
     a.acc_dump = d_acc;
-    if ((rc = launch_br<kBrGates, true>(e, a))) return rc;
+    if ((rc = launch_br_auto<true>(e, a, kBrGates))) return rc;
     HB_CUDA_TRY(cudaMemcpyAsync(acc_out, d_acc, 2 * kN * 4, cudaMemcpyDeviceToHost, e->stream));
     HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
     return HB_OK;
@@ -1534,7 +1821,7 @@ int hb_debug_bootstrap_wo_ks(hb_engine *e, const uint32_t *lin, size_t count, ui
     a.items = e->d_br;
     a.n_work = (uint32_t)count;
     a.margin = e->d_margin;
-    if ((rc = launch_br<kBrGates, true>(e, a))) return rc;
+    if ((rc = launch_br_auto<true>(e, a, kBrGates))) return rc;
     HB_CUDA_TRY(cudaMemcpy2DAsync(out, (size_t)(kN + 1) * 4, e->d_big, kBigStride * 4, (size_t)(kN + 1) * 4, count,
                                   cudaMemcpyDeviceToHost, e->stream));
     HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
@@ -1587,7 +1874,7 @@ int hb_debug_fourier(hb_engine *e, const uint32_t *polys, size_t count, double *
     HB_CUDA_TRY(cudaMalloc(&d_in, count * kN * 4));
     HB_CUDA_TRY(cudaMalloc(&d_out, count * kNH * sizeof(double2)));
     HB_CUDA_TRY(cudaMemcpy(d_in, polys, count * kN * 4, cudaMemcpyHostToDevice));
-    k_bk_to_fourier<<<(unsigned)((count + 1) / 2), 128, 0, e->stream>>>(d_in, d_out, (int)count, e->d_W, e->d_TW);
+    k_bk_to_fourier<<<(unsigned)((count + 1) / 2), 128, 0, e->stream>>>(d_in, d_out, (int)count, e->d_W, e->d_TW, 1);
     HB_CUDA_TRY(cudaGetLastError());
     HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
     HB_CUDA_TRY(cudaMemcpy(out, d_out, count * kNH * sizeof(double2), cudaMemcpyDeviceToHost));

@@ -91,7 +91,7 @@ struct Stream {
     }
 };
 
-enum : uint64_t { DOM_LWE_KEY = 1, DOM_TRLWE_KEY = 2, DOM_BK = 3, DOM_KSK = 4, DOM_ENC = 5 };
+enum : uint64_t { DOM_LWE_KEY = 1, DOM_TRLWE_KEY = 2, DOM_BK = 3, DOM_KSK = 4, DOM_ENC = 5, DOM_BK2 = 6 };
 
 static inline uint32_t lwe_dot(const uint32_t *a, const uint32_t *key, int n) {
     uint32_t acc = 0;
@@ -120,8 +120,13 @@ static void parallel_for(size_t count, int threads, F &&fn) {
 
 bool params_ok(const hb_params *p) {
     return p && p->n > 0 && p->n <= kMaxLweN && p->N == kN && p->k == 1 && p->bg_bits == kBgBits &&
-           p->l == kL && p->ks_base_bits == kKsBaseBits && p->ks_t == kKsT;
+           p->l == kL && p->ks_base_bits == kKsBaseBits && p->ks_t == kKsT &&
+           (p->bk_unroll == 0 || p->bk_unroll == 1 || (p->bk_unroll == 2 && (p->n & 1) == 0));
 }
+
+int bk_unroll(const hb_params *p) { return p->bk_unroll == 2 ? 2 : 1; }
+
+size_t bk_tgsw_count(const hb_params *p) { return bk_unroll(p) == 2 ? (size_t)(p->n / 2) * 3 : (size_t)p->n; }
 
 }  // namespace hb
 
@@ -141,7 +146,7 @@ void hb_default_params(hb_params *p) {
     p->l = 3;
     p->ks_base_bits = 2;
     p->ks_t = 8;
-    p->_pad = 0;
+    p->bk_unroll = 1;
     p->lwe_stdev = 1.0 / 32768.0;    // 2^-15
     p->bk_stdev = 1.0 / 33554432.0;  // 2^-25
 }
@@ -149,7 +154,7 @@ void hb_default_params(hb_params *p) {
 size_t hb_lwe_words(const hb_params *p) { return (size_t)p->n + 1; }
 
 size_t hb_bk_words(const hb_params *p) {
-    return (size_t)p->n * (p->k + 1) * p->l * (p->k + 1) * p->N;
+    return bk_tgsw_count(p) * (p->k + 1) * p->l * (p->k + 1) * p->N;
 }
 
 size_t hb_ksk_words(const hb_params *p) {
@@ -178,12 +183,26 @@ int hb_keygen(const hb_params *p, uint64_t seed, uint32_t *lwe_key, uint32_t *tr
         if (trlwe_key[i]) support.push_back(i);
 
     const int rows = (k + 1) * l;
-    // BK_i = TGSW(s_i): row (q, pp) = TRLWE(0) + s_i * 2^(32-(pp+1)Bgbits) on poly q
-    parallel_for((size_t)n * rows, threads, [&](size_t item) {
-        const int i = (int)(item / rows), row = (int)(item % rows);
+    // BK_i = TGSW(s_i): row (q, pp) = TRLWE(0) + s_i * 2^(32-(pp+1)Bgbits) on poly q.
+    // bk_unroll 2: TGSW g = 3 m + comp of key pair (2m, 2m+1) encrypts
+    // s_i s_j, s_i (1 - s_j), (1 - s_i) s_j for comp 0, 1, 2.
+    const bool pairs = bk_unroll(p) == 2;
+    parallel_for(bk_tgsw_count(p) * rows, threads, [&](size_t item) {
+        const int g = (int)(item / rows), row = (int)(item % rows);
+        uint32_t msg;
+        uint64_t nonce;
+        if (pairs) {
+            const uint32_t si = lwe_key[2 * (g / 3)], sj = lwe_key[2 * (g / 3) + 1];
+            const int comp = g % 3;
+            msg = comp == 0 ? (si & sj) : comp == 1 ? (si & (1u - sj)) : ((1u - si) & sj);
+            nonce = (DOM_BK2 << 56) | ((uint64_t)(g / 3) << 16) | ((uint64_t)comp << 8) | (uint64_t)row;
+        } else {
+            msg = lwe_key[g];
+            nonce = (DOM_BK << 56) | ((uint64_t)g << 16) | (uint64_t)row;
+        }
         uint32_t *trlwe = bk + item * (size_t)(k + 1) * N;
         uint32_t *mask = trlwe, *body = trlwe + (size_t)k * N;
-        Stream r(seed, (DOM_BK << 56) | ((uint64_t)i << 16) | (uint64_t)row);
+        Stream r(seed, nonce);
         for (int j = 0; j < N; j++) mask[j] = r.u32();
         for (int j = 0; j < N; j++) body[j] = r.gauss_torus(p->bk_stdev);
         for (int s : support) {  // body += X^s * mask (negacyclic)
@@ -191,7 +210,7 @@ int hb_keygen(const hb_params *p, uint64_t seed, uint32_t *lwe_key, uint32_t *tr
             for (int j = N - s; j < N; j++) body[j + s - N] -= mask[j];
         }
         const int q = row / l, pp = row % l;
-        trlwe[(size_t)q * N] += lwe_key[i] * (1u << (32 - (pp + 1) * p->bg_bits));
+        trlwe[(size_t)q * N] += msg * (1u << (32 - (pp + 1) * p->bg_bits));
     });
 
     const int nin = k * N;

@@ -25,6 +25,8 @@ constexpr int kKskStride = 640;   // words per device KSK row (n + 1 padded)
 
 void set_error(const std::string &msg);
 bool params_ok(const hb_params *p);
+int bk_unroll(const hb_params *p);          // 1 or 2 (0 reads as 1)
+size_t bk_tgsw_count(const hb_params *p);   // TGSW samples in the bootstrapping key
 
 // Bootstrapped-gate work items produced from hb_gate records.
 struct BrItem {      // lin = (0, c0) + alpha * pool[src_a] + beta * pool[src_b]

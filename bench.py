@@ -41,11 +41,18 @@ for _p in (ROOT, os.path.join(ROOT, "baseline", "_ref")):
 
 import numpy as np  # noqa: E402
 
-# F_BS: algorithmic FP64 flops of one blind rotation:
-# n * [(k+1)(l+1) * F_FFT + (k+1)^2 * l * (N/2) * 8],  F_FFT = 5 (N/2) log2(N/2) + 6 (N/2)
+# F_BS: algorithmic FP64 flops of one blind rotation.
+# CGGI key (bk_unroll 1): n * [(k+1)(l+1) * F_FFT + (k+1)^2 * l * (N/2) * 8],
+#   F_FFT = 5 (N/2) log2(N/2) + 6 (N/2) (transform + twist), 8 flops per complex MAC.
+# Key pairs (bk_unroll 2): n/2 * [(k+1)(l+1) * F_FFT + (k+1) l * 3 * (N/2) * (6 + 2 * 8) + 3 * (N/2) * 7]:
+#   per pair one external product; per (digit row, component, bin) one complex
+#   product with (X^e - 1) and two complex MACs; (X^e - 1) evaluated once per
+#   component and bin (complex product + subtraction).
 F_FFT = 5 * 512 * 9 + 6 * 512
-F_BS = 630 * (2 * 4 * F_FFT + 4 * 3 * 512 * 8)
-assert F_BS == 162_570_240
+F_BS1 = 630 * (2 * 4 * F_FFT + 4 * 3 * 512 * 8)
+F_BS2 = 315 * (2 * 4 * F_FFT + 2 * 3 * 3 * 512 * 22 + 3 * 512 * 7)
+assert F_BS1 == 162_570_240 and F_BS2 == 133_056_000
+F_BS = {1: F_BS1, 2: F_BS2}
 METRIC = "bootstrapped gates/sec"
 WORKLOAD = "cfg1: 4096 independent bootstrapped NAND gates per GPU (TFHE n=630,N=1024,k=1,Bg=2^7,l=3,KS 2^2x8)"
 
@@ -59,6 +66,7 @@ def parse_args():
     ap.add_argument("--gates", type=int, default=4096)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-compare", action="store_true", help="skip the CGGI-key-layout comparison leg")
     ap.add_argument("--bnn", choices=("none", "neuron", "layer", "cfg3", "cfg4", "cfg5"), default="neuron",
                     help="extra encrypted-BNN latency measurement (BASELINE configs 2-5) on rank 0")
     return ap.parse_args()
@@ -256,6 +264,38 @@ def bnn_latency(kind, seed):
     return rep
 
 
+def cggi_layout_leg(args, dist, dev, recs, h_in, steps=5):
+    """The same NAND step with the CGGI bootstrapping key (bk_unroll 1: one
+    external product per key bit) on a second engine, for comparison with the
+    default key-pair layout."""
+    from paper_1806_03461_b200 import tfhe
+
+    p = tfhe.default_params()
+    p.bk_unroll = 1
+    keys = tfhe.KeySet(seed=args.seed, params=p)
+    eng = tfhe.Engine(keys, device=dev)
+    n = recs.size
+    eng.reserve(3 * n)
+    eng.upload(0, h_in)
+    for _ in range(3):
+        eng.run_gates(recs)
+    eng.sync()
+    dist.barrier()
+    tot, brs = 0.0, []
+    for _ in range(steps):
+        eng.flush_l2()
+        eng.sync()
+        eng.run_gates(recs)
+        br, ks = eng.last_timing()
+        brs.append(br)
+        tot += br + ks
+    value = n * dist.world * steps / dist.max(tot / 1e3)
+    eng.close()
+    return {"bk_unroll": 1, "value": value, "unit": "gates/s", "blind_rotate_ms": statistics.median(brs),
+            "kernel": "k_blind_rotate", "flops_per_bootstrap": F_BS[1], "steps": steps,
+            "note": "CGGI key layout (one TGSW per key bit), same inputs, L2 flushed per step"}
+
+
 def last_profiled_traffic(kernel="k_blind_rotate"):
     """DRAM bytes per launch of `kernel` from the newest profiles/*/traffic.json
     (written by scripts/ncu_summary.py from an `ncu --set full` capture)."""
@@ -364,7 +404,8 @@ def run_ours(args, dist):
     correct &= bool(np.array_equal(keys.decrypt(h_out2[1]), 1 - (a & b))) or args.steps < 2
 
     br_med = statistics.median(br_ms)
-    achieved = n * F_BS / (br_med / 1e3) / 1e12
+    unroll = 2 if keys.params.bk_unroll == 2 else 1
+    achieved = n * F_BS[unroll] / (br_med / 1e3) / 1e12
     traffic, traffic_src = last_profiled_traffic()
     # nominal FP64 peak: 64 DFMA lanes per SM x 2 flops x max SM clock
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -384,13 +425,16 @@ def run_ours(args, dist):
         "gpu_launches": int(launches),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic, "traffic_source": traffic_src,
-                     "kernel": "k_blind_rotate", "flops_per_bootstrap": F_BS,
+                     "kernel": "k_blind_rotate_u2" if unroll == 2 else "k_blind_rotate",
+                     "flops_per_bootstrap": F_BS[unroll],
                      "peak_source": "DFMA micro-benchmark in this run (MEASURED_PEAKS.json has no FP64 figure)",
                      "peak_nominal": nominal, "frac_of_nominal": (achieved / nominal) if nominal else None},
         "kernel_ms": {"blind_rotate": br_med, "key_switch": statistics.median(ks_ms)},
         "clocks": clk,
         "correct": correct,
     }
+    if not args.no_compare:
+        line["alt_layout"] = cggi_layout_leg(args, dist, dev, recs, h_in)
     if dist.rank == 0 and args.bnn != "none":
         try:
             line["bnn"] = bnn_latency(args.bnn, args.seed)

@@ -27,7 +27,7 @@ void or_default_params(or_params *p) {
     p->l = 3;
     p->ks_base_bits = 2;
     p->ks_t = 8;
-    p->bk_unroll = 1;
+    p->bk_unroll = 2;  /* key pairs */
     p->lwe_stdev = 1.0 / 32768.0;      /* 2^-15 */
     p->bk_stdev = 1.0 / 33554432.0;    /* 2^-25 */
 }

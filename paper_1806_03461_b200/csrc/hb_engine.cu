@@ -1000,10 +1000,19 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate_u2(const BrArgs args
 #pragma unroll
             for (int c = 0; c < 3; c++) {
                 double2 F[8];  // (X^{e_c} - 1) at this thread's bins (recomputed per row pair: registers)
+                {
+                    // psi^{e(4t+1)} w8^{e m}: w8^{4e} = (-1)^e, so bins m + 4 are bins m
+                    // with the sign flipped for odd e (integer sign-bit flips, no FP64 work)
+                    const long long flip = (long long)(ex[c] & 1) << 63;
+                    double2 p[4];
 #pragma unroll
-                for (int m = 0; m < 8; m++) {
-                    const double2 p = m == 0 ? base[c] : cmul(base[c], c_w8[(ex[c] * m) & 7]);
-                    F[m] = make_double2(p.x - 1.0, p.y);
+                    for (int m = 0; m < 4; m++) p[m] = m == 0 ? base[c] : cmul(base[c], c_w8[(ex[c] * m) & 7]);
+#pragma unroll
+                    for (int m = 0; m < 4; m++) {
+                        F[m] = make_double2(p[m].x - 1.0, p[m].y);
+                        F[m + 4] = make_double2(__longlong_as_double(__double_as_longlong(p[m].x) ^ flip) - 1.0,
+                                                __longlong_as_double(__double_as_longlong(p[m].y) ^ flip));
+                    }
                 }
 #pragma unroll
                 for (int h = 0; h < 2; h++, st++) {
@@ -1062,6 +1071,204 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate_u2(const BrArgs args
     }
     uint32_t *out = args.big + (size_t)e * kBigStride;
     for (int c = t; c <= kN; c += 64) {
+        uint32_t v;
+        if (c == 0) v = accA[0];
+        else if (c < kN) v = 0u - accA[kN - c];
+        else v = accB[0];
+        out[c] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Latency mode with the key-pair key (narrow levels): one bootstrap per CTA,
+// three 64-thread groups; group r takes digit rows 2r, 2r+1 of every key pair
+// (one dual forward FFT + the 6 (component, row) MAC stages, streamed through a
+// 3-deep per-group ring), writes its partial Fourier sums into its exchange
+// buffer; groups 0/1 sum the partials of output polynomial 0/1, run its inverse
+// FFT and update ACC.
+// ---------------------------------------------------------------------------
+constexpr int kLatStagesU2 = 3;
+
+struct BrLatSmemU2 {
+    double2 bk[3][kLatStagesU2][2 * kNH];    // per-group stage rings
+    uint64_t full[3][kLatStagesU2], empty[3][kLatStagesU2];
+    uint32_t acc[2][kN];
+    double2 xch[3][2][kXchStride];           // per-group single-buffered exchange; partials [o][512]
+    uint16_t bar[kMaxLweN + 1];
+    TwSeeds tws[64];
+};
+
+template <bool kDebug>
+__global__ void __launch_bounds__(192, 1) k_blind_rotate_u2_lat(const BrArgs args) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    BrLatSmemU2 &sm = *reinterpret_cast<BrLatSmemU2 *>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = warp >> 1;
+    const int t = threadIdx.x & 63;
+    const int bar_id = 1 + grp;
+    const int n = args.n;
+    const int pairs = min(n, args.iters) / 2;
+    const int stages_needed = pairs * 6;  // this group's stages
+    const char *bk_src = reinterpret_cast<const char *>(args.bkf);
+    const uint32_t e = blockIdx.x;
+    uint32_t *accA = sm.acc[0];
+    uint32_t *accB = sm.acc[1];
+    double2 *xch = &sm.xch[grp][0][0];
+    uint64_t *full = sm.full[grp], *empty = sm.empty[grp];
+    // group-local stage s -> global stage (s / 6) * 18 + grp * 6 + s % 6
+    auto stage_src = [&](int s) {
+        return bk_src + (size_t)((s / 6) * kStagesPerPair + grp * 6 + s % 6) * kRowBytes;
+    };
+
+    if (threadIdx.x < 64) {
+        TwSeeds ts;
+        ts.f_a0 = args.TW[t];
+        ts.step_a = args.W[t];
+        ts.step_b = args.W[8 * (t & 7)];
+        ts.i_b0 = args.TW[t >> 3];
+        ts.i_stepb = args.TW[32 * (t & 7) + 8];
+        sm.tws[t] = ts;
+    }
+    int issued = 0;  // group producer (t == 0) state
+    if (t == 0) {
+        for (int s = 0; s < kLatStagesU2; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 2);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (; issued < kLatStagesU2 && issued < stages_needed; issued++) {
+            mbar_arrive_expect_tx(&full[issued], kRowBytes);
+            bulk_g2s(sm.bk[grp][issued], stage_src(issued), kRowBytes, &full[issued]);
+        }
+    }
+    {   // K1: linear combination + modulus switch (all 192 threads)
+        const uint32_t lanes = args.lanes;
+        const BrItem it = args.items[e / lanes];
+        const uint32_t lane_id = e % lanes;
+        const int alpha = (int8_t)(it.coef & 0xFF), beta = (int8_t)((it.coef >> 8) & 0xFF);
+        const uint32_t *A = args.pool + ((size_t)it.src_a * lanes + lane_id) * args.pool_stride;
+        const uint32_t *B = args.pool + ((size_t)it.src_b * lanes + lane_id) * args.pool_stride;
+        for (int c = threadIdx.x; c <= n; c += 192) {
+            uint32_t v = (uint32_t)alpha * __ldg(&A[c]);
+            if (beta) v += (uint32_t)beta * __ldg(&B[c]);
+            if (c == n) v += it.c0;
+            sm.bar[c] = (uint16_t)(((v + (1u << 20)) >> 21) & (2 * kN - 1));
+        }
+    }
+    __syncthreads();
+    {
+        const int barb = sm.bar[n];
+        for (int i = threadIdx.x; i < kN; i += 192) {
+            accA[i] = 0;
+            accB[i] = (((i + barb) & kN) ? 0u - args.mu : args.mu);
+        }
+    }
+    __syncthreads();
+
+    double max_err = 0.0;
+    int st = 0;  // this group's next stage
+    for (int pm = 0; pm < pairs; pm++) {
+        const int ai = sm.bar[2 * pm], aj = sm.bar[2 * pm + 1];
+        double2 x[2][8];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int row = 2 * grp + h;
+            const int q = row / kL, p = row % kL;
+            const uint32_t *P = q ? accB : accA;
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                const int j = t + 64 * m;
+                x[h][m] = make_double2(small_int_to_double(gadget_digit(P[j], p)),
+                                       small_int_to_double(gadget_digit(P[j + kNH], p)));
+            }
+        }
+        nega_fft_fwd_n<2, true>(x, xch, t, sm.tws[t], bar_id);
+        double2 f0[8], f1[8];
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            const int ec = c == 0 ? ((ai + aj) & (2 * kN - 1)) : (c == 1 ? ai : aj);
+            double2 F[8];
+            {
+                const double2 base = __ldg(&args.PSI[(ec * (4 * t + 1)) & (2 * kN - 1)]);
+                const long long flip = (long long)(ec & 1) << 63;
+                double2 p[4];
+#pragma unroll
+                for (int m = 0; m < 4; m++) p[m] = m == 0 ? base : cmul(base, c_w8[(ec * m) & 7]);
+#pragma unroll
+                for (int m = 0; m < 4; m++) {
+                    F[m] = make_double2(p[m].x - 1.0, p[m].y);
+                    F[m + 4] = make_double2(__longlong_as_double(__double_as_longlong(p[m].x) ^ flip) - 1.0,
+                                            __longlong_as_double(__double_as_longlong(p[m].y) ^ flip));
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; h++, st++) {
+                const int s = st % kLatStagesU2;
+                mbar_wait(&full[s], (st / kLatStagesU2) & 1);
+                const double2 *bk0 = sm.bk[grp][s];
+                const double2 *bk1 = sm.bk[grp][s] + kNH;
+#pragma unroll
+                for (int m = 0; m < 8; m++) {
+                    const double2 y = cmul(x[h][m], F[m]);
+                    if (c == 0 && h == 0) {
+                        f0[m] = cmul(y, bk0[t + 64 * m]);
+                        f1[m] = cmul(y, bk1[t + 64 * m]);
+                    } else {
+                        cmac(f0[m], y, bk0[t + 64 * m]);
+                        cmac(f1[m], y, bk1[t + 64 * m]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                if (t == 0 && issued < stages_needed) {  // refill this slot kLatStagesU2 stages ahead
+                    mbar_wait(&empty[s], ((issued / kLatStagesU2) - 1) & 1);
+                    mbar_arrive_expect_tx(&full[s], kRowBytes);
+                    bulk_g2s(sm.bk[grp][s], stage_src(issued), kRowBytes, &full[s]);
+                    issued++;
+                }
+                __syncwarp();
+            }
+        }
+        // partials into this group's exchange buffer: [0][.] output poly 0, [1][.] output poly 1
+        group_bar(bar_id);  // the forward FFT's last readers of xch are done
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+            xch[t + 64 * m] = f0[m];
+            xch[kNH + t + 64 * m] = f1[m];
+        }
+        __syncthreads();
+        if (grp < 2) {
+            double2 y[1][8];
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                const int k = grp * kNH + t + 64 * m;
+                y[0][m] = cadd(cadd(sm.xch[0][0][k], sm.xch[1][0][k]), sm.xch[2][0][k]);
+            }
+            asm volatile("bar.sync 4, 128;" ::: "memory");  // groups 0/1: partial reads done before reuse
+            nega_fft_inv_n<1, true>(y, xch, t, sm.tws[t], bar_id);
+            uint32_t *P = grp ? accB : accA;
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                const double lo = y[0][m].x, hi = y[0][m].y;
+                if (kDebug) {
+                    max_err = fmax(max_err, fabs(lo - rint(lo)));
+                    max_err = fmax(max_err, fabs(hi - rint(hi)));
+                }
+                const int j = t + 64 * m;
+                P[j] += round_to_torus(lo);
+                P[j + kNH] += round_to_torus(hi);
+            }
+        }
+        __syncthreads();  // ACC updated, partials consumed
+    }
+
+    if (kDebug && args.margin) atomicMax(args.margin, (unsigned long long)__double_as_longlong(max_err));
+    if (kDebug && args.acc_dump) {
+        uint32_t *dst = args.acc_dump + (size_t)e * 2 * kN;
+        for (int c = threadIdx.x; c < 2 * kN; c += 192) dst[c] = (c < kN) ? accA[c] : accB[c - kN];
+    }
+    uint32_t *out = args.big + (size_t)e * kBigStride;
+    for (int c = threadIdx.x; c <= kN; c += 192) {
         uint32_t v;
         if (c == 0) v = accA[0];
         else if (c < kN) v = 0u - accA[kN - c];
@@ -1366,6 +1573,12 @@ int launch_br_auto(hb_engine *e, const BrArgs &a, int force_g = 0) {
     const uint32_t sms = (uint32_t)e->num_sms;
     const int gsel = force_g ? force_g : (a.n_work <= sms ? 1 : (a.n_work <= 2u * sms ? 2 : kBrGates));
     if (e->unroll == 2) {
+        if (!force_g && gsel == 1 && e->latency_mode) {
+            k_blind_rotate_u2_lat<kDebug><<<a.n_work, 192, sizeof(BrLatSmemU2), e->stream>>>(a);
+            HB_CUDA_TRY(cudaGetLastError());
+            e->n_launch++;
+            return HB_OK;
+        }
         if (gsel == 1) return launch_br_u2<1, kDebug>(e, a);
         if (gsel == 2) return launch_br_u2<2, kDebug>(e, a);
         return launch_br_u2<kBrGates, kDebug>(e, a);
@@ -1480,6 +1693,10 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
                                      (int)br_smem_bytes<2>()));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)br_smem_bytes<1>()));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_lat<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrLatSmemU2)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_lat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrLatSmemU2)));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_lat<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(BrLatSmem)));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_lat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

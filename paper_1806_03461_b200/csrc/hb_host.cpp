@@ -146,7 +146,7 @@ void hb_default_params(hb_params *p) {
     p->l = 3;
     p->ks_base_bits = 2;
     p->ks_t = 8;
-    p->bk_unroll = 1;
+    p->bk_unroll = 2;  // key pairs (one external product per two key bits)
     p->lwe_stdev = 1.0 / 32768.0;    // 2^-15
     p->bk_stdev = 1.0 / 33554432.0;  // 2^-25
 }

@@ -16,8 +16,8 @@ import numpy as np
 from .tfhe import KeySet, default_params
 
 FORMAT = "hebnn-b200/tfhe"
-VERSION = 1
-_PARAM_FIELDS = ("n", "N", "k", "bg_bits", "l", "ks_base_bits", "ks_t", "lwe_stdev", "bk_stdev")
+VERSION = 2  # 2: params carry bk_unroll (bootstrapping-key layout)
+_PARAM_FIELDS = ("n", "N", "k", "bg_bits", "l", "ks_base_bits", "ks_t", "bk_unroll", "lwe_stdev", "bk_stdev")
 
 
 def _params_doc(p):

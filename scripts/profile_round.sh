@@ -4,7 +4,7 @@ set -u
 TAG=${1:-prof}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
-CMD="python bench.py --steps 3 --warmup 3 --bnn none --no-cpu-baseline"
+CMD="python bench.py --steps 3 --warmup 3 --bnn none --no-cpu-baseline --no-compare"
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/nvsmi.txt 2>&1
 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 $CMD > $OUT/plain.log 2>&1 && \

@@ -24,6 +24,28 @@ def cuda_available():
         return False
 
 
+# Default key layout (bk_unroll 2, key pairs) and, suffixed 1, the CGGI layout
+# (bk_unroll 1, one TGSW per key bit); both are product paths with their own
+# oracle restatement and golden vectors.
+
+def oracle_params(unroll=None):
+    from oracle import oracle as O
+
+    p = O.default_params()
+    if unroll is not None:
+        p.bk_unroll = unroll
+    return p
+
+
+def product_params(unroll=None):
+    from paper_1806_03461_b200 import tfhe
+
+    p = tfhe.default_params()
+    if unroll is not None:
+        p.bk_unroll = unroll
+    return p
+
+
 @pytest.fixture(scope="session")
 def keys():
     from paper_1806_03461_b200 import tfhe
@@ -35,14 +57,14 @@ def keys():
 def okeys():
     from oracle import oracle as O
 
-    return O.Keys(O.default_params(), 42)
+    return O.Keys(oracle_params(), 42)
 
 
 @pytest.fixture(scope="session")
 def octx(okeys):
     from oracle import oracle as O
 
-    return O.Context(O.default_params(), okeys)
+    return O.Context(oracle_params(), okeys)
 
 
 @pytest.fixture(scope="session")
@@ -50,5 +72,35 @@ def engine(keys):
     from paper_1806_03461_b200 import tfhe
 
     eng = tfhe.Engine(keys, device=0)
+    yield eng
+    eng.close()
+
+
+@pytest.fixture(scope="session")
+def keys1():
+    from paper_1806_03461_b200 import tfhe
+
+    return tfhe.KeySet(seed=42, params=product_params(1))
+
+
+@pytest.fixture(scope="session")
+def okeys1():
+    from oracle import oracle as O
+
+    return O.Keys(oracle_params(1), 42)
+
+
+@pytest.fixture(scope="session")
+def octx1(okeys1):
+    from oracle import oracle as O
+
+    return O.Context(oracle_params(1), okeys1)
+
+
+@pytest.fixture(scope="session")
+def engine1(keys1):
+    from paper_1806_03461_b200 import tfhe
+
+    eng = tfhe.Engine(keys1, device=0)
     yield eng
     eng.close()

@@ -15,6 +15,7 @@ class OracleEngine:
     def __init__(self, keys):
         self.keys = keys
         self.p = O.default_params()
+        self.p.bk_unroll = keys.params.bk_unroll
         ok = O.Keys(self.p, keys.seed)
         assert np.array_equal(ok.lwe_key, keys.lwe_key), "oracle and product keys differ"
         self.ctx = O.Context(self.p, ok)

@@ -12,21 +12,31 @@ pytestmark = pytest.mark.gpu
 P = O.default_params()
 
 
+@pytest.fixture(params=["pairs", "cggi"])
+def kit(request):
+    """(engine, keys, oracle context) of one bootstrapping-key layout:
+    key pairs (bk_unroll 2, default) or CGGI (bk_unroll 1)."""
+    sfx = "" if request.param == "pairs" else "1"
+    return tuple(request.getfixturevalue(name + sfx) for name in ("engine", "keys", "octx"))
+
+
 def _lin(keys, seed, count):
     rng = np.random.default_rng(seed)
     bits = rng.integers(0, 2, count).astype(np.uint8)
     return keys.encrypt(bits, seed=seed, stream=1)
 
 
-@pytest.mark.parametrize("iters", [1, 2, 7])
-def test_blind_rotate_prefix_bit_exact(engine, keys, octx, iters):
+@pytest.mark.parametrize("iters", [1, 2, 7, 10])
+def test_blind_rotate_prefix_bit_exact(kit, iters):
+    engine, keys, octx = kit
     lwe = _lin(keys, 11, 1)[0]
     got = engine.debug_blind_rotate(lwe, iters=iters)
     want = octx.blind_rotate(lwe, iters=iters)
     assert np.array_equal(got, want)
 
 
-def test_bootstrap_wo_ks_bit_exact(engine, keys, octx):
+def test_bootstrap_wo_ks_bit_exact(kit):
+    engine, keys, octx = kit
     lin = _lin(keys, 12, 6)
     got = engine.debug_bootstrap_wo_ks(lin)
     margin = engine.debug_fft_margin()
@@ -35,7 +45,8 @@ def test_bootstrap_wo_ks_bit_exact(engine, keys, octx):
     assert margin < 0.25, margin
 
 
-def test_keyswitch_bit_exact(engine, keys, octx):
+def test_keyswitch_bit_exact(kit):
+    engine, keys, octx = kit
     rng = np.random.default_rng(13)
     big = rng.integers(0, 2**32, (40, P.N + 1), dtype=np.uint64).astype(np.uint32)
     got = engine.debug_keyswitch(big)
@@ -44,7 +55,8 @@ def test_keyswitch_bit_exact(engine, keys, octx):
 
 
 @pytest.mark.parametrize("name", list(tfhe.GATE_LIN))
-def test_gate_truth_table_and_bit_exact(engine, keys, octx, name):
+def test_gate_truth_table_and_bit_exact(kit, name):
+    engine, keys, octx = kit
     c0, al, be = tfhe.GATE_LIN[name]
     a_bits = np.array([0, 0, 1, 1], np.uint8)
     b_bits = np.array([0, 1, 0, 1], np.uint8)
@@ -68,7 +80,8 @@ def test_gate_truth_table_and_bit_exact(engine, keys, octx, name):
         assert np.array_equal(out[i], octx.gate(c0, al, ca[i], be, cb[i]))
 
 
-def test_mux_bit_exact(engine, keys, octx):
+def test_mux_bit_exact(kit):
+    engine, keys, octx = kit
     s = np.array([0, 0, 0, 0, 1, 1, 1, 1], np.uint8)
     a = np.array([0, 0, 1, 1, 0, 0, 1, 1], np.uint8)
     b = np.array([0, 1, 0, 1, 0, 1, 0, 1], np.uint8)
@@ -87,16 +100,21 @@ def test_mux_bit_exact(engine, keys, octx):
         assert np.array_equal(out[i], octx.mux(cs[i], ca[i], cb[i]))
 
 
-def test_gpu_matches_committed_golden_vectors(engine, keys):
-    """The sm_100a engine reproduces tests/golden/tfhe_golden_seed42.npz
-    (oracle-generated: keys from seed 42, encryptions, gates, MUX, stages)."""
+def test_gpu_matches_committed_golden_vectors(kit):
+    """The sm_100a engine reproduces tests/golden/tfhe_golden_seed42.npz (CGGI)
+    and tfhe_golden_pairs_seed42.npz (key pairs) — oracle-generated: keys from
+    seed 42, encryptions, gates, MUX, stages."""
     import os
 
-    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "tfhe_golden_seed42.npz"))
+    engine, keys, _ = kit
+    pairs = keys.params.bk_unroll == 2
+    name = "tfhe_golden_pairs_seed42.npz" if pairs else "tfhe_golden_seed42.npz"
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", name))
     assert np.array_equal(keys.lwe_key, g["lwe_key"])
+    assert int(g["bk_sum"]) == int(keys.bk.astype(np.uint64).sum())
     inputs = g["inputs"]
     assert np.array_equal(keys.encrypt(g["input_bits"], seed=42, stream=77), inputs)
-    assert np.array_equal(engine.debug_blind_rotate(inputs[0], iters=3), g["acc_prefix3"])
+    assert np.array_equal(engine.debug_blind_rotate(inputs[0], iters=4 if pairs else 3), g["acc_prefix3"])
     assert np.array_equal(engine.debug_bootstrap_wo_ks(inputs[2:3])[0], g["bootstrap_wo_ks"])
     assert np.array_equal(engine.debug_keyswitch(g["ks_in"][None, :])[0], g["ks_out"])
     engine.reserve(16)

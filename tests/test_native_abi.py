@@ -33,12 +33,24 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_params():
     L = _native.lib()
-    assert L.hb_abi_version() == 1
+    assert L.hb_abi_version() == 2
     p = _native.default_params()
     assert (p.n, p.N, p.k, p.bg_bits, p.l, p.ks_base_bits, p.ks_t) == (630, 1024, 1, 7, 3, 2, 8)
     assert L.hb_lwe_words(ctypes.byref(p)) == 631
-    assert L.hb_bk_words(ctypes.byref(p)) == 630 * 6 * 2 * 1024
     assert L.hb_ksk_words(ctypes.byref(p)) == 1024 * 8 * 3 * 631
+    p.bk_unroll = 1
+    assert L.hb_bk_words(ctypes.byref(p)) == 630 * 6 * 2 * 1024
+    p.bk_unroll = 2  # key pairs: 3 TGSW per pair
+    assert L.hb_bk_words(ctypes.byref(p)) == 315 * 3 * 6 * 2 * 1024
+
+
+def test_key_pairs_need_even_n():
+    p = _native.default_params()
+    p.bk_unroll, p.n = 2, 629
+    out = np.zeros(4, np.uint32)
+    rc = _native.lib().hb_keygen(ctypes.byref(p), 1, _native.u32p(out), _native.u32p(out),
+                                 _native.u32p(out), _native.u32p(out), 1)
+    assert rc == _native.HB_EINVAL
 
 
 def test_invalid_arguments_are_value_errors(keys):

@@ -11,12 +11,14 @@ from oracle import oracle as O
 
 P = O.default_params()
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "tfhe_golden_seed42.npz")
+GOLDEN_PAIRS = os.path.join(os.path.dirname(__file__), "golden", "tfhe_golden_pairs_seed42.npz")
 
 
 def test_default_params_match_baseline():
     # BASELINE.json configs[0]
     assert (P.n, P.N, P.k, P.bg_bits, P.l, P.ks_base_bits, P.ks_t) == (630, 1024, 1, 7, 3, 2, 8)
     assert P.lwe_stdev == 2.0 ** -15 and P.bk_stdev == 2.0 ** -25
+    assert P.bk_unroll == 2  # key-pair bootstrapping key by default; 1 = one TGSW per key bit
 
 
 @pytest.mark.parametrize("seed", [0, 1, 2])
@@ -77,16 +79,54 @@ def test_keyswitch_key_decrypts_to_scaled_key_bits(okeys):
 
 
 @pytest.mark.skipif(not os.path.exists(GOLDEN), reason="golden vectors not generated")
-def test_oracle_reproduces_golden_vectors(okeys, octx):
-    g = np.load(GOLDEN)
+def _check_golden(path, okeys, octx, prefix_iters):
+    g = np.load(path)
     assert g["lwe_key"].tobytes() == okeys.lwe_key.tobytes()
     assert int(g["bk_sum"]) == int(okeys.bk.astype(np.uint64).sum())
     assert int(g["ksk_sum"]) == int(okeys.ksk.astype(np.uint64).sum())
     inputs = g["inputs"]
     assert np.array_equal(O.encrypt(P, okeys, g["input_bits"], 42, 77), inputs)
-    assert np.array_equal(octx.blind_rotate(inputs[0], iters=3), g["acc_prefix3"])
+    assert np.array_equal(octx.blind_rotate(inputs[0], iters=prefix_iters), g["acc_prefix3"])
     assert np.array_equal(octx.keyswitch(g["ks_in"]), g["ks_out"])
     for name, (c0, al, be) in O.GATE_LIN.items():
         if name in ("AND", "XOR"):
             out = octx.gate(c0, al, inputs[0], be, inputs[1])
             assert np.array_equal(out, g[f"gate_{name}"]), name
+
+
+def test_oracle_reproduces_golden_vectors(okeys1, octx1):
+    """CGGI layout (bk_unroll 1)."""
+    _check_golden(GOLDEN, okeys1, octx1, 3)
+
+
+def test_oracle_reproduces_golden_vectors_key_pairs(okeys, octx):
+    """Key-pair layout (bk_unroll 2, the default)."""
+    _check_golden(GOLDEN_PAIRS, okeys, octx, 4)
+
+
+def test_cggi_key_layout_bit_identical_to_oracle(keys1, okeys1):
+    assert np.array_equal(keys1.bk, okeys1.bk.reshape(-1))
+    assert np.array_equal(keys1.ksk, okeys1.ksk.reshape(-1))
+
+
+def _acc_phase(okeys, acc):
+    """Phase polynomial B - A*s of a TRLWE accumulator (exact)."""
+    A, B = acc[:1024], acc[1024:]
+    s = okeys.trlwe_key.astype(np.int32)
+    return (B - O.negacyclic_mul(s, A)).astype(np.uint32).view(np.int32).astype(np.int64)
+
+
+def test_key_pair_blind_rotation_equals_cggi_blind_rotation(okeys, octx, okeys1, octx1):
+    """The key-pair CMux rotates the accumulator by X^{a_i s_i + a_j s_j} per
+    pair, so after the whole key both layouts hold X^{sum a_i s_i - b} * TV:
+    identical message polynomials (+-1/8 per coefficient), independent noise."""
+    assert np.array_equal(okeys.lwe_key, okeys1.lwe_key)
+    rng = np.random.default_rng(8)
+    for trial in range(3):
+        lwe = O.encrypt(P, okeys, rng.integers(0, 2, 1).astype(np.uint8), 3, 40 + trial)[0]
+        ph2 = _acc_phase(okeys, octx.blind_rotate(lwe))
+        ph1 = _acc_phase(okeys1, octx1.blind_rotate(lwe))
+        eighth = 1 << 29
+        for ph in (ph1, ph2):
+            assert np.all(np.abs(np.abs(ph) - eighth) < eighth // 4)
+        assert np.array_equal(np.sign(ph1), np.sign(ph2))

@@ -193,7 +193,7 @@ def cpu_nand_sample(seed, gates, threads):
     pool[:gates] = O.encrypt(p, keys, a, seed, 1)
     pool[gates:2 * gates] = O.encrypt(p, keys, b, seed, 2)
     recs = np.zeros(gates, dtype=[("dst", "<u4"), ("src_a", "<u4"), ("src_b", "<u4"), ("src_c", "<u4"),
-                                  ("c0", "<u4"), ("alpha", "i1"), ("beta", "i1"), ("kind", "i1"), ("_pad", "i1")])
+                                  ("c0", "<u4"), ("alpha", "i1"), ("beta", "i1"), ("kind", "i1"), ("gamma", "i1")])
     c0, al, be = O.GATE_LIN["NAND"]
     recs["dst"] = np.arange(2 * gates, 3 * gates)
     recs["src_a"] = np.arange(gates)

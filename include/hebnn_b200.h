@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define HB_ABI_VERSION 2
+#define HB_ABI_VERSION 3
 
 /* status codes */
 #define HB_OK 0
@@ -63,16 +63,22 @@ typedef struct hb_params {
  *   kind HB_GATE_MUX : pool[dst] = src_a ? src_b : src_c (native CGGI MUX:
  *                      2 blind rotations + 1 key switch); alpha / beta are the
  *                      signs (+-1) applied to src_b / src_c (NOT flags).
+ *   kind HB_GATE_LIN3: pool[dst] = KS(BS((0,c0) + alpha*pool[src_a] + beta*pool[src_b]
+ *                      + gamma*pool[src_c])), alpha, beta, gamma in {-2,-1,0,1,2}:
+ *                      one bootstrap for 3-input threshold gates, e.g. majority
+ *                      (c0 0, 1 1 1: a full adder's carry) and 3-input XOR
+ *                      (c0 0, -2 -2 -2: a full adder's sum).
  * Slot numbers address the engine pool; with `lanes` > 1 every record is run
  * for lanes l = 0..lanes-1 on slots (slot * lanes + l). */
 typedef struct hb_gate {
     uint32_t dst, src_a, src_b, src_c;
     uint32_t c0;
-    int8_t alpha, beta, kind, _pad;
+    int8_t alpha, beta, kind, gamma;
 } hb_gate;
 
 #define HB_GATE_LIN2 0
 #define HB_GATE_MUX 1
+#define HB_GATE_LIN3 2
 
 typedef struct hb_engine hb_engine;
 

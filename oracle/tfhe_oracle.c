@@ -662,6 +662,22 @@ void or_gate(const or_ctx *c, uint32_t c0, int32_t alpha, const uint32_t *A, int
     free(lin); free(big);
 }
 
+/* 3-input threshold gate (hb_gate kind LIN3): majority with (0; 1, 1, 1),
+ * 3-input XOR with (0; -2, -2, -2) — the phases +-1/8 sum to +-1/8 or +-3/8,
+ * doubled to +-1/4 mod 1 with the sign carrying the parity. */
+void or_gate3(const or_ctx *c, uint32_t c0, int32_t alpha, const uint32_t *A, int32_t beta,
+              const uint32_t *B, int32_t gamma, const uint32_t *C, uint32_t *out) {
+    const int n = c->p.n, nb = c->p.k * c->p.N;
+    uint32_t *lin = malloc(sizeof(uint32_t) * (n + 1));
+    uint32_t *big = malloc(sizeof(uint32_t) * (nb + 1));
+    for (int i = 0; i <= n; i++)
+        lin[i] = (uint32_t)alpha * A[i] + (uint32_t)beta * B[i] + (uint32_t)gamma * C[i];
+    lin[n] += c0;
+    or_bootstrap_wo_ks(c, lin, 1u << 29, big);
+    or_keyswitch(c, big, out);
+    free(lin); free(big);
+}
+
 void or_mux(const or_ctx *c, const uint32_t *S, const uint32_t *A, const uint32_t *B,
             uint32_t *out) {
     const int n = c->p.n, nb = c->p.k * c->p.N;
@@ -709,6 +725,8 @@ static void run_one(const or_ctx *c, const or_gate_rec *g, uint32_t *pool, size_
         for (int i = 0; i <= nb; i++) u1[i] += u2[i];
         u1[nb] += eighth;
         or_keyswitch(c, u1, dst);
+    } else if (g->kind == 2) {
+        or_gate3(c, g->c0, g->alpha, A, g->beta, B, g->gamma, pool + (size_t)g->src_c * stride, dst);
     } else {
         or_gate(c, g->c0, g->alpha, A, g->beta, g->beta ? B : NULL, dst);
     }

@@ -100,6 +100,9 @@ void or_keyswitch(const or_ctx *c, const uint32_t *in, uint32_t *out);
  * (alpha, beta) in {-2,-1,0,1,2}; B may be NULL when beta == 0. */
 void or_gate(const or_ctx *c, uint32_t c0, int32_t alpha, const uint32_t *A, int32_t beta,
              const uint32_t *B, uint32_t *out);
+/* Three-input bootstrapped threshold gate: out = KS(BS((0,c0) + alpha*A + beta*B + gamma*C)). */
+void or_gate3(const or_ctx *c, uint32_t c0, int32_t alpha, const uint32_t *A, int32_t beta,
+              const uint32_t *B, int32_t gamma, const uint32_t *C, uint32_t *out);
 /* Native CGGI MUX: S ? A : B = KS((0,1/8) + BS((0,-1/8)+S+A) + BS((0,-1/8)-S+B)). */
 void or_mux(const or_ctx *c, const uint32_t *S, const uint32_t *A, const uint32_t *B,
             uint32_t *out);
@@ -109,7 +112,7 @@ void or_mux(const or_ctx *c, const uint32_t *S, const uint32_t *A, const uint32_
 typedef struct or_gate_rec {
     uint32_t dst, src_a, src_b, src_c;
     uint32_t c0;
-    int8_t alpha, beta, kind, _pad;
+    int8_t alpha, beta, kind, gamma;  /* kind 0 LIN2, 1 MUX, 2 LIN3 (gamma * src_c) */
 } or_gate_rec;
 int or_run_gates(const or_ctx *c, const or_gate_rec *gates, size_t n, uint32_t *pool,
                  size_t pool_stride, int threads);

@@ -22,6 +22,7 @@ HB_ENOMEM = -3
 
 GATE_LIN2 = 0
 GATE_MUX = 1
+GATE_LIN3 = 2
 
 # Every symbol the header declares (tests check the library exports them all).
 EXPORTED = (
@@ -60,7 +61,7 @@ class HbParams(ctypes.Structure):
 
 GATE_DTYPE = np.dtype(
     [("dst", "<u4"), ("src_a", "<u4"), ("src_b", "<u4"), ("src_c", "<u4"), ("c0", "<u4"),
-     ("alpha", "i1"), ("beta", "i1"), ("kind", "i1"), ("_pad", "i1")]
+     ("alpha", "i1"), ("beta", "i1"), ("kind", "i1"), ("gamma", "i1")]
 )
 assert GATE_DTYPE.itemsize == 24
 

@@ -21,7 +21,11 @@ of the reference API) runs every pending node on the GPU one level at a time
 (the level histogram is the batch schedule).  While building the
 DAG, gates whose result is already determined are not bootstrapped (trivial
 inputs, repeated inputs, common subexpressions, MUX with trivial data inputs);
-the counted `GateStats` are unaffected and decrypted values are identical
+a full adder's OR(AND(a,b), AND(XOR(a,b),c)) becomes one 3-input majority
+bootstrap and XOR(XOR(a,b),c) one 3-input XOR bootstrap (hb_gate LIN3), and a
+flush executes only the pending gates that a live handle still reaches (the
+rest stay in the DAG, dormant, and run if they are ever needed again).  The
+counted `GateStats` are unaffected and decrypted values are identical
 (SURVEY.md §8 f2).  With ``lanes = B`` every handle carries B independent
 ciphertexts that share one DAG.
 """
@@ -35,7 +39,7 @@ import weakref
 import numpy as np
 
 from . import gate_api as api
-from ._native import GATE_DTYPE, GATE_LIN2, GATE_MUX
+from ._native import GATE_DTYPE, GATE_LIN2, GATE_LIN3, GATE_MUX
 from .gate_api import AND, MUX, OR, XNOR, XOR, CipherBit, ContextMismatchError, GateBackend, GateStats, ScopeError
 from .tfhe import EIGHTH, MASK32, Engine, KeySet
 
@@ -45,6 +49,8 @@ _OP_INPUT = 1   # fresh encryption
 _OP_AND = 2     # AND(ref_a, ref_b): NOT flags live in the refs
 _OP_XOR = 3     # XOR(node_a, node_b): NOT flags are pushed to the output ref
 _OP_MUX = 4     # MUX(node_s, ref_a, ref_b): selector kept positive
+_OP_MAJ = 5     # MAJ(ref_a, ref_b, ref_c): 3-input majority (a full adder's carry)
+_OP_XOR3 = 6    # XOR3(node_a, node_b, node_c): NOT flags pushed to the output ref
 
 _C_AND = (-EIGHTH) & MASK32
 _C_XOR = 2 * EIGHTH
@@ -52,6 +58,19 @@ _C_XOR = 2 * EIGHTH
 
 class DeviceError(RuntimeError):
     """Raised when the B200 engine cannot run (no device, CUDA failure)."""
+
+
+class _Bit(CipherBit):
+    """`CipherBit` that tells its context when it dies, so a flush can skip
+    gates no live handle reaches (the handle contract is the reference's)."""
+
+    __slots__ = ()
+
+    def __del__(self):
+        try:
+            self._ctx._drop(self._value >> 1)
+        except Exception:  # interpreter shutdown
+            pass
 
 
 # ---------------------------------------------------------------------------
@@ -171,8 +190,10 @@ class TfheContext(GateBackend):
         self._lvl = [0]        # execution level (after elision)
         self._slot = [-1]      # logical pool slot
         self._done = [True]
+        self._hcnt = [0]       # live handles per node
         self._cse = {}
         self._pending = []     # node ids not yet executed
+        self._dormant = set()  # not executed: unreachable from live handles at their flush
         self._inputs = {}      # node id -> host ciphertexts [lanes][n+1] not yet uploaded
         self._engine = None
         self._slots = None
@@ -234,6 +255,37 @@ class TfheContext(GateBackend):
         self._lvl.append(lvl)
         self._slot.append(slot)
         self._done.append(False)
+        self._hcnt.append(0)
+        if self._dormant and op != _OP_INPUT:
+            for r in (a, b, c):
+                if (r >> 1) in self._dormant:
+                    self._revive(r >> 1)
+        return nid
+
+    def _bit(self, r, level, trivial=None):
+        """A handle on ref r (counted for the live-gate filter of flush)."""
+        self._hcnt[r >> 1] += 1
+        return _Bit(self, r, level, trivial)
+
+    def _drop(self, nid):
+        self._hcnt[nid] -= 1
+
+    def _revive(self, nid):
+        """Dormant node (and its dormant operands) back to pending."""
+        stack = [nid]
+        while stack:
+            n = stack.pop()
+            if n not in self._dormant:
+                continue
+            self._dormant.discard(n)
+            self._pending.append(n)
+            if self._op[n] != _OP_INPUT:
+                stack.extend((self._a[n] >> 1, self._b[n] >> 1, self._c[n] >> 1))
+
+    def _cse_get(self, key):
+        nid = self._cse.get(key)
+        if nid is not None and nid in self._dormant:
+            self._revive(nid)
         return nid
 
     def encrypt(self, b):
@@ -257,7 +309,7 @@ class TfheContext(GateBackend):
             nid = self._add_node(_OP_INPUT, 0, 0, 0, 0, slot)
             self._done[nid] = True  # value known on the host; uploaded at flush
             self._inputs[nid] = cts
-            return CipherBit(self, nid << 1, 0)
+            return self._bit(nid << 1, 0)
 
     def encrypt_many(self, bits):
         """Vectorised encrypt: bits shape [count] (broadcast over lanes) or
@@ -280,7 +332,7 @@ class TfheContext(GateBackend):
                 nid = self._add_node(_OP_INPUT, 0, 0, 0, 0, slot)
                 self._done[nid] = True
                 self._inputs[nid] = cts[i]
-                out.append(CipherBit(self, nid << 1, 0))
+                out.append(self._bit(nid << 1, 0))
             return out
 
     def import_ciphertexts(self, cts):
@@ -297,7 +349,7 @@ class TfheContext(GateBackend):
                 nid = self._add_node(_OP_INPUT, 0, 0, 0, 0, self._new_slot())
                 self._done[nid] = True
                 self._inputs[nid] = np.ascontiguousarray(cts[i])
-                out.append(CipherBit(self, nid << 1, 0))
+                out.append(self._bit(nid << 1, 0))
             return out
 
     def export_ciphertexts(self, handles):
@@ -305,9 +357,12 @@ class TfheContext(GateBackend):
         constants become noiseless trivial samples)."""
         self._check(*handles)
         with self._lock:
+            refs = [h._value for h in handles]
+            for r in refs:
+                if (r >> 1) in self._dormant:
+                    self._revive(r >> 1)
             if self._pending:
                 self.flush()
-            refs = [h._value for h in handles]
             out = np.zeros((len(refs), self.lanes, self.params.n + 1), np.uint32)
             live = [i for i, r in enumerate(refs) if (r >> 1) != 0]
             if live:
@@ -327,7 +382,7 @@ class TfheContext(GateBackend):
         """SimContext.trivial_const (backend.py:183-186): public, free, level 0."""
         if b not in (0, 1):
             raise ValueError(f"plaintext bit must be 0 or 1, got {b!r}")
-        return CipherBit(self, int(b), 0, trivial_value=int(b))
+        return self._bit(int(b), 0, int(b))
 
     # -- gates -------------------------------------------------------------------
 
@@ -341,10 +396,14 @@ class TfheContext(GateBackend):
             return ra
         if ra == rb ^ 1:
             return 0
+        if ra & rb & 1:  # OR(u, v): a full adder's carry folds into one majority
+            m = self._try_maj(ra ^ 1, rb ^ 1)
+            if m is not None:
+                return m ^ 1
         if ra > rb:
             ra, rb = rb, ra
         key = (_OP_AND, ra, rb)
-        nid = self._cse.get(key)
+        nid = self._cse_get(key)
         if nid is None:
             lvl = 1 + max(self._lvl[ra >> 1], self._lvl[rb >> 1])
             nid = self._add_node(_OP_AND, ra, rb, 0, lvl, self._new_slot())
@@ -361,16 +420,76 @@ class TfheContext(GateBackend):
             return ra ^ (rb & 1)
         if na == nb:
             return neg
+        # XOR(XOR(p, q), r) = XOR3(p, q, r): one bootstrap at a lower level
+        # (the deeper XOR operand is absorbed)
+        for x, y in sorted(((na, nb), (nb, na)), key=lambda t: -self._lvl[t[0]]):
+            if self._op[x] == _OP_XOR:
+                p, q = self._a[x] >> 1, self._b[x] >> 1
+                if y == p:
+                    return (q << 1) | neg
+                if y == q:
+                    return (p << 1) | neg
+                return self._mk_xor3(p, q, y) | neg
         if na > nb:
             na, nb = nb, na
         key = (_OP_XOR, na, nb)
-        nid = self._cse.get(key)
+        nid = self._cse_get(key)
         if nid is None:
             lvl = 1 + max(self._lvl[na], self._lvl[nb])
             nid = self._add_node(_OP_XOR, na << 1, nb << 1, 0, lvl, self._new_slot())
             self._cse[key] = nid
             self._pending.append(nid)
         return (nid << 1) | neg
+
+    def _try_maj(self, u, v):
+        """ref of OR(u, v) as MAJ(x, y, z) when {u, v} = {AND(x, y), AND(XOR(x, y), z)}
+        (reference circuits.py:101-108 builds a full adder's carry this way)."""
+        op, A, B = self._op, self._a, self._b
+        for g, h in ((u, v), (v, u)):
+            if (g | h) & 1:
+                continue
+            G, H = g >> 1, h >> 1
+            if op[G] != _OP_AND or op[H] != _OP_AND:
+                continue
+            x, y = A[G], B[G]
+            pair = {x >> 1, y >> 1}
+            for w, z in ((A[H], B[H]), (B[H], A[H])):
+                W = w >> 1
+                if op[W] == _OP_XOR and {A[W] >> 1, B[W] >> 1} == pair and (w & 1) == ((x ^ y) & 1):
+                    return self._mk_maj(x, y, z)
+        return None
+
+    def _mk_maj(self, x, y, z):
+        """ref of MAJ(x, y, z) (refs with NOT flags) with constant/duplicate elision."""
+        for p, q, r in ((x, y, z), (x, z, y), (y, z, x)):
+            if p == q:
+                return p
+            if p == q ^ 1:
+                return r
+        for p, q, r in ((x, y, z), (y, x, z), (z, x, y)):
+            if (p >> 1) == 0:  # MAJ(0, q, r) = AND(q, r); MAJ(1, q, r) = OR(q, r)
+                return (self._mk_and(q ^ 1, r ^ 1) ^ 1) if p & 1 else self._mk_and(q, r)
+        x, y, z = sorted((x, y, z))
+        key = (_OP_MAJ, x, y, z)
+        nid = self._cse_get(key)
+        if nid is None:
+            lvl = 1 + max(self._lvl[x >> 1], self._lvl[y >> 1], self._lvl[z >> 1])
+            nid = self._add_node(_OP_MAJ, x, y, z, lvl, self._new_slot())
+            self._cse[key] = nid
+            self._pending.append(nid)
+        return nid << 1
+
+    def _mk_xor3(self, p, q, r):
+        """ref of XOR3 of three distinct non-constant nodes."""
+        p, q, r = sorted((p, q, r))
+        key = (_OP_XOR3, p, q, r)
+        nid = self._cse_get(key)
+        if nid is None:
+            lvl = 1 + max(self._lvl[p], self._lvl[q], self._lvl[r])
+            nid = self._add_node(_OP_XOR3, p << 1, q << 1, r << 1, lvl, self._new_slot())
+            self._cse[key] = nid
+            self._pending.append(nid)
+        return nid << 1
 
     def _mk_mux(self, rs, ra, rb):
         if rs & 1:  # MUX(~s, a, b) = MUX(s, b, a)
@@ -396,7 +515,7 @@ class TfheContext(GateBackend):
         if rb == rs ^ 1:  # s ? a : ~s = ~s OR a
             return self._mk_and(rs, ra ^ 1) ^ 1
         key = (_OP_MUX, rs, ra, rb)
-        nid = self._cse.get(key)
+        nid = self._cse_get(key)
         if nid is None:
             lvl = 1 + max(self._lvl[rs >> 1], self._lvl[ra >> 1], self._lvl[rb >> 1])
             nid = self._add_node(_OP_MUX, rs, ra, rb, lvl, self._new_slot())
@@ -419,7 +538,7 @@ class TfheContext(GateBackend):
                 r = self._mk_xor(ra, rb)
             else:  # XNOR
                 r = self._mk_xor(ra, rb) ^ 1
-        return CipherBit(self, r, level)
+            return self._bit(r, level)
 
     def g_and(self, a, b):
         return self._binary_gate(AND, a, b)
@@ -439,7 +558,8 @@ class TfheContext(GateBackend):
         if not api.not_is_free():
             return self.g_xnor(a, self.trivial_const(0))
         trivial = None if a.trivial_value is None else 1 - a.trivial_value
-        return CipherBit(self, a._value ^ 1, a.level, trivial_value=trivial)
+        with self._lock:
+            return self._bit(a._value ^ 1, a.level, trivial)
 
     def g_mux(self, s, a, b):
         """SimContext.g_mux (backend.py:230-237)."""
@@ -450,7 +570,7 @@ class TfheContext(GateBackend):
         with self._lock:
             self._record(MUX, level)
             r = self._mk_mux(s._value, a._value, b._value)
-        return CipherBit(self, r, level)
+            return self._bit(r, level)
 
     # -- scoped stats (backend.py:241-257) --------------------------------------
 
@@ -480,7 +600,25 @@ class TfheContext(GateBackend):
     def schedule(self):
         """(level, records) batches the next flush would launch."""
         with self._lock:
-            return self._build_schedule(self._pending)
+            return self._build_schedule(self._live(self._pending))
+
+    def _live(self, pending):
+        """Pending nodes reachable from live handles (through pending operands)."""
+        pend = set(pending)
+        hcnt, op, A, B, C = self._hcnt, self._op, self._a, self._b, self._c
+        stack = [n for n in pending if hcnt[n] > 0]
+        need = set()
+        while stack:
+            n = stack.pop()
+            if n in need:
+                continue
+            need.add(n)
+            if op[n] != _OP_INPUT:
+                for r in (A[n], B[n], C[n]):
+                    m = r >> 1
+                    if m in pend and m not in need:
+                        stack.append(m)
+        return [n for n in pending if n in need]
 
     def _build_schedule(self, pending):
         if not pending:
@@ -509,19 +647,26 @@ class TfheContext(GateBackend):
         is_and = op == _OP_AND
         is_xor = op == _OP_XOR
         is_mux = op == _OP_MUX
+        is_maj = op == _OP_MAJ
+        is_x3 = op == _OP_XOR3
+        three = is_mux | is_maj | is_x3
         recs = np.zeros(op.size, dtype=GATE_DTYPE)
         recs["dst"] = self._map_slots(dst)
         recs["src_a"] = self._map_slots(s_a)
         recs["src_b"] = self._map_slots(s_b)
         # MUX records: src_a = selector, src_b = a, src_c = b (refs a/b/c of the node)
-        recs["src_c"] = np.where(is_mux, self._map_slots(np.where(s_c >= 0, s_c, 0)), 0)
+        recs["src_c"] = np.where(three, self._map_slots(np.where(s_c >= 0, s_c, 0)), 0)
         sa = 1 - 2 * (a & 1)
         sb = 1 - 2 * (b & 1)
-        recs["kind"] = np.where(is_mux, GATE_MUX, GATE_LIN2)
+        sc = 1 - 2 * (c & 1)
+        recs["kind"] = np.where(is_mux, GATE_MUX, np.where(is_maj | is_x3, GATE_LIN3, GATE_LIN2))
         recs["c0"] = np.where(is_and, _C_AND, np.where(is_xor, _C_XOR, 0)).astype(np.uint32)
-        # AND: signs of the refs; XOR: 2, 2; MUX: selector positive, alpha/beta = signs of a / b
-        recs["alpha"] = np.where(is_and, sa, np.where(is_xor, 2, sb))
-        recs["beta"] = np.where(is_and, sb, np.where(is_xor, 2, 1 - 2 * (c & 1)))
+        # AND: signs of the refs; XOR: 2, 2; MUX: selector positive, alpha/beta = signs of a / b;
+        # MAJ: signs of the three refs (c0 0); XOR3: -2, -2, -2 (c0 0: the doubled sum is
+        # +-1/4 with the sign carrying the parity)
+        recs["alpha"] = np.where(is_and | is_maj, sa, np.where(is_xor, 2, np.where(is_x3, -2, sb)))
+        recs["beta"] = np.where(is_and | is_maj, sb, np.where(is_xor, 2, np.where(is_x3, -2, sc)))
+        recs["gamma"] = np.where(is_maj, sc, np.where(is_x3, -2, 0))
         order = np.argsort(lvl, kind="stable")
         lvl_sorted = lvl[order]
         bounds = np.flatnonzero(np.diff(lvl_sorted)) + 1
@@ -541,8 +686,10 @@ class TfheContext(GateBackend):
                 for nid, ps in zip(nids, phys):
                     eng.upload(int(ps) * self.lanes, self._inputs[nid].reshape(self.lanes, -1))
                 self._inputs.clear()
-            pending = self._pending
+            pending = self._live(self._pending)
+            self._dormant.update(set(self._pending).difference(pending))
             if not pending:
+                self._pending = []
                 return
             batches = self._build_schedule(pending)
             try:
@@ -633,6 +780,9 @@ class TfheContext(GateBackend):
                 if (r >> 1) == 0:
                     res[i] = r & 1
             if live:
+                for i in live:
+                    if (refs[i] >> 1) in self._dormant:
+                        self._revive(refs[i] >> 1)
                 if any(not self._done[refs[i] >> 1] for i in live) or self._pending:
                     self.flush()
                 cts = self._ciphertexts([refs[i] for i in live])
@@ -654,6 +804,8 @@ class TfheContext(GateBackend):
         with self._lock:
             if (c._value >> 1) == 0:
                 return None
+            if (c._value >> 1) in self._dormant:
+                self._revive(c._value >> 1)
             if self._pending:
                 self.flush()
             cts = self._ciphertexts([c._value])[0]

@@ -520,11 +520,14 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
         const BrItem it = args.items[e / lanes];
         const uint32_t lane_id = e % lanes;
         const int alpha = (int8_t)(it.coef & 0xFF), beta = (int8_t)((it.coef >> 8) & 0xFF);
+        const int gamma = (int8_t)((it.coef >> 16) & 0xFF);
         const uint32_t *A = args.pool + ((size_t)it.src_a * lanes + lane_id) * args.pool_stride;
         const uint32_t *B = args.pool + ((size_t)it.src_b * lanes + lane_id) * args.pool_stride;
+        const uint32_t *C = args.pool + ((size_t)it.src_c * lanes + lane_id) * args.pool_stride;
         for (int c = t; c <= n; c += 64) {
             uint32_t v = (uint32_t)alpha * __ldg(&A[c]);
             if (beta) v += (uint32_t)beta * __ldg(&B[c]);
+            if (gamma) v += (uint32_t)gamma * __ldg(&C[c]);
             if (c == n) v += it.c0;
             bar[c] = (uint16_t)(((v + (1u << 20)) >> 21) & (2 * kN - 1));
         }
@@ -747,11 +750,14 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_lat(const BrArgs args) 
         const BrItem it = args.items[e / lanes];
         const uint32_t lane_id = e % lanes;
         const int alpha = (int8_t)(it.coef & 0xFF), beta = (int8_t)((it.coef >> 8) & 0xFF);
+        const int gamma = (int8_t)((it.coef >> 16) & 0xFF);
         const uint32_t *A = args.pool + ((size_t)it.src_a * lanes + lane_id) * args.pool_stride;
         const uint32_t *B = args.pool + ((size_t)it.src_b * lanes + lane_id) * args.pool_stride;
+        const uint32_t *C = args.pool + ((size_t)it.src_c * lanes + lane_id) * args.pool_stride;
         for (int c = threadIdx.x; c <= n; c += 192) {
             uint32_t v = (uint32_t)alpha * __ldg(&A[c]);
             if (beta) v += (uint32_t)beta * __ldg(&B[c]);
+            if (gamma) v += (uint32_t)gamma * __ldg(&C[c]);
             if (c == n) v += it.c0;
             sm.bar[c] = (uint16_t)(((v + (1u << 20)) >> 21) & (2 * kN - 1));
         }
@@ -937,11 +943,14 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate_u2(const BrArgs args
         const BrItem it = args.items[e / lanes];
         const uint32_t lane_id = e % lanes;
         const int alpha = (int8_t)(it.coef & 0xFF), beta = (int8_t)((it.coef >> 8) & 0xFF);
+        const int gamma = (int8_t)((it.coef >> 16) & 0xFF);
         const uint32_t *A = args.pool + ((size_t)it.src_a * lanes + lane_id) * args.pool_stride;
         const uint32_t *B = args.pool + ((size_t)it.src_b * lanes + lane_id) * args.pool_stride;
+        const uint32_t *C = args.pool + ((size_t)it.src_c * lanes + lane_id) * args.pool_stride;
         for (int c = t; c <= n; c += 64) {
             uint32_t v = (uint32_t)alpha * __ldg(&A[c]);
             if (beta) v += (uint32_t)beta * __ldg(&B[c]);
+            if (gamma) v += (uint32_t)gamma * __ldg(&C[c]);
             if (c == n) v += it.c0;
             bar[c] = (uint16_t)(((v + (1u << 20)) >> 21) & (2 * kN - 1));
         }
@@ -1146,11 +1155,14 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_u2_lat(const BrArgs arg
         const BrItem it = args.items[e / lanes];
         const uint32_t lane_id = e % lanes;
         const int alpha = (int8_t)(it.coef & 0xFF), beta = (int8_t)((it.coef >> 8) & 0xFF);
+        const int gamma = (int8_t)((it.coef >> 16) & 0xFF);
         const uint32_t *A = args.pool + ((size_t)it.src_a * lanes + lane_id) * args.pool_stride;
         const uint32_t *B = args.pool + ((size_t)it.src_b * lanes + lane_id) * args.pool_stride;
+        const uint32_t *C = args.pool + ((size_t)it.src_c * lanes + lane_id) * args.pool_stride;
         for (int c = threadIdx.x; c <= n; c += 192) {
             uint32_t v = (uint32_t)alpha * __ldg(&A[c]);
             if (beta) v += (uint32_t)beta * __ldg(&B[c]);
+            if (gamma) v += (uint32_t)gamma * __ldg(&C[c]);
             if (c == n) v += it.c0;
             sm.bar[c] = (uint16_t)(((v + (1u << 20)) >> 21) & (2 * kN - 1));
         }
@@ -1605,7 +1617,10 @@ BrArgs br_args(hb_engine *e) {
     return a;
 }
 
-int32_t pack_coef(int alpha, int beta) { return (int32_t)((uint32_t)(uint8_t)(int8_t)alpha | ((uint32_t)(uint8_t)(int8_t)beta << 8)); }
+int32_t pack_coef(int alpha, int beta, int gamma = 0) {
+    return (int32_t)((uint32_t)(uint8_t)(int8_t)alpha | ((uint32_t)(uint8_t)(int8_t)beta << 8) |
+                     ((uint32_t)(uint8_t)(int8_t)gamma << 16));
+}
 
 }  // namespace
 
@@ -1853,7 +1868,7 @@ static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_
     size_t nbr = 0;
     for (size_t i = 0; i < n; i++) {
         const hb_gate &g = gates[i];
-        if (g.kind != HB_GATE_LIN2 && g.kind != HB_GATE_MUX) {
+        if (g.kind != HB_GATE_LIN2 && g.kind != HB_GATE_MUX && g.kind != HB_GATE_LIN3) {
             set_error("hb_run_gates: unknown gate kind " + std::to_string((int)g.kind));
             return HB_EINVAL;
         }
@@ -1877,12 +1892,16 @@ static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_
     for (size_t i = 0; i < n; i++) {
         const hb_gate &g = gates[i];
         if (g.kind == HB_GATE_LIN2) {
-            hbr[b] = BrItem{g.src_a, g.src_b, g.c0, pack_coef(g.alpha, g.beta)};
+            hbr[b] = BrItem{g.src_a, g.src_b, g.src_a, g.c0, pack_coef(g.alpha, g.beta)};
+            hks[i] = KsItem{g.dst, (uint32_t)b, 0xFFFFFFFFu, 0u};
+            b += 1;
+        } else if (g.kind == HB_GATE_LIN3) {
+            hbr[b] = BrItem{g.src_a, g.src_b, g.src_c, g.c0, pack_coef(g.alpha, g.beta, g.gamma)};
             hks[i] = KsItem{g.dst, (uint32_t)b, 0xFFFFFFFFu, 0u};
             b += 1;
         } else {
-            hbr[b] = BrItem{g.src_a, g.src_b, 0u - eighth, pack_coef(1, g.alpha)};
-            hbr[b + 1] = BrItem{g.src_a, g.src_c, 0u - eighth, pack_coef(-1, g.beta)};
+            hbr[b] = BrItem{g.src_a, g.src_b, g.src_a, 0u - eighth, pack_coef(1, g.alpha)};
+            hbr[b + 1] = BrItem{g.src_a, g.src_c, g.src_a, 0u - eighth, pack_coef(-1, g.beta)};
             hks[i] = KsItem{g.dst, (uint32_t)b, (uint32_t)(b + 1), eighth};
             b += 2;
         }
@@ -1994,7 +2013,7 @@ int hb_debug_blind_rotate(hb_engine *e, const uint32_t *lwe, uint32_t mu, int32_
     if ((rc = ensure_dev((void **)&e->d_br, &e->br_cap, 1, sizeof(BrItem), false, e->stream))) return rc;
     if ((rc = ensure_dev((void **)&e->d_big, &e->big_cap, kBigStride, sizeof(uint32_t), false, e->stream))) return rc;
     uint32_t *d_in = e->d_tmp, *d_acc = e->d_tmp + ((2 * words + 3) & ~size_t(3));
-    BrItem it{0, 0, 0, pack_coef(1, 0)};
+    BrItem it{0, 0, 0, 0, pack_coef(1, 0)};
     HB_CUDA_TRY(cudaMemcpyAsync(d_in, lwe, words * 4, cudaMemcpyHostToDevice, e->stream));
     HB_CUDA_TRY(cudaMemcpyAsync(e->d_br, &it, sizeof it, cudaMemcpyHostToDevice, e->stream));
     BrArgs a = br_args(e);
@@ -2028,7 +2047,7 @@ int hb_debug_bootstrap_wo_ks(hb_engine *e, const uint32_t *lin, size_t count, ui
     if ((rc = ensure_dev((void **)&e->d_big, &e->big_cap, count * kBigStride, sizeof(uint32_t), false, e->stream)))
         return rc;
     std::vector<BrItem> items(count);
-    for (size_t i = 0; i < count; i++) items[i] = BrItem{(uint32_t)i, (uint32_t)i, 0u, pack_coef(1, 0)};
+    for (size_t i = 0; i < count; i++) items[i] = BrItem{(uint32_t)i, (uint32_t)i, (uint32_t)i, 0u, pack_coef(1, 0)};
     HB_CUDA_TRY(cudaMemcpyAsync(e->d_tmp, lin, count * words * 4, cudaMemcpyHostToDevice, e->stream));
     HB_CUDA_TRY(cudaMemcpyAsync(e->d_br, items.data(), count * sizeof(BrItem), cudaMemcpyHostToDevice, e->stream));
     HB_CUDA_TRY(cudaMemsetAsync(e->d_margin, 0, sizeof(unsigned long long), e->stream));

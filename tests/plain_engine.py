@@ -11,7 +11,7 @@ product package.
 
 import numpy as np
 
-from paper_1806_03461_b200._native import GATE_MUX
+from paper_1806_03461_b200._native import GATE_LIN3, GATE_MUX
 
 EIGHTH = 1 << 29
 
@@ -53,8 +53,10 @@ class PlainEngine:
                 u2 = _sign_to_phase((-EIGHTH - A + int(r["beta"]) * C) & 0xFFFFFFFF)
                 out = _sign_to_phase((EIGHTH + u1 + u2) & 0xFFFFFFFF)
             else:
-                v = (int(r["c0"]) + int(r["alpha"]) * A + int(r["beta"]) * B) & 0xFFFFFFFF
-                out = _sign_to_phase(v)
+                v = int(r["c0"]) + int(r["alpha"]) * A + int(r["beta"]) * B
+                if r["kind"] == GATE_LIN3:
+                    v = v + int(r["gamma"]) * self.pool[r["src_c"] * lanes + lane]
+                out = _sign_to_phase(v & 0xFFFFFFFF)
             self.pool[r["dst"] * lanes + lane] = out
 
     def sync(self):

@@ -1,0 +1,86 @@
+"""Host DAG: full-adder fusion into 3-input bootstraps (majority, XOR3) and
+the live-handle filter of flush (dormant gates), on the plaintext stand-in
+engine (CPU).  Decrypted values and GateStats must equal SimContext's."""
+
+import itertools
+
+import numpy as np
+
+from hebnn.backend import SimContext
+from hebnn.circuits import encrypt_word, decrypt_word, rc_add, reduce_tree_sum
+from plain_engine import plain_context_class
+
+Ctx = plain_context_class()
+
+
+def _fa(ctx, a, b, c):
+    # reference circuits._full_adder (circuits.py:101-108)
+    axb = ctx.g_xor(a, b)
+    s = ctx.g_xor(axb, c)
+    t = ctx.g_and(axb, c)
+    return s, ctx.g_or(ctx.g_and(a, b), t)
+
+
+def test_full_adder_is_two_bootstraps_and_exact():
+    for bits in itertools.product((0, 1), repeat=3):
+        ctx = Ctx(seed=3)
+        a, b, c = (ctx.encrypt(v) for v in bits)
+        s, cout = _fa(ctx, a, b, c)
+        assert (ctx.decrypt(s), ctx.decrypt(cout)) == (sum(bits) & 1, int(sum(bits) >= 2))
+        assert ctx.exec_stats["bootstraps"] == 2  # XOR3 + MAJ; the 3 intermediates stay dormant
+        assert ctx.gate_count == 5                # counted like SimContext
+        assert ctx.exec_stats["levels"] == 1
+
+
+def test_full_adder_with_negated_inputs():
+    for bits in itertools.product((0, 1), repeat=3):
+        ctx = Ctx(seed=3)
+        a, b, c = (ctx.encrypt(v) for v in bits)
+        na, nc = ctx.g_not(a), ctx.g_not(c)
+        s, cout = _fa(ctx, na, b, nc)
+        x = (1 - bits[0], bits[1], 1 - bits[2])
+        assert (ctx.decrypt(s), ctx.decrypt(cout)) == (sum(x) & 1, int(sum(x) >= 2))
+
+
+def test_live_intermediate_is_still_executed():
+    ctx = Ctx(seed=4)
+    a, b, c = ctx.encrypt(1), ctx.encrypt(0), ctx.encrypt(1)
+    axb = ctx.g_xor(a, b)
+    s = ctx.g_xor(axb, c)
+    t = ctx.g_and(axb, c)
+    cout = ctx.g_or(ctx.g_and(a, b), t)
+    assert ctx.decrypt(cout) == 1 and ctx.decrypt(s) == 0
+    assert ctx.decrypt(t) == 1 and ctx.decrypt(axb) == 1  # were live: executed in the same flush
+
+
+def test_dormant_gate_is_revived_by_cse_and_by_reuse():
+    ctx = Ctx(seed=5)
+    a, b = ctx.encrypt(1), ctx.encrypt(1)
+    ctx.g_and(a, b)                  # handle dropped at once
+    keep = ctx.g_xor(a, b)
+    assert ctx.decrypt(keep) == 0
+    before = ctx.exec_stats["bootstraps"]
+    again = ctx.g_and(a, b)          # CSE hit on the dormant AND
+    assert ctx.decrypt(again) == 1
+    assert ctx.exec_stats["bootstraps"] == before + 1
+    # a dormant operand deep in a new gate
+    x = ctx.g_and(a, ctx.g_not(b))   # dormant after the next flush
+    y = ctx.g_or(x, a)
+    del x
+    assert ctx.decrypt(y) == 1
+
+
+def test_stats_and_values_match_simcontext_on_adder_trees():
+    rng = np.random.default_rng(7)
+    for trial in range(4):
+        n = int(rng.integers(3, 12))
+        vals = rng.integers(0, 2, n).tolist()
+        outs = []
+        for C in (SimContext, lambda: Ctx(seed=9)):
+            ctx = C()
+            bits = [ctx.encrypt(v) for v in vals]
+            w = reduce_tree_sum(bits)
+            x = rc_add(w, encrypt_word(ctx, 5, w.width))
+            outs.append((decrypt_word(w), decrypt_word(x), ctx.global_stats.as_dict()))
+        assert outs[0] == outs[1]
+        assert outs[0][0] == sum(vals)

@@ -100,6 +100,29 @@ def test_mux_bit_exact(kit):
         assert np.array_equal(out[i], octx.mux(cs[i], ca[i], cb[i]))
 
 
+@pytest.mark.parametrize("name", ["MAJ", "XOR3", "MAJ_NEG"])
+def test_three_input_gates_truth_table_and_bit_exact(kit, name):
+    """hb_gate LIN3: majority (a full adder's carry) and 3-input XOR (its sum)
+    in one bootstrap each, bit-exact vs the oracle's or_gate3."""
+    engine, keys, octx = kit
+    bits = np.array([[(i >> k) & 1 for k in range(3)] for i in range(8)], np.uint8).T  # [3][8]
+    cts = [keys.encrypt(bits[k], seed=41, stream=k) for k in range(3)]
+    engine.reserve(32)
+    for k in range(3):
+        engine.upload(8 * k, cts[k])
+    coef = {"MAJ": (1, 1, 1), "XOR3": (-2, -2, -2), "MAJ_NEG": (1, -1, 1)}[name]
+    recs = tfhe.gate_records(8)
+    for i in range(8):
+        recs[i] = (24 + i, i, 8 + i, 16 + i, 0, coef[0], coef[1], 2, coef[2])
+    engine.run_gates(recs)
+    out = engine.download(24, 8)
+    a, b, c = bits.astype(int)
+    want = {"MAJ": (a + b + c) >= 2, "XOR3": (a ^ b ^ c) == 1, "MAJ_NEG": (a + (1 - b) + c) >= 2}[name]
+    assert np.array_equal(keys.decrypt(out), want.astype(np.uint8))
+    for i in (0, 3, 5, 7):
+        assert np.array_equal(out[i], octx.gate3(0, coef[0], cts[0][i], coef[1], cts[1][i], coef[2], cts[2][i]))
+
+
 def test_gpu_matches_committed_golden_vectors(kit):
     """The sm_100a engine reproduces tests/golden/tfhe_golden_seed42.npz (CGGI)
     and tfhe_golden_pairs_seed42.npz (key pairs) — oracle-generated: keys from

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_params():
     L = _native.lib()
-    assert L.hb_abi_version() == 2
+    assert L.hb_abi_version() == 3
     p = _native.default_params()
     assert (p.n, p.N, p.k, p.bg_bits, p.l, p.ks_base_bits, p.ks_t) == (630, 1024, 1, 7, 3, 2, 8)
     assert L.hb_lwe_words(ctypes.byref(p)) == 631
@@ -68,7 +68,7 @@ def test_invalid_arguments_are_value_errors(keys):
 
 def test_gate_record_layout_matches_header():
     assert _native.GATE_DTYPE.itemsize == 24
-    assert list(_native.GATE_DTYPE.names) == ["dst", "src_a", "src_b", "src_c", "c0", "alpha", "beta", "kind", "_pad"]
+    assert list(_native.GATE_DTYPE.names) == ["dst", "src_a", "src_b", "src_c", "c0", "alpha", "beta", "kind", "gamma"]
 
 
 def test_decrypt_host_side(keys):

@@ -12,6 +12,7 @@
 //   k_keyswitch       K4  batched LWE key switch (uint32), KSK rows shared by a
 //                     tile of gates
 //   k_gather          pool slots -> contiguous buffer for download
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 
@@ -1181,6 +1182,13 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_u2_lat(const BrArgs arg
     int st = 0;  // this group's next stage
     for (int pm = 0; pm < pairs; pm++) {
         const int ai = sm.bar[2 * pm], aj = sm.bar[2 * pm + 1];
+        int ex[3];
+        double2 base[3];  // issued before the FFT: the table loads' L2 latency overlaps it
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            ex[c] = c == 0 ? ((ai + aj) & (2 * kN - 1)) : (c == 1 ? ai : aj);
+            base[c] = __ldg(&args.PSI[(ex[c] * (4 * t + 1)) & (2 * kN - 1)]);
+        }
         double2 x[2][8];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
@@ -1198,14 +1206,13 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_u2_lat(const BrArgs arg
         double2 f0[8], f1[8];
 #pragma unroll
         for (int c = 0; c < 3; c++) {
-            const int ec = c == 0 ? ((ai + aj) & (2 * kN - 1)) : (c == 1 ? ai : aj);
+            const int ec = ex[c];
             double2 F[8];
             {
-                const double2 base = __ldg(&args.PSI[(ec * (4 * t + 1)) & (2 * kN - 1)]);
                 const long long flip = (long long)(ec & 1) << 63;
                 double2 p[4];
 #pragma unroll
-                for (int m = 0; m < 4; m++) p[m] = m == 0 ? base : cmul(base, c_w8[(ec * m) & 7]);
+                for (int m = 0; m < 4; m++) p[m] = m == 0 ? base[c] : cmul(base[c], c_w8[(ec * m) & 7]);
 #pragma unroll
                 for (int m = 0; m < 4; m++) {
                     F[m] = make_double2(p[m].x - 1.0, p[m].y);
@@ -1286,6 +1293,214 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_u2_lat(const BrArgs arg
         else if (c < kN) v = 0u - accA[kN - c];
         else v = accB[0];
         out[c] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Latency mode for very narrow levels (<= #SM/2 bootstraps), key pairs: one
+// bootstrap per 2-CTA cluster.  CTA q owns TRLWE polynomial q (ACC_q and its
+// three digit rows 3q..3q+2); group g of CTA q transforms digit row 3q+g
+// (single FFT) and runs its 3 (component) MAC stages from a 3-slot ring
+// (slot c = component c, refilled with the next pair's stage as soon as it is
+// consumed).  Partials meet over distributed shared memory: group 0 of CTA q
+// sums output polynomial q over the six groups (3 local, 3 in the peer CTA),
+// inverse-transforms it and updates ACC_q.  Two cluster barriers per pair.
+// ---------------------------------------------------------------------------
+// cluster barriers: the full (release/acquire) form publishes shared-memory
+// writes to the peer CTA; the relaxed arrive only orders execution (used once
+// the peer's DSMEM loads have been consumed) and its wait is deferred.
+__device__ __forceinline__ void cluster_sync_acq_rel() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
+struct BrCluSmemU2 {
+    double2 bk[3][3][2 * kNH];               // [group][component slot][output poly][bin]
+    uint64_t full[3][3];
+    uint32_t acc[kN];                        // ACC_q
+    double2 xch[3][2][kXchStride];           // per group: FFT exchange, then partials [o][512]
+    double2 inv[kXchStride];                 // group 0's inverse-FFT exchange
+    uint16_t bar[kMaxLweN + 1];
+    TwSeeds tws[64];
+};
+
+template <bool kDebug>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) k_blind_rotate_u2_clu(const BrArgs args) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    BrCluSmemU2 &sm = *reinterpret_cast<BrCluSmemU2 *>(smem_raw);
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int q = (int)cluster.block_rank();   // TRLWE polynomial owned by this CTA
+    BrCluSmemU2 &peer = *cluster.map_shared_rank(&sm, q ^ 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = warp >> 1;
+    const int t = threadIdx.x & 63;
+    const int bar_id = 1 + grp;
+    const int n = args.n;
+    const int pairs = min(n, args.iters) / 2;
+    const char *bk_src = reinterpret_cast<const char *>(args.bkf);
+    const uint32_t e = blockIdx.x >> 1;
+    const int row = 3 * q + grp, p = grp;         // digit row of this group: poly q, digit p
+    const int rp = row >> 1, h = row & 1;
+    auto stage_src = [&](int pm, int c) {
+        return bk_src + (size_t)(pm * kStagesPerPair + rp * 6 + c * 2 + h) * kRowBytes;
+    };
+    double2 *xch = &sm.xch[grp][0][0];
+
+    if (threadIdx.x < 64) {
+        TwSeeds ts;
+        ts.f_a0 = args.TW[t];
+        ts.step_a = args.W[t];
+        ts.step_b = args.W[8 * (t & 7)];
+        ts.i_b0 = args.TW[t >> 3];
+        ts.i_stepb = args.TW[32 * (t & 7) + 8];
+        sm.tws[t] = ts;
+    }
+    if (t == 0) {
+        for (int c = 0; c < 3; c++) mbar_init(&sm.full[grp][c], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (pairs > 0) {
+            for (int c = 0; c < 3; c++) {
+                mbar_arrive_expect_tx(&sm.full[grp][c], kRowBytes);
+                bulk_g2s(sm.bk[grp][c], stage_src(0, c), kRowBytes, &sm.full[grp][c]);
+            }
+        }
+    }
+    {   // K1: linear combination + modulus switch (both CTAs)
+        const uint32_t lanes = args.lanes;
+        const BrItem it = args.items[e / lanes];
+        const uint32_t lane_id = e % lanes;
+        const int alpha = (int8_t)(it.coef & 0xFF), beta = (int8_t)((it.coef >> 8) & 0xFF);
+        const int gamma = (int8_t)((it.coef >> 16) & 0xFF);
+        const uint32_t *A = args.pool + ((size_t)it.src_a * lanes + lane_id) * args.pool_stride;
+        const uint32_t *B = args.pool + ((size_t)it.src_b * lanes + lane_id) * args.pool_stride;
+        const uint32_t *C = args.pool + ((size_t)it.src_c * lanes + lane_id) * args.pool_stride;
+        for (int c = threadIdx.x; c <= n; c += 192) {
+            uint32_t v = (uint32_t)alpha * __ldg(&A[c]);
+            if (beta) v += (uint32_t)beta * __ldg(&B[c]);
+            if (gamma) v += (uint32_t)gamma * __ldg(&C[c]);
+            if (c == n) v += it.c0;
+            sm.bar[c] = (uint16_t)(((v + (1u << 20)) >> 21) & (2 * kN - 1));
+        }
+    }
+    __syncthreads();
+    {
+        const int barb = sm.bar[n];
+        for (int i = threadIdx.x; i < kN; i += 192)
+            sm.acc[i] = q == 0 ? 0u : (((i + barb) & kN) ? 0u - args.mu : args.mu);
+    }
+    cluster.sync();  // peer smem live (DSMEM), ACC initialised
+
+    double max_err = 0.0;
+    for (int pm = 0; pm < pairs; pm++) {
+        const int ai = sm.bar[2 * pm], aj = sm.bar[2 * pm + 1];
+        int ex[3];
+        double2 base[3];  // issued before the FFT: the table loads' L2 latency overlaps it
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            ex[c] = c == 0 ? ((ai + aj) & (2 * kN - 1)) : (c == 1 ? ai : aj);
+            base[c] = __ldg(&args.PSI[(ex[c] * (4 * t + 1)) & (2 * kN - 1)]);
+        }
+        double2 x[1][8];
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+            const int j = t + 64 * m;
+            x[0][m] = make_double2(small_int_to_double(gadget_digit(sm.acc[j], p)),
+                                   small_int_to_double(gadget_digit(sm.acc[j + kNH], p)));
+        }
+        if (pm > 0) cluster_wait();  // the peer has read our previous partials (relaxed arrive below)
+        nega_fft_fwd_n<1, true>(x, xch, t, sm.tws[t], bar_id);
+        double2 f0[8], f1[8];
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            const int ec = ex[c];
+            double2 F[8];
+            {
+                const long long flip = (long long)(ec & 1) << 63;
+                double2 pw[4];
+#pragma unroll
+                for (int m = 0; m < 4; m++) pw[m] = m == 0 ? base[c] : cmul(base[c], c_w8[(ec * m) & 7]);
+#pragma unroll
+                for (int m = 0; m < 4; m++) {
+                    F[m] = make_double2(pw[m].x - 1.0, pw[m].y);
+                    F[m + 4] = make_double2(__longlong_as_double(__double_as_longlong(pw[m].x) ^ flip) - 1.0,
+                                            __longlong_as_double(__double_as_longlong(pw[m].y) ^ flip));
+                }
+            }
+            mbar_wait(&sm.full[grp][c], pm & 1);
+            const double2 *bk0 = sm.bk[grp][c];
+            const double2 *bk1 = sm.bk[grp][c] + kNH;
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                const double2 y = cmul(x[0][m], F[m]);
+                if (c == 0) {
+                    f0[m] = cmul(y, bk0[t + 64 * m]);
+                    f1[m] = cmul(y, bk1[t + 64 * m]);
+                } else {
+                    cmac(f0[m], y, bk0[t + 64 * m]);
+                    cmac(f1[m], y, bk1[t + 64 * m]);
+                }
+            }
+            group_bar(bar_id);  // both warps done with the slot
+            if (t == 0 && pm + 1 < pairs) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive_expect_tx(&sm.full[grp][c], kRowBytes);
+                bulk_g2s(sm.bk[grp][c], stage_src(pm + 1, c), kRowBytes, &sm.full[grp][c]);
+            }
+        }
+        // partials [o][512] into this group's exchange buffer (its FFT readers are done:
+        // the group barrier of the last stage above)
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+            xch[t + 64 * m] = f0[m];
+            xch[kNH + t + 64 * m] = f1[m];
+        }
+        cluster_sync_acq_rel();  // all six groups' partials visible cluster-wide
+        if (grp != 0) cluster_arrive_relaxed();
+        if (grp == 0) {
+            double2 y[1][8];
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                const int k = q * kNH + t + 64 * m;  // partial of output q in each group's [o][512]
+                const double2 *l0 = &sm.xch[0][0][0], *l1 = &sm.xch[1][0][0], *l2 = &sm.xch[2][0][0];
+                const double2 *r0 = &peer.xch[0][0][0], *r1 = &peer.xch[1][0][0], *r2 = &peer.xch[2][0][0];
+                double2 v = cadd(cadd(l0[k], l1[k]), l2[k]);
+                v = cadd(v, cadd(cadd(r0[k], r1[k]), r2[k]));
+                y[0][m] = v;
+            }
+            cluster_arrive_relaxed();  // partial reads consumed (values are in registers)
+            nega_fft_inv_n<1, true>(y, sm.inv, t, sm.tws[t], bar_id);
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                const double lo = y[0][m].x, hi = y[0][m].y;
+                if (kDebug) {
+                    max_err = fmax(max_err, fabs(lo - rint(lo)));
+                    max_err = fmax(max_err, fabs(hi - rint(hi)));
+                }
+                const int j = t + 64 * m;
+                sm.acc[j] += round_to_torus(lo);
+                sm.acc[j + kNH] += round_to_torus(hi);
+            }
+        }
+        __syncthreads();  // ACC_q updated
+    }
+    if (pairs > 0) cluster_wait();  // the peer is done reading our shared memory
+
+    if (kDebug && args.margin) atomicMax(args.margin, (unsigned long long)__double_as_longlong(max_err));
+    if (kDebug && args.acc_dump) {
+        uint32_t *dst = args.acc_dump + (size_t)e * 2 * kN + (size_t)q * kN;
+        for (int c = threadIdx.x; c < kN; c += 192) dst[c] = sm.acc[c];
+    }
+    uint32_t *out = args.big + (size_t)e * kBigStride;
+    if (q == 0) {
+        for (int c = threadIdx.x; c < kN; c += 192) out[c] = c == 0 ? sm.acc[0] : 0u - sm.acc[kN - c];
+    } else if (threadIdx.x == 0) {
+        out[kN] = sm.acc[0];
     }
 }
 
@@ -1506,6 +1721,7 @@ struct hb_engine {
     int num_sms = 148;
     size_t max_work = kMaxWorkPerLaunch;  // HEBNN_B200_MAX_WORK overrides (tests)
     bool latency_mode = true;             // HEBNN_B200_LATENCY_MODE=0 disables (A/B tests)
+    bool cluster_mode = true;             // 2-CTA clusters for <= #SM/2 key-pair bootstraps (HEBNN_B200_CLUSTER_MODE=0)
 };
 
 namespace {
@@ -1585,6 +1801,12 @@ int launch_br_auto(hb_engine *e, const BrArgs &a, int force_g = 0) {
     const uint32_t sms = (uint32_t)e->num_sms;
     const int gsel = force_g ? force_g : (a.n_work <= sms ? 1 : (a.n_work <= 2u * sms ? 2 : kBrGates));
     if (e->unroll == 2) {
+        if (!force_g && e->latency_mode && e->cluster_mode && 2 * a.n_work <= sms) {
+            k_blind_rotate_u2_clu<kDebug><<<2 * a.n_work, 192, sizeof(BrCluSmemU2), e->stream>>>(a);
+            HB_CUDA_TRY(cudaGetLastError());
+            e->n_launch++;
+            return HB_OK;
+        }
         if (!force_g && gsel == 1 && e->latency_mode) {
             k_blind_rotate_u2_lat<kDebug><<<a.n_work, 192, sizeof(BrLatSmemU2), e->stream>>>(a);
             HB_CUDA_TRY(cudaGetLastError());
@@ -1708,6 +1930,10 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
                                      (int)br_smem_bytes<2>()));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)br_smem_bytes<1>()));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_clu<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrCluSmemU2)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_clu<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrCluSmemU2)));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_lat<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(BrLatSmemU2)));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_lat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1720,6 +1946,7 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
     e->num_sms = prop.multiProcessorCount;
     if (const char *mw = std::getenv("HEBNN_B200_MAX_WORK")) e->max_work = std::max<size_t>(2, std::strtoull(mw, nullptr, 10));
     if (const char *lm = std::getenv("HEBNN_B200_LATENCY_MODE")) e->latency_mode = std::atoi(lm) != 0;
+    if (const char *cm = std::getenv("HEBNN_B200_CLUSTER_MODE")) e->cluster_mode = std::atoi(cm) != 0;
 
     // BK -> Fourier
     const size_t npoly = bk_tgsw_count(p) * kRows * 2;

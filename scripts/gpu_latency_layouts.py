@@ -11,7 +11,7 @@ p = tfhe.default_params(); p.bk_unroll = unroll
 keys = tfhe.KeySet(seed=3, params=p)
 eng = tfhe.Engine(keys)
 res = {}
-for n in (1, 16, 148, 296, 592):
+for n in (1, 16, 74, 148, 296, 592):
     rng = np.random.default_rng(n)
     a = rng.integers(0, 2, n).astype(np.uint8); b = rng.integers(0, 2, n).astype(np.uint8)
     eng.reserve(3 * n)
@@ -29,8 +29,8 @@ for n in (1, 16, 148, 296, 592):
 print(json.dumps(res))
 '''
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-for unroll in (2, 1):
-    for lat in ("1", "0"):
-        env = dict(os.environ, HEBNN_B200_LATENCY_MODE=lat)
-        r = subprocess.run([sys.executable, "-c", CODE, str(unroll)], cwd=root, env=env, capture_output=True, text=True)
-        print(f"bk_unroll={unroll} latency_mode={lat} ms(BR+KS) per level width:", r.stdout.strip() or r.stderr[-800:], flush=True)
+for unroll, lat, clu in ((2, "1", "1"), (2, "1", "0"), (2, "0", "0"), (1, "1", "0"), (1, "0", "0")):
+    env = dict(os.environ, HEBNN_B200_LATENCY_MODE=lat, HEBNN_B200_CLUSTER_MODE=clu)
+    r = subprocess.run([sys.executable, "-c", CODE, str(unroll)], cwd=root, env=env, capture_output=True, text=True)
+    print(f"bk_unroll={unroll} latency_mode={lat} cluster_mode={clu} ms(BR+KS) per level width:",
+          r.stdout.strip() or r.stderr[-800:], flush=True)

@@ -195,3 +195,45 @@ np.save(sys.argv[1], eng.download(2 * n, n))
         subprocess.run([sys.executable, "-c", code, path], check=True, cwd=root, env=env)
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("n", [5, 100, 200])
+def test_narrow_level_kernels_agree(n):
+    """Levels of <= #SM/2, <= #SM and <= 2 #SM bootstraps run on the 2-CTA
+    cluster kernel, the latency kernel or 1-2 bootstraps per CTA; every choice
+    must give the same ciphertexts (both key layouts)."""
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import os, sys, numpy as np
+sys.path.insert(0, os.getcwd())
+from paper_1806_03461_b200 import tfhe
+n, unroll = int(sys.argv[2]), int(sys.argv[3])
+p = tfhe.default_params(); p.bk_unroll = unroll
+keys = tfhe.KeySet(seed=42, params=p)
+eng = tfhe.Engine(keys)
+rng = np.random.default_rng(n)
+eng.reserve(4 * n)
+eng.upload(0, keys.encrypt(rng.integers(0, 2, 3 * n).astype(np.uint8), seed=6, stream=1))
+recs = tfhe.gate_records(n)
+recs["dst"], recs["src_a"], recs["src_b"], recs["src_c"] = np.arange(3 * n, 4 * n), np.arange(n), np.arange(n, 2 * n), np.arange(2 * n, 3 * n)
+recs["kind"] = np.where(np.arange(n) % 2 == 0, 2, 0)   # MAJ and XOR
+recs["alpha"], recs["beta"], recs["gamma"] = 1, 1, 1
+recs["c0"] = np.where(recs["kind"] == 2, 0, tfhe.GATE_LIN["XOR"][0])
+recs["alpha"][recs["kind"] == 0] = 2
+recs["beta"][recs["kind"] == 0] = 2
+recs["gamma"][recs["kind"] == 0] = 0
+eng.run_gates(recs)
+np.save(sys.argv[1], eng.download(3 * n, n))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for unroll in (2, 1):
+        outs = []
+        for lat, clu in (("1", "1"), ("1", "0"), ("0", "0")):
+            path = f"/tmp/hb_narrow_{n}_{unroll}_{lat}{clu}.npy"
+            env = dict(os.environ, HEBNN_B200_LATENCY_MODE=lat, HEBNN_B200_CLUSTER_MODE=clu)
+            subprocess.run([sys.executable, "-c", code, path, str(n), str(unroll)], check=True, cwd=root, env=env)
+            outs.append(np.load(path))
+        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])

@@ -604,6 +604,9 @@ class TfheContext(GateBackend):
 
     def _live(self, pending):
         """Pending nodes reachable from live handles (through pending operands)."""
+        return self._live_levels(pending) if len(pending) > 2048 else self._live_walk(pending)
+
+    def _live_walk(self, pending):
         pend = set(pending)
         hcnt, op, A, B, C = self._hcnt, self._op, self._a, self._b, self._c
         stack = [n for n in pending if hcnt[n] > 0]
@@ -619,6 +622,26 @@ class TfheContext(GateBackend):
                     if m in pend and m not in need:
                         stack.append(m)
         return [n for n in pending if n in need]
+
+    def _live_levels(self, pending):
+        """_live for large flushes: one numpy sweep per level, deepest first
+        (operands sit at strictly lower levels than their consumers)."""
+        ids = np.asarray(pending, dtype=np.int64)
+        lvl = np.asarray(self._lvl, dtype=np.int64)[ids]
+        pos = np.full(len(self._op), -1, dtype=np.int64)
+        pos[ids] = np.arange(ids.size)
+        opnd = np.stack([np.asarray(self._a, dtype=np.int64)[ids] >> 1, np.asarray(self._b, dtype=np.int64)[ids] >> 1,
+                         np.asarray(self._c, dtype=np.int64)[ids] >> 1], axis=1)
+        opnd[np.asarray(self._op, dtype=np.int8)[ids] == _OP_INPUT] = 0
+        need = np.asarray(self._hcnt, dtype=np.int64)[ids] > 0
+        order = np.argsort(-lvl, kind="stable")
+        bounds = np.flatnonzero(np.diff(lvl[order])) + 1
+        for chunk in np.split(order, bounds):
+            sel = chunk[need[chunk]]
+            if sel.size:
+                q = pos[opnd[sel].reshape(-1)]
+                need[q[q >= 0]] = True
+        return ids[need].tolist()
 
     def _build_schedule(self, pending):
         if not pending:
@@ -681,10 +704,7 @@ class TfheContext(GateBackend):
             t0 = time.perf_counter()
             eng = self._ensure_engine()
             if self._inputs:
-                nids = list(self._inputs)
-                phys = self._map_slots([self._slot[nid] for nid in nids])
-                for nid, ps in zip(nids, phys):
-                    eng.upload(int(ps) * self.lanes, self._inputs[nid].reshape(self.lanes, -1))
+                self._upload_inputs(eng, list(self._inputs), [self._inputs[nid] for nid in self._inputs])
                 self._inputs.clear()
             pending = self._live(self._pending)
             self._dormant.update(set(self._pending).difference(pending))
@@ -709,6 +729,17 @@ class TfheContext(GateBackend):
             self.exec_stats["flush_s"] += time.perf_counter() - t0
             self._pending = []
 
+    def _upload_inputs(self, eng, nids, cts):
+        """Host ciphertexts of input nodes -> their pool slots, one copy per run
+        of consecutive physical slots (inputs are allocated in order)."""
+        phys = np.asarray(self._map_slots([self._slot[nid] for nid in nids]), dtype=np.int64)
+        order = np.argsort(phys, kind="stable")
+        phys = phys[order]
+        breaks = np.flatnonzero(np.diff(phys) != 1) + 1
+        for run in np.split(np.arange(phys.size), breaks):
+            block = np.stack([np.asarray(cts[order[i]], np.uint32).reshape(self.lanes, -1) for i in run])
+            eng.upload(int(phys[run[0]]) * self.lanes, block.reshape(run.size * self.lanes, -1))
+
     def replay(self, handles, cts):
         """Per-model DAG caching: the circuit is data-oblivious,
         so after one evaluation the recorded level schedule can be re-run on new
@@ -731,9 +762,7 @@ class TfheContext(GateBackend):
             t0 = time.perf_counter()
             eng = self._ensure_engine()
             self._inputs.clear()
-            phys = self._map_slots([self._slot[nid] for nid in nids])
-            for ps, c in zip(phys, cts):
-                eng.upload(int(ps) * self.lanes, c)
+            self._upload_inputs(eng, nids, list(cts))
             try:
                 for _lvl, recs in self._history:
                     eng.run_gates(recs, lanes=self.lanes)

@@ -84,3 +84,16 @@ def test_stats_and_values_match_simcontext_on_adder_trees():
             outs.append((decrypt_word(w), decrypt_word(x), ctx.global_stats.as_dict()))
         assert outs[0] == outs[1]
         assert outs[0][0] == sum(vals)
+
+
+def test_vectorised_live_filter_matches_traversal():
+    ctx = Ctx(seed=11)
+    rng = np.random.default_rng(3)
+    bits = [ctx.encrypt(int(v)) for v in rng.integers(0, 2, 700)]
+    w = reduce_tree_sum(bits)
+    keep = [w.bits[-1], ctx.g_and(bits[0], bits[1])]
+    del w
+    pending = list(ctx._pending)
+    assert len(pending) > 2048
+    assert sorted(ctx._live_levels(pending)) == sorted(ctx._live_walk(pending))
+    assert keep

@@ -161,11 +161,13 @@ class TfheContext(GateBackend):
     enc_stream: ChaCha stream id of this context's encryptions (defaults to a
               per-process creation counter, so runs are reproducible)
     keys:     an explicit `KeySet` (overrides ``seed``)
+    stream_at: pending gates that start a background flush while the DAG is
+              still being built (0 disables; flush points are unchanged)
     """
 
     _CHUNK = 4096  # logical slots reserved at a time
 
-    def __init__(self, seed=0, device=0, lanes=1, enc_seed=None, keys=None, enc_stream=None):
+    def __init__(self, seed=0, device=0, lanes=1, enc_seed=None, keys=None, enc_stream=None, stream_at=16384):
         if lanes < 1:
             raise ValueError("lanes must be >= 1")
         self.global_stats = GateStats(label="global")
@@ -201,6 +203,9 @@ class TfheContext(GateBackend):
         self._chunks = []
         self._slot_next = 0
         self._finalizer = None
+        self.stream_at = int(stream_at)  # pending gates that start a background flush (0: off)
+        self._bg = None
+        self._bg_error = []
         # execution statistics
         self.exec_stats = {"bootstraps": 0, "gates": 0, "levels": 0, "device_ms": 0.0, "flushes": 0,
                            "flush_s": 0.0}
@@ -538,6 +543,8 @@ class TfheContext(GateBackend):
                 r = self._mk_xor(ra, rb)
             else:  # XNOR
                 r = self._mk_xor(ra, rb) ^ 1
+            if self.stream_at:
+                self._maybe_stream()
             return self._bit(r, level)
 
     def g_and(self, a, b):
@@ -570,6 +577,8 @@ class TfheContext(GateBackend):
         with self._lock:
             self._record(MUX, level)
             r = self._mk_mux(s._value, a._value, b._value)
+            if self.stream_at:
+                self._maybe_stream()
             return self._bit(r, level)
 
     # -- scoped stats (backend.py:241-257) --------------------------------------
@@ -701,33 +710,65 @@ class TfheContext(GateBackend):
     def flush(self):
         """Execute every pending gate on the device (level by level)."""
         with self._lock:
-            t0 = time.perf_counter()
-            eng = self._ensure_engine()
-            if self._inputs:
-                self._upload_inputs(eng, list(self._inputs), [self._inputs[nid] for nid in self._inputs])
-                self._inputs.clear()
-            pending = self._live(self._pending)
-            self._dormant.update(set(self._pending).difference(pending))
-            if not pending:
-                self._pending = []
-                return
-            batches = self._build_schedule(pending)
-            try:
-                for _lvl, recs in batches:
-                    eng.run_gates(recs, lanes=self.lanes)
-                eng.sync()
-            except RuntimeError as exc:
+            self._launch(wait=True)
+
+    def _maybe_stream(self):
+        """Streaming flush: once `stream_at` gates are pending and the previous
+        background batch is done, run them on a background thread while the
+        caller keeps building the DAG (device work overlaps host Python)."""
+        if (self.stream_at and len(self._pending) >= self.stream_at
+                and (self._bg is None or not self._bg.is_alive())):
+            self._launch(wait=False)
+
+    def _join_bg(self):
+        bg, self._bg = self._bg, None
+        if bg is not None:
+            bg.join()
+            if self._bg_error:
+                exc = self._bg_error.pop()
+                self._bg_error.clear()
                 raise DeviceError(str(exc)) from exc
-            self._history.extend(batches)
-            for nid in pending:
-                self._done[nid] = True
-            n_mux = sum(int(np.count_nonzero(r["kind"] == GATE_MUX)) for _, r in batches)
-            self.exec_stats["gates"] += len(pending) * self.lanes
-            self.exec_stats["bootstraps"] += (len(pending) + n_mux) * self.lanes
-            self.exec_stats["levels"] += len(batches)
-            self.exec_stats["flushes"] += 1
-            self.exec_stats["flush_s"] += time.perf_counter() - t0
-            self._pending = []
+
+    @staticmethod
+    def _run_batches(eng, batches, lanes, errors):
+        try:
+            for _lvl, recs in batches:
+                eng.run_gates(recs, lanes=lanes)
+            eng.sync()
+        except RuntimeError as exc:
+            errors.append(exc)
+
+    def _launch(self, wait):
+        self._join_bg()
+        t0 = time.perf_counter()
+        eng = self._ensure_engine()
+        if self._inputs:
+            self._upload_inputs(eng, list(self._inputs), [self._inputs[nid] for nid in self._inputs])
+            self._inputs.clear()
+        pending = self._live(self._pending)
+        self._dormant.update(set(self._pending).difference(pending))
+        self._pending = []
+        if not pending:
+            return
+        batches = self._build_schedule(pending)
+        self._history.extend(batches)
+        for nid in pending:
+            self._done[nid] = True  # results are read only after _join_bg
+        n_mux = sum(int(np.count_nonzero(r["kind"] == GATE_MUX)) for _, r in batches)
+        self.exec_stats["gates"] += len(pending) * self.lanes
+        self.exec_stats["bootstraps"] += (len(pending) + n_mux) * self.lanes
+        self.exec_stats["levels"] += len(batches)
+        self.exec_stats["flushes"] += 1
+        if wait:
+            errors = []
+            self._run_batches(eng, batches, self.lanes, errors)
+            if errors:
+                raise DeviceError(str(errors[0])) from errors[0]
+        else:
+            self._bg = threading.Thread(target=self._run_batches, args=(eng, batches, self.lanes, self._bg_error),
+                                        daemon=True)
+            self._bg.start()
+        self.exec_stats["flush_s"] += time.perf_counter() - t0
 
     def _upload_inputs(self, eng, nids, cts):
         """Host ciphertexts of input nodes -> their pool slots, one copy per run
@@ -759,6 +800,7 @@ class TfheContext(GateBackend):
             nids = [h._value >> 1 for h in handles]
             if any(nid == 0 or self._op[nid] != _OP_INPUT for nid in nids) or any(h._value & 1 for h in handles):
                 raise ValueError("replay inputs must be (non-negated) input handles")
+            self._join_bg()
             t0 = time.perf_counter()
             eng = self._ensure_engine()
             self._inputs.clear()
@@ -784,6 +826,7 @@ class TfheContext(GateBackend):
             else:
                 need.append(i)
         if need:
+            self._join_bg()
             eng = self._ensure_engine()
             slots = self._map_slots([self._slot[nodes[i]] for i in need])
             phys = (slots[:, None] * self.lanes + np.arange(self.lanes)[None, :]).reshape(-1)

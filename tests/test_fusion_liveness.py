@@ -97,3 +97,21 @@ def test_vectorised_live_filter_matches_traversal():
     assert len(pending) > 2048
     assert sorted(ctx._live_levels(pending)) == sorted(ctx._live_walk(pending))
     assert keep
+
+
+def test_streaming_flush_matches_single_flush():
+    """Background flushes while the DAG is built (stream_at) give the same
+    values and stats; only a few extra gates (live at the trigger) may run."""
+    rng = np.random.default_rng(12)
+    vals = rng.integers(0, 2, 300).tolist()
+    res = []
+    for stream_at in (0, 200):
+        ctx = Ctx(seed=13, stream_at=stream_at)
+        bits = [ctx.encrypt(v) for v in vals]
+        w = reduce_tree_sum(bits)
+        x = rc_add(w, encrypt_word(ctx, 77, w.width))
+        res.append((decrypt_word(w), decrypt_word(x), ctx.global_stats.as_dict(), ctx.exec_stats["bootstraps"],
+                    ctx.exec_stats["flushes"]))
+    assert res[0][:3] == res[1][:3] and res[0][0] == sum(vals)
+    assert res[1][4] > 1                        # background flushes happened
+    assert res[1][3] <= res[0][3] * 1.05        # little extra work

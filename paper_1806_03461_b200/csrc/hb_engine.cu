@@ -874,6 +874,10 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_lat(const BrArgs args) 
 // ---------------------------------------------------------------------------
 constexpr int kStagesU2 = 7;
 constexpr int kStagesPerPair = 3 * kRows;  // (row pair, component, row) stages per key pair
+#ifndef HB_EXP_BK_SAME
+#define HB_EXP_BK_SAME 0  // timing experiment only (results wrong): every pair re-reads pair 0's stages
+#endif
+__device__ __forceinline__ size_t u2_stage(int s) { return HB_EXP_BK_SAME ? (size_t)(s % kStagesPerPair) : (size_t)s; }
 
 __constant__ double2 c_w8[8] = {{1.0, 0.0},
                                 {0.70710678118654752440, 0.70710678118654752440},
@@ -923,7 +927,7 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate_u2(const BrArgs args
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (; issued < kStagesU2 && issued < stages_needed; issued++) {
             mbar_arrive_expect_tx(&sm.full[issued], kRowBytes);
-            bulk_g2s(sm.bk[issued], bk_src + (size_t)issued * kRowBytes, kRowBytes, &sm.full[issued]);
+            bulk_g2s(sm.bk[issued], bk_src + u2_stage(issued) * kRowBytes, kRowBytes, &sm.full[issued]);
         }
     }
     __syncthreads();
@@ -989,7 +993,7 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate_u2(const BrArgs args
                     const int s2 = issued % kStagesU2;
                     mbar_wait(&sm.empty[s2], ((issued / kStagesU2) - 1) & 1);
                     mbar_arrive_expect_tx(&sm.full[s2], kRowBytes);
-                    bulk_g2s(sm.bk[s2], bk_src + (size_t)issued * kRowBytes, kRowBytes, &sm.full[s2]);
+                    bulk_g2s(sm.bk[s2], bk_src + u2_stage(issued) * kRowBytes, kRowBytes, &sm.full[s2]);
                 }
             }
             __syncwarp();

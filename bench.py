@@ -67,8 +67,9 @@ def parse_args():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compare", action="store_true", help="skip the CGGI-key-layout comparison leg")
-    ap.add_argument("--bnn", choices=("none", "neuron", "layer", "cfg3", "cfg4", "cfg5"), default="neuron",
-                    help="extra encrypted-BNN latency measurement (BASELINE configs 2-5) on rank 0")
+    ap.add_argument("--bnn", choices=("none", "neuron", "layer", "cfg3", "cfg4", "cfg5"), default="layer",
+                    help="extra encrypted-BNN latency measurement (BASELINE configs 2-5): one GPU on rank 0, "
+                         "or Out-P over all ranks for N > 1")
     return ap.parse_args()
 
 
@@ -296,6 +297,47 @@ def cggi_layout_leg(args, dist, dev, recs, h_in, steps=5):
             "note": "CGGI key layout (one TGSW per key bit), same inputs, L2 flushed per step"}
 
 
+def bnn_outp(kind, seed, dist, dev):
+    """N > 1: one batch of BASELINE config `kind` with Out-P:
+    every rank evaluates a cost-balanced slice of each layer's output units on
+    its own GPU (its own DAG, built concurrently) and the layer's output
+    ciphertexts are all-gathered (NCCL) before the next layer.  Time = max over
+    ranks from a barrier to the gathered last layer (host DAG build included)."""
+    import torch
+
+    from paper_1806_03461_b200 import parallel, workloads
+    from paper_1806_03461_b200.backend import TfheContext, shared_keys
+    from hebnn.model import oracle_eval
+
+    cfg = {"neuron": "cfg2n", "layer": "cfg2l"}.get(kind, kind)
+    model, batch = workloads.build(cfg, seed)
+    X = workloads.inputs(cfg, model, batch, seed + 1)
+    keys = shared_keys(seed)  # deterministic: identical on every rank
+    cts = keys.encrypt(np.ascontiguousarray(X.T).reshape(-1), seed=seed + 7, stream=900)
+    cts = cts.reshape(X.shape[1], batch, -1)
+    warm = TfheContext(seed=seed, device=dev)
+    warm.decrypt(warm.g_and(warm.encrypt(1), warm.encrypt(1)))
+    comm = parallel.TorchComm(device=f"cuda:{dev}" if torch.distributed.get_backend() == "nccl" else "cpu")
+    ev = parallel.OutPEvaluator(lambda: TfheContext(seed=seed, device=dev, lanes=batch), comm)
+    dist.barrier()
+    t0 = time.perf_counter()
+    result = ev.run(model, cts)
+    elapsed = dist.max(time.perf_counter() - t0)
+    rep = {"config": cfg, "batch": batch, "mode": f"Out-P over {dist.world} GPUs", "first_eval_s": elapsed,
+           "units_per_rank": [s["units"] for s in ev.stats],
+           "executed_bootstraps_this_rank": sum(s["executed"]["bootstraps"] for s in ev.stats)}
+    if dist.rank == 0:
+        ctx = TfheContext(seed=seed, device=dev, lanes=batch)
+        if model.output_mode == "score_words":
+            got = parallel.decode_scores(ctx, result)
+        else:
+            bits = keys.decrypt(np.stack(result).reshape(-1, cts.shape[-1])).reshape(len(result), batch)
+            got = np.where(bits.T == 1, 1, -1)
+        rep["matches_oracle_eval"] = all(list(got[b]) == oracle_eval(model, [1 if v else -1 for v in X[b]])
+                                         for b in range(batch))
+    return rep
+
+
 def last_profiled_traffic(kernel="k_blind_rotate"):
     """DRAM bytes per launch of `kernel` from the newest profiles/*/traffic.json
     (written by scripts/ncu_summary.py from an `ncu --set full` capture)."""
@@ -435,7 +477,14 @@ def run_ours(args, dist):
     }
     if not args.no_compare:
         line["alt_layout"] = cggi_layout_leg(args, dist, dev, recs, h_in)
-    if dist.rank == 0 and args.bnn != "none":
+    if args.bnn != "none" and dist.world > 1:
+        try:
+            rep = bnn_outp(args.bnn, args.seed, dist, dev)
+            if dist.rank == 0:
+                line["bnn"] = rep
+        except Exception as exc:  # report, never hide
+            line["bnn"] = {"error": repr(exc)}
+    elif dist.rank == 0 and args.bnn != "none":
         try:
             line["bnn"] = bnn_latency(args.bnn, args.seed)
         except Exception as exc:  # report, never hide

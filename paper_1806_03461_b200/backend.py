@@ -190,7 +190,7 @@ class TfheContext(GateBackend):
         self._b = [0]
         self._c = [0]
         self._lvl = [0]        # execution level (after elision)
-        self._slot = [-1]      # logical pool slot
+        # logical pool slot of node nid is nid - 1 (every node takes the next slot)
         self._done = [True]
         self._hcnt = [0]       # live handles per node
         self._cse = {}
@@ -219,7 +219,8 @@ class TfheContext(GateBackend):
         return self._engine
 
     def _new_slot(self):
-        """Next logical ciphertext slot of this context (no device needed)."""
+        """Next logical ciphertext slot of this context (no device needed);
+        slots are handed out with node ids, so slot = node id - 1."""
         s = self._slot_next
         self._slot_next += 1
         return s
@@ -258,7 +259,6 @@ class TfheContext(GateBackend):
         self._b.append(b)
         self._c.append(c)
         self._lvl.append(lvl)
-        self._slot.append(slot)
         self._done.append(False)
         self._hcnt.append(0)
         if self._dormant and op != _OP_INPUT:
@@ -286,12 +286,6 @@ class TfheContext(GateBackend):
             self._pending.append(n)
             if self._op[n] != _OP_INPUT:
                 stack.extend((self._a[n] >> 1, self._b[n] >> 1, self._c[n] >> 1))
-
-    def _cse_get(self, key):
-        nid = self._cse.get(key)
-        if nid is not None and nid in self._dormant:
-            self._revive(nid)
-        return nid
 
     def encrypt(self, b):
         """Fresh encryption of bit b (all lanes) — SimContext.encrypt, backend.py:178-181."""
@@ -408,7 +402,9 @@ class TfheContext(GateBackend):
         if ra > rb:
             ra, rb = rb, ra
         key = (_OP_AND, ra, rb)
-        nid = self._cse_get(key)
+        nid = self._cse.get(key)
+        if nid is not None and self._dormant and nid in self._dormant:
+            self._revive(nid)
         if nid is None:
             lvl = 1 + max(self._lvl[ra >> 1], self._lvl[rb >> 1])
             nid = self._add_node(_OP_AND, ra, rb, 0, lvl, self._new_slot())
@@ -427,18 +423,24 @@ class TfheContext(GateBackend):
             return neg
         # XOR(XOR(p, q), r) = XOR3(p, q, r): one bootstrap at a lower level
         # (the deeper XOR operand is absorbed)
-        for x, y in sorted(((na, nb), (nb, na)), key=lambda t: -self._lvl[t[0]]):
-            if self._op[x] == _OP_XOR:
-                p, q = self._a[x] >> 1, self._b[x] >> 1
-                if y == p:
-                    return (q << 1) | neg
-                if y == q:
-                    return (p << 1) | neg
-                return self._mk_xor3(p, q, y) | neg
+        op = self._op
+        xa, xb = op[na] == _OP_XOR, op[nb] == _OP_XOR
+        if xa or xb:
+            if xa and xb and self._lvl[nb] > self._lvl[na]:
+                xa = False
+            x, y = (na, nb) if xa else (nb, na)
+            p, q = self._a[x] >> 1, self._b[x] >> 1
+            if y == p:
+                return (q << 1) | neg
+            if y == q:
+                return (p << 1) | neg
+            return self._mk_xor3(p, q, y) | neg
         if na > nb:
             na, nb = nb, na
         key = (_OP_XOR, na, nb)
-        nid = self._cse_get(key)
+        nid = self._cse.get(key)
+        if nid is not None and self._dormant and nid in self._dormant:
+            self._revive(nid)
         if nid is None:
             lvl = 1 + max(self._lvl[na], self._lvl[nb])
             nid = self._add_node(_OP_XOR, na << 1, nb << 1, 0, lvl, self._new_slot())
@@ -476,7 +478,9 @@ class TfheContext(GateBackend):
                 return (self._mk_and(q ^ 1, r ^ 1) ^ 1) if p & 1 else self._mk_and(q, r)
         x, y, z = sorted((x, y, z))
         key = (_OP_MAJ, x, y, z)
-        nid = self._cse_get(key)
+        nid = self._cse.get(key)
+        if nid is not None and self._dormant and nid in self._dormant:
+            self._revive(nid)
         if nid is None:
             lvl = 1 + max(self._lvl[x >> 1], self._lvl[y >> 1], self._lvl[z >> 1])
             nid = self._add_node(_OP_MAJ, x, y, z, lvl, self._new_slot())
@@ -488,7 +492,9 @@ class TfheContext(GateBackend):
         """ref of XOR3 of three distinct non-constant nodes."""
         p, q, r = sorted((p, q, r))
         key = (_OP_XOR3, p, q, r)
-        nid = self._cse_get(key)
+        nid = self._cse.get(key)
+        if nid is not None and self._dormant and nid in self._dormant:
+            self._revive(nid)
         if nid is None:
             lvl = 1 + max(self._lvl[p], self._lvl[q], self._lvl[r])
             nid = self._add_node(_OP_XOR3, p << 1, q << 1, r << 1, lvl, self._new_slot())
@@ -520,7 +526,9 @@ class TfheContext(GateBackend):
         if rb == rs ^ 1:  # s ? a : ~s = ~s OR a
             return self._mk_and(rs, ra ^ 1) ^ 1
         key = (_OP_MUX, rs, ra, rb)
-        nid = self._cse_get(key)
+        nid = self._cse.get(key)
+        if nid is not None and self._dormant and nid in self._dormant:
+            self._revive(nid)
         if nid is None:
             lvl = 1 + max(self._lvl[rs >> 1], self._lvl[ra >> 1], self._lvl[rb >> 1])
             nid = self._add_node(_OP_MUX, rs, ra, rb, lvl, self._new_slot())
@@ -530,10 +538,14 @@ class TfheContext(GateBackend):
 
     def _binary_gate(self, kind, a, b):
         """SimContext._binary_gate (backend.py:205-209) on real ciphertexts."""
-        self._check(a, b)
-        level = max(a.level, b.level) + 1
+        if not (isinstance(a, CipherBit) and isinstance(b, CipherBit) and a._ctx is self and b._ctx is self):
+            raise ContextMismatchError("bit handle does not belong to this context")
+        la, lb = a.level, b.level
+        level = (la if la > lb else lb) + 1
         with self._lock:
-            self._record(kind, level)
+            self.global_stats.record(kind, level)
+            for scope in self._scopes:
+                scope.record(kind, level)
             ra, rb = a._value, b._value
             if kind == AND:
                 r = self._mk_and(ra, rb)
@@ -543,9 +555,10 @@ class TfheContext(GateBackend):
                 r = self._mk_xor(ra, rb)
             else:  # XNOR
                 r = self._mk_xor(ra, rb) ^ 1
-            if self.stream_at:
+            if self.stream_at and len(self._pending) >= self.stream_at:
                 self._maybe_stream()
-            return self._bit(r, level)
+            self._hcnt[r >> 1] += 1
+            return _Bit(self, r, level)
 
     def g_and(self, a, b):
         return self._binary_gate(AND, a, b)
@@ -662,11 +675,8 @@ class TfheContext(GateBackend):
             b = np.fromiter((self._b[i] for i in pending), np.int64, len(pending))
             c = np.fromiter((self._c[i] for i in pending), np.int64, len(pending))
             lvl = np.fromiter((self._lvl[i] for i in pending), np.int64, len(pending))
-            sl = self._slot
-            dst = np.fromiter((sl[i] for i in pending), np.int64, len(pending))
-            s_a = np.fromiter((sl[r >> 1] for r in a.tolist()), np.int64, len(pending))
-            s_b = np.fromiter((sl[r >> 1] for r in b.tolist()), np.int64, len(pending))
-            s_c = np.fromiter((sl[r >> 1] for r in c.tolist()), np.int64, len(pending))
+            dst = np.asarray(pending, dtype=np.int64) - 1
+            s_a, s_b, s_c = (a >> 1) - 1, (b >> 1) - 1, (c >> 1) - 1
         else:
             ids = np.asarray(pending, dtype=np.int64)
             op = np.asarray(self._op, dtype=np.int8)[ids]
@@ -674,8 +684,7 @@ class TfheContext(GateBackend):
             b = np.asarray(self._b, dtype=np.int64)[ids]
             c = np.asarray(self._c, dtype=np.int64)[ids]
             lvl = np.asarray(self._lvl, dtype=np.int64)[ids]
-            slot = np.asarray(self._slot, dtype=np.int64)
-            dst, s_a, s_b, s_c = slot[ids], slot[a >> 1], slot[b >> 1], slot[c >> 1]
+            dst, s_a, s_b, s_c = ids - 1, (a >> 1) - 1, (b >> 1) - 1, (c >> 1) - 1
         is_and = op == _OP_AND
         is_xor = op == _OP_XOR
         is_mux = op == _OP_MUX
@@ -773,7 +782,7 @@ class TfheContext(GateBackend):
     def _upload_inputs(self, eng, nids, cts):
         """Host ciphertexts of input nodes -> their pool slots, one copy per run
         of consecutive physical slots (inputs are allocated in order)."""
-        phys = np.asarray(self._map_slots([self._slot[nid] for nid in nids]), dtype=np.int64)
+        phys = np.asarray(self._map_slots(np.asarray(nids, dtype=np.int64) - 1), dtype=np.int64)
         order = np.argsort(phys, kind="stable")
         phys = phys[order]
         breaks = np.flatnonzero(np.diff(phys) != 1) + 1
@@ -828,7 +837,7 @@ class TfheContext(GateBackend):
         if need:
             self._join_bg()
             eng = self._ensure_engine()
-            slots = self._map_slots([self._slot[nodes[i]] for i in need])
+            slots = self._map_slots([nodes[i] - 1 for i in need])
             phys = (slots[:, None] * self.lanes + np.arange(self.lanes)[None, :]).reshape(-1)
             try:
                 got = eng.gather(phys.astype(np.uint32))

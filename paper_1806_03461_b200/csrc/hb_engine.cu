@@ -874,6 +874,9 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_lat(const BrArgs args) 
 // ---------------------------------------------------------------------------
 constexpr int kStagesU2 = 7;
 constexpr int kStagesPerPair = 3 * kRows;  // (row pair, component, row) stages per key pair
+#ifndef HB_TRACE
+#define HB_TRACE 0  // per-phase clock64 trace of the cluster latency kernel (printf, one pair)
+#endif
 #ifndef HB_EXP_BK_SAME
 #define HB_EXP_BK_SAME 0  // timing experiment only (results wrong): every pair re-reads pair 0's stages
 #endif
@@ -1327,7 +1330,7 @@ struct BrCluSmemU2 {
     double2 bk[3][3][2 * kNH];               // [group][component slot][output poly][bin]
     uint64_t full[3][3];
     uint32_t acc[kN];                        // ACC_q
-    double2 xch[3][2][kXchStride];           // per group: FFT exchange, then partials [o][512]
+    double2 xch[3][2][kXchStride];           // per group: [0] FFT exchange, then own partial; [1] peer's partial
     double2 inv[kXchStride];                 // group 0's inverse-FFT exchange
     uint16_t bar[kMaxLweN + 1];
     TwSeeds tws[64];
@@ -1401,7 +1404,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) k_blind_rota
     cluster.sync();  // peer smem live (DSMEM), ACC initialised
 
     double max_err = 0.0;
+#if HB_TRACE
+    long long tr[12];
+#define HB_TR(k) do { if (pm == 100) tr[k] = clock64(); } while (0)
+#else
+#define HB_TR(k) do { } while (0)
+#endif
     for (int pm = 0; pm < pairs; pm++) {
+        HB_TR(0);
         const int ai = sm.bar[2 * pm], aj = sm.bar[2 * pm + 1];
         int ex[3];
         double2 base[3];  // issued before the FFT: the table loads' L2 latency overlaps it
@@ -1418,7 +1428,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) k_blind_rota
                                    small_int_to_double(gadget_digit(sm.acc[j + kNH], p)));
         }
         if (pm > 0) cluster_wait();  // the peer has read our previous partials (relaxed arrive below)
+        HB_TR(1);
         nega_fft_fwd_n<1, true>(x, xch, t, sm.tws[t], bar_id);
+        HB_TR(2);
         double2 f0[8], f1[8];
 #pragma unroll
         for (int c = 0; c < 3; c++) {
@@ -1450,35 +1462,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) k_blind_rota
                     cmac(f1[m], y, bk1[t + 64 * m]);
                 }
             }
-            group_bar(bar_id);  // both warps done with the slot
-            if (t == 0 && pm + 1 < pairs) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        HB_TR(9);
+        group_bar(bar_id);  // both warps done with the three slots (and with the FFT's xch reads)
+        HB_TR(10);
+        if (t == 0 && pm + 1 < pairs) {  // the next pair's stages load during reduce / inverse / FFT
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            for (int c = 0; c < 3; c++) {
                 mbar_arrive_expect_tx(&sm.full[grp][c], kRowBytes);
                 bulk_g2s(sm.bk[grp][c], stage_src(pm + 1, c), kRowBytes, &sm.full[grp][c]);
             }
         }
-        // partials [o][512] into this group's exchange buffer (its FFT readers are done:
-        // the group barrier of the last stage above)
+        // partial of our output q into this group's exchange buffer (its FFT readers are
+        // done: the group barrier of the last stage above); the partial of the peer's
+        // output goes straight into the upper half of the peer group's buffer (unused by
+        // its single-poly FFT; its previous contents were consumed before the peer's
+        // relaxed arrive that our cluster_wait matched)
+        {
+            double2 *remote = &peer.xch[grp][1][0];
 #pragma unroll
-        for (int m = 0; m < 8; m++) {
-            xch[t + 64 * m] = f0[m];
-            xch[kNH + t + 64 * m] = f1[m];
+            for (int m = 0; m < 8; m++) {
+                xch[t + 64 * m] = q ? f1[m] : f0[m];
+                remote[t + 64 * m] = q ? f0[m] : f1[m];
+            }
         }
+        HB_TR(3);
         cluster_sync_acq_rel();  // all six groups' partials visible cluster-wide
+        HB_TR(4);
         if (grp != 0) cluster_arrive_relaxed();
         if (grp == 0) {
             double2 y[1][8];
 #pragma unroll
             for (int m = 0; m < 8; m++) {
-                const int k = q * kNH + t + 64 * m;  // partial of output q in each group's [o][512]
-                const double2 *l0 = &sm.xch[0][0][0], *l1 = &sm.xch[1][0][0], *l2 = &sm.xch[2][0][0];
-                const double2 *r0 = &peer.xch[0][0][0], *r1 = &peer.xch[1][0][0], *r2 = &peer.xch[2][0][0];
-                double2 v = cadd(cadd(l0[k], l1[k]), l2[k]);
-                v = cadd(v, cadd(cadd(r0[k], r1[k]), r2[k]));
+                const int k = t + 64 * m;  // own partials in [g][0], the peer's in [g][1]
+                double2 v = cadd(cadd(sm.xch[0][0][k], sm.xch[1][0][k]), sm.xch[2][0][k]);
+                v = cadd(v, cadd(cadd(sm.xch[0][1][k], sm.xch[1][1][k]), sm.xch[2][1][k]));
                 y[0][m] = v;
             }
-            cluster_arrive_relaxed();  // partial reads consumed (values are in registers)
+            cluster_arrive_relaxed();  // received partials consumed (values are in registers)
+            HB_TR(5);
             nega_fft_inv_n<1, true>(y, sm.inv, t, sm.tws[t], bar_id);
+            HB_TR(6);
 #pragma unroll
             for (int m = 0; m < 8; m++) {
                 const double lo = y[0][m].x, hi = y[0][m].y;
@@ -1491,8 +1515,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) k_blind_rota
                 sm.acc[j + kNH] += round_to_torus(hi);
             }
         }
+        HB_TR(7);
         __syncthreads();  // ACC_q updated
+        HB_TR(8);
+#if HB_TRACE
+        if (pm == 100 && blockIdx.x == 0 && threadIdx.x == 0)
+            printf("clu trace: digits %lld fwd %lld mac %lld bar %lld partials %lld sync1 %lld reduce %lld inv %lld "
+                   "acc %lld sync2 %lld\n",
+                   tr[1] - tr[0], tr[2] - tr[1], tr[9] - tr[2], tr[10] - tr[9], tr[3] - tr[10], tr[4] - tr[3],
+                   tr[5] - tr[4], tr[6] - tr[5], tr[7] - tr[6], tr[8] - tr[7]);
+#endif
     }
+#undef HB_TR
     if (pairs > 0) cluster_wait();  // the peer is done reading our shared memory
 
     if (kDebug && args.margin) atomicMax(args.margin, (unsigned long long)__double_as_longlong(max_err));

@@ -115,3 +115,27 @@ def test_streaming_flush_matches_single_flush():
     assert res[0][:3] == res[1][:3] and res[0][0] == sum(vals)
     assert res[1][4] > 1                        # background flushes happened
     assert res[1][3] <= res[0][3] * 1.05        # little extra work
+
+
+def test_concurrent_gate_issue_with_streaming():
+    """Several threads issue gates on one context (SimContext's lock contract,
+    backend.py:174,200) while background flushes run (small stream_at)."""
+    import threading
+
+    ctx = Ctx(seed=21, stream_at=64)
+    rng = np.random.default_rng(5)
+    data = [rng.integers(0, 2, 40).tolist() for _ in range(4)]
+    results = {}
+
+    def work(i):
+        bits = [ctx.encrypt(v) for v in data[i]]
+        results[i] = reduce_tree_sum(bits)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    for i in range(4):
+        assert decrypt_word(results[i]) == sum(data[i])
+    assert ctx.exec_stats["flushes"] > 1

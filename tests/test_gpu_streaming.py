@@ -1,0 +1,33 @@
+"""Streaming flushes on the B200: background level batches while the
+reference compiler builds the DAG give bit-identical output ciphertexts."""
+
+import random
+
+import numpy as np
+import pytest
+
+from hebnn.compiler import eval_model
+from hebnn.model import DenseLayer, SignActivation, TernaryModel, oracle_eval, validate_model
+
+pytestmark = pytest.mark.gpu
+
+
+def test_streaming_flush_bit_identical():
+    from paper_1806_03461_b200.backend import TfheContext
+
+    rng = random.Random(3)
+    d, p = 200, 12
+    rows = tuple(tuple(rng.choice((-1, 1)) for _ in range(d)) for _ in range(p))
+    model = validate_model(TernaryModel(d, (DenseLayer(rows, (0,) * p), SignActivation()), "sign_bits"))
+    xs = [rng.choice((0, 1)) for _ in range(d)]
+    outs = []
+    for stream_at in (0, 300):
+        ctx = TfheContext(seed=42, enc_stream=77, stream_at=stream_at)
+        handles = [ctx.encrypt(v) for v in xs]
+        res, _ = eval_model(ctx, model, handles)
+        outs.append((ctx.export_ciphertexts(res), [ctx.decrypt(h) for h in res], ctx.exec_stats["flushes"]))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1]
+    want = oracle_eval(model, [1 if v else -1 for v in xs])
+    assert [1 if b else -1 for b in outs[0][1]] == want
+    assert outs[1][2] > outs[0][2]

@@ -237,3 +237,41 @@ np.save(sys.argv[1], eng.download(3 * n, n))
             subprocess.run([sys.executable, "-c", code, path, str(n), str(unroll)], check=True, cwd=root, env=env)
             outs.append(np.load(path))
         assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+def test_random_mixed_level_bit_exact_vs_oracle(kit):
+    """512 random records of every kind (LIN2 gates with random signs, MUX,
+    3-input majority / XOR3 with random signs) in one level: the GPU pool
+    equals the oracle's or_run_gates pool word for word."""
+    engine, keys, octx = kit
+    rng = np.random.default_rng(99)
+    n_in, n = 96, 512
+    bits = rng.integers(0, 2, n_in).astype(np.uint8)
+    cts = keys.encrypt(bits, seed=77, stream=5)
+    recs = tfhe.gate_records(n)
+    recs["dst"] = n_in + np.arange(n)
+    srcs = rng.integers(0, n_in, (n, 3))
+    recs["src_a"], recs["src_b"], recs["src_c"] = srcs[:, 0], srcs[:, 1], srcs[:, 2]
+    kind = rng.integers(0, 3, n)
+    recs["kind"] = kind
+    names = list(tfhe.GATE_LIN)
+    for i in range(n):
+        if kind[i] == 0:
+            c0, al, be = tfhe.GATE_LIN[names[rng.integers(0, len(names))]]
+            recs["c0"][i], recs["alpha"][i], recs["beta"][i], recs["gamma"][i] = c0, al, be, 0
+        elif kind[i] == 1:
+            recs["c0"][i], recs["alpha"][i], recs["beta"][i], recs["gamma"][i] = 0, rng.choice((-1, 1)), rng.choice((-1, 1)), 0
+        else:
+            sg = rng.choice((-1, 1), 3)
+            coef = (-2, -2, -2) if rng.integers(0, 2) else tuple(int(v) for v in sg)
+            recs["c0"][i], recs["alpha"][i], recs["beta"][i], recs["gamma"][i] = 0, coef[0], coef[1], coef[2]
+    engine.reserve(n_in + n)
+    engine.upload(0, cts)
+    engine.run_gates(recs)
+    got = engine.download(n_in, n)
+    pool = np.zeros((n_in + n, P.n + 1), np.uint32)
+    pool[:n_in] = cts
+    import os
+
+    octx.run_gates(recs, pool, threads=os.cpu_count() or 1)
+    assert np.array_equal(got, pool[n_in:])

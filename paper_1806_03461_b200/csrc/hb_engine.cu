@@ -3,15 +3,20 @@
 // 205-237, where SimContext only simulates each gate in plaintext).
 //
 // Kernels:
-//   k_bk_to_fourier   K6  BK (u32 coefficients) -> FP64 negacyclic Fourier domain
-//   k_blind_rotate    K1+K2+K3 fused: gate linear combination + mod switch,
-//                     630 CMux external products (gadget decomposition, FP64
-//                     FFT in registers/shared memory, BK rows streamed by
-//                     cp.async.bulk into a shared-memory ring and reused by
-//                     every gate of the CTA), sample extraction
-//   k_keyswitch       K4  batched LWE key switch (uint32), KSK rows shared by a
-//                     tile of gates
-//   k_gather          pool slots -> contiguous buffer for download
+//   k_bk_to_fourier        K6  BK (u32 coefficients) -> FP64 negacyclic Fourier domain
+//   k_blind_rotate_u2      K1+K2+K3 fused, key-pair bootstrapping key (default):
+//                          gate linear combination (2 or 3 inputs) + mod switch,
+//                          315 external products with the combined TGSW
+//                          sum_c (X^e_c - 1) BK_c (gadget decomposition, FP64 FFT in
+//                          registers/shared memory, BK stages streamed by
+//                          cp.async.bulk into a shared-memory ring and reused by
+//                          every gate of the CTA), sample extraction
+//   k_blind_rotate_u2_lat  the same for narrow levels: one bootstrap per CTA
+//   k_blind_rotate_u2_clu  the same for very narrow levels: one bootstrap per 2-CTA cluster
+//   k_blind_rotate[_lat]   CGGI bootstrapping key (bk_unroll 1): 630 CMux steps
+//   k_keyswitch            K4  batched LWE key switch (uint32), KSK table chunks
+//                          shared by a tile of gates
+//   k_gather               pool slots -> contiguous buffer for download
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>

@@ -57,7 +57,9 @@ _C_XOR = 2 * EIGHTH
 
 
 class DeviceError(RuntimeError):
-    """Raised when the B200 engine cannot run (no device, CUDA failure)."""
+    """Raised when the B200 engine cannot run (no device, CUDA failure).  The
+    gates of the failed flush count as executed, so a context that raised it
+    must not be decrypted from again (create a new one)."""
 
 
 class _Bit(CipherBit):

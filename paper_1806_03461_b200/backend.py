@@ -817,13 +817,28 @@ class TfheContext(GateBackend):
             self._inputs.clear()
             self._upload_inputs(eng, nids, list(cts))
             try:
-                for _lvl, recs in self._history:
+                for _lvl, recs in self._replay_schedule():
                     eng.run_gates(recs, lanes=self.lanes)
                 eng.sync()
             except RuntimeError as exc:
                 raise DeviceError(str(exc)) from exc
             self.exec_stats["replays"] = self.exec_stats.get("replays", 0) + 1
             self.exec_stats["flush_s"] += time.perf_counter() - t0
+
+    def _replay_schedule(self):
+        """The executed history regrouped by node level: streaming flushes split
+        a model's levels over several launches; a replay runs each level once."""
+        if getattr(self, "_replay_cache", (None,))[0] != len(self._history):
+            if len(self._history) > 1:
+                lv = np.concatenate([np.full(r.size, l, np.int64) for l, r in self._history])
+                recs = np.concatenate([r for _, r in self._history])
+                order = np.argsort(lv, kind="stable")
+                bounds = np.flatnonzero(np.diff(lv[order])) + 1
+                sched = [(int(lv[c[0]]), recs[c]) for c in np.split(order, bounds)]
+            else:
+                sched = list(self._history)
+            self._replay_cache = (len(self._history), sched)
+        return self._replay_cache[1]
 
     def _ciphertexts(self, refs):
         """Host LWE samples [len(refs)][lanes][n+1] for node refs (no negation)."""

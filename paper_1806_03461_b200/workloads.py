@@ -126,18 +126,20 @@ def run_encrypted(ctx_cls, config, seed=0, device=0, options=EvalOptions(), chec
             if check:
                 oks.append(all(list(got2[b]) == oracle_eval(model, [1 if v else -1 for v in X2[b]])
                                for b in range(batch)))
-        replay = {"replays": replays, "latency_s": min(times), "matches_oracle_eval": all(oks) if check else None}
+        replay = {"replays": replays, "latency_s": min(times), "bootstraps_per_s": ctx.exec_stats["bootstraps"] / min(times),
+                  "matches_oracle_eval": all(oks) if check else None}
     return {
         "config": config, "batch": batch, "counted_gates": counted,
         "counted_gates_per_input": ctx.gate_count,
         "executed_bootstraps": ctx.exec_stats["bootstraps"], "levels": ctx.exec_stats["levels"],
         "depth": ctx.global_stats.max_level,
-        "encrypt_s": t1 - t0, "dag_build_s": t2 - t1, "device_flush_s": t3 - t2, "decrypt_s": t4 - t3,
-        "latency_s": t3 - t2 + (t4 - t3),
-        # encrypt + DAG build (overlapping background flushes) + final flush + decrypt
+        # first evaluation: encrypt + DAG build through the reference compiler (with
+        # background flushes running on the device meanwhile) + final flush + decrypt
         "first_eval_s": t4 - t0,
-        "bootstraps_per_s": ctx.exec_stats["bootstraps"] / (t3 - t2),
-        "counted_gates_per_s": counted / (t3 - t2),
+        "encrypt_s": t1 - t0, "dag_build_s": t2 - t1, "final_flush_s": t3 - t2, "decrypt_s": t4 - t3,
+        "background_flushes": ctx.exec_stats["flushes"] - 1,
+        "bootstraps_per_s": ctx.exec_stats["bootstraps"] / (t4 - t0),
+        "counted_gates_per_s": counted / (t4 - t0),
         "matches_oracle_eval": ok,
         "replay": replay,
     }

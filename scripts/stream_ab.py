@@ -15,6 +15,6 @@ for cfg in cfgs:
         cls = type("C", (TfheContext,), {"__init__": lambda self, *a, _sa=sa, **k: TfheContext.__init__(self, *a, stream_at=_sa, **k)})
         rep = workloads.run_encrypted(cls, cfg)
         print(json.dumps({"config": cfg, "stream_at": sa, "first_eval_s": rep["first_eval_s"],
-                          "dag_build_s": rep["dag_build_s"], "final_flush_s": rep["device_flush_s"],
+                          "dag_build_s": rep["dag_build_s"], "final_flush_s": rep["final_flush_s"],
                           "executed": rep["executed_bootstraps"], "levels": rep["levels"],
                           "ok": rep["matches_oracle_eval"]}), flush=True)

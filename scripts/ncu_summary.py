@@ -44,6 +44,12 @@ for rep in sorted(f for f in os.listdir(src) if f.endswith(".ncu-rep")):
         rd = float(v[h.index("dram__bytes_read.sum")]) * mult.get(units[h.index("dram__bytes_read.sum")], 1)
         wr = float(v[h.index("dram__bytes_write.sum")]) * mult.get(units[h.index("dram__bytes_write.sum")], 1)
         traffic[rep.replace(".ncu-rep", "")] = rd + wr
+        tmult = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
+        ti = h.index("gpu__time_duration.sum")
+        dur = float(v[ti]) * tmult.get(units[ti], 1e-3)
+        hbm = 6547.5  # MEASURED_PEAKS.json hbm_gbs
+        lines.insert(-1, f"- DRAM bandwidth: {(rd + wr) / dur / 1e9:.1f} GB/s = {100 * (rd + wr) / dur / 1e9 / hbm:.2f}% "
+                         f"of the measured {hbm} GB/s")
 launch = os.path.join(src, "launches.csv")
 if os.path.exists(launch):
     txt = [l for l in open(launch) if not l.startswith("==")]

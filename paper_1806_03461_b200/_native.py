@@ -69,6 +69,25 @@ assert GATE_DTYPE.itemsize == 24
 _lib = None
 
 
+_dag = None
+
+
+def dag_module():
+    """The host gate-DAG extension (csrc/hb_dag.cpp; built by paper_1806_03461_b200.build)."""
+    global _dag
+    if _dag is None:
+        import importlib.util
+        import sysconfig
+
+        path = os.path.join(_HERE, "_lib", "hb_dag" + sysconfig.get_config_var("EXT_SUFFIX"))
+        if not os.path.exists(path):
+            raise NativeLibraryMissing(f"{path} not found: build it with `python -m paper_1806_03461_b200.build`")
+        spec = importlib.util.spec_from_file_location("hb_dag", path)
+        _dag = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(_dag)
+    return _dag
+
+
 def lib():
     """Load the engine library (raises NativeLibraryMissing if absent)."""
     global _lib

@@ -39,18 +39,20 @@ import weakref
 import numpy as np
 
 from . import gate_api as api
-from ._native import GATE_DTYPE, GATE_LIN2, GATE_LIN3, GATE_MUX
+from ._native import GATE_DTYPE, GATE_LIN2, GATE_LIN3, GATE_MUX, dag_module
 from .gate_api import AND, MUX, OR, XNOR, XOR, CipherBit, ContextMismatchError, GateBackend, GateStats, ScopeError
 from .tfhe import EIGHTH, MASK32, Engine, KeySet
 
-# internal node opcodes
-_OP_CONST = 0   # node 0: the constant 0 (ref 0 = false, ref 1 = true)
-_OP_INPUT = 1   # fresh encryption
-_OP_AND = 2     # AND(ref_a, ref_b): NOT flags live in the refs
-_OP_XOR = 3     # XOR(node_a, node_b): NOT flags are pushed to the output ref
-_OP_MUX = 4     # MUX(node_s, ref_a, ref_b): selector kept positive
-_OP_MAJ = 5     # MAJ(ref_a, ref_b, ref_c): 3-input majority (a full adder's carry)
-_OP_XOR3 = 6    # XOR3(node_a, node_b, node_c): NOT flags pushed to the output ref
+# node opcodes of the native gate DAG (csrc/hb_dag.cpp): node 0 is the constant 0
+# (ref 0 = false, ref 1 = true); refs are (node << 1) | NOT flag
+_DAG = dag_module()
+_OP_INPUT = _DAG.OP_INPUT
+_OP_AND = _DAG.OP_AND
+_OP_XOR = _DAG.OP_XOR
+_OP_MUX = _DAG.OP_MUX
+_OP_MAJ = _DAG.OP_MAJ
+_OP_XOR3 = _DAG.OP_XOR3
+_KIND = {AND: 0, OR: 1, XOR: 2, XNOR: 3}  # Dag.gate kinds
 
 _C_AND = (-EIGHTH) & MASK32
 _C_XOR = 2 * EIGHTH
@@ -186,24 +188,14 @@ class TfheContext(GateBackend):
             _CONTEXT_SERIAL += 1
             serial = _CONTEXT_SERIAL
         self.enc_stream = (serial if enc_stream is None else int(enc_stream)) & 0xFFFFF
-        # DAG storage (parallel lists; node 0 is the constant 0)
-        self._op = [_OP_CONST]
-        self._a = [0]
-        self._b = [0]
-        self._c = [0]
-        self._lvl = [0]        # execution level (after elision)
-        # logical pool slot of node nid is nid - 1 (every node takes the next slot)
-        self._done = [True]
-        self._hcnt = [0]       # live handles per node
-        self._cse = {}
-        self._pending = []     # node ids not yet executed
-        self._dormant = set()  # not executed: unreachable from live handles at their flush
+        # gate DAG (native, csrc/hb_dag.cpp): node store, elision, CSE, full-adder
+        # fusion, live-handle counts; logical pool slot of node n is n - 1
+        self._dag = _DAG.Dag()
         self._inputs = {}      # node id -> host ciphertexts [lanes][n+1] not yet uploaded
         self._engine = None
         self._slots = None
         self._history = []     # every executed (level, records) batch, in order (f1 replay)
         self._chunks = []
-        self._slot_next = 0
         self._finalizer = None
         self.stream_at = int(stream_at)  # pending gates that start a background flush (0: off)
         self._bg = None
@@ -220,19 +212,13 @@ class TfheContext(GateBackend):
             self._finalizer = weakref.finalize(self, _release_chunks, self._slots, self._chunks)
         return self._engine
 
-    def _new_slot(self):
-        """Next logical ciphertext slot of this context (no device needed);
-        slots are handed out with node ids, so slot = node id - 1."""
-        s = self._slot_next
-        self._slot_next += 1
-        return s
 
     def _map_slots(self, logical):
         """Logical slots -> engine record slots (chunks of the shared pool are
         reserved on demand, aligned to `lanes` so slot * lanes + lane is the
         physical pool index)."""
         self._ensure_engine()
-        need = self._slot_next // self._CHUNK + 1
+        need = (self._dag.size() - 1) // self._CHUNK + 1
         while len(self._chunks) < need:
             base = self._slots.alloc(self._CHUNK * self.lanes, align=self.lanes)
             self._chunks.append((base, self._CHUNK * self.lanes))
@@ -254,40 +240,13 @@ class TfheContext(GateBackend):
 
     # -- bit creation ----------------------------------------------------------
 
-    def _add_node(self, op, a, b, c, lvl, slot):
-        nid = len(self._op)
-        self._op.append(op)
-        self._a.append(a)
-        self._b.append(b)
-        self._c.append(c)
-        self._lvl.append(lvl)
-        self._done.append(False)
-        self._hcnt.append(0)
-        if self._dormant and op != _OP_INPUT:
-            for r in (a, b, c):
-                if (r >> 1) in self._dormant:
-                    self._revive(r >> 1)
-        return nid
-
     def _bit(self, r, level, trivial=None):
         """A handle on ref r (counted for the live-gate filter of flush)."""
-        self._hcnt[r >> 1] += 1
+        self._dag.hinc(r >> 1)
         return _Bit(self, r, level, trivial)
 
     def _drop(self, nid):
-        self._hcnt[nid] -= 1
-
-    def _revive(self, nid):
-        """Dormant node (and its dormant operands) back to pending."""
-        stack = [nid]
-        while stack:
-            n = stack.pop()
-            if n not in self._dormant:
-                continue
-            self._dormant.discard(n)
-            self._pending.append(n)
-            if self._op[n] != _OP_INPUT:
-                stack.extend((self._a[n] >> 1, self._b[n] >> 1, self._c[n] >> 1))
+        self._dag.hdec(nid)
 
     def encrypt(self, b):
         """Fresh encryption of bit b (all lanes) — SimContext.encrypt, backend.py:178-181."""
@@ -306,9 +265,7 @@ class TfheContext(GateBackend):
             idx0 = self._enc_count
             self._enc_count += self.lanes
             cts = self._encrypt_host(bits.astype(np.uint8), idx0)
-            slot = self._new_slot()
-            nid = self._add_node(_OP_INPUT, 0, 0, 0, 0, slot)
-            self._done[nid] = True  # value known on the host; uploaded at flush
+            nid = self._dag.add_input()  # value known on the host; uploaded at flush
             self._inputs[nid] = cts
             return self._bit(nid << 1, 0)
 
@@ -329,9 +286,7 @@ class TfheContext(GateBackend):
             cts = self._encrypt_host(bits.reshape(-1).astype(np.uint8), idx0).reshape(count, self.lanes, -1)
             out = []
             for i in range(count):
-                slot = self._new_slot()
-                nid = self._add_node(_OP_INPUT, 0, 0, 0, 0, slot)
-                self._done[nid] = True
+                nid = self._dag.add_input()
                 self._inputs[nid] = cts[i]
                 out.append(self._bit(nid << 1, 0))
             return out
@@ -347,8 +302,7 @@ class TfheContext(GateBackend):
         with self._lock:
             out = []
             for i in range(cts.shape[0]):
-                nid = self._add_node(_OP_INPUT, 0, 0, 0, 0, self._new_slot())
-                self._done[nid] = True
+                nid = self._dag.add_input()
                 self._inputs[nid] = np.ascontiguousarray(cts[i])
                 out.append(self._bit(nid << 1, 0))
             return out
@@ -360,9 +314,8 @@ class TfheContext(GateBackend):
         with self._lock:
             refs = [h._value for h in handles]
             for r in refs:
-                if (r >> 1) in self._dormant:
-                    self._revive(r >> 1)
-            if self._pending:
+                self._dag.revive(r >> 1)
+            if self._dag.pending_count():
                 self.flush()
             out = np.zeros((len(refs), self.lanes, self.params.n + 1), np.uint32)
             live = [i for i, r in enumerate(refs) if (r >> 1) != 0]
@@ -387,157 +340,6 @@ class TfheContext(GateBackend):
 
     # -- gates -------------------------------------------------------------------
 
-    def _mk_and(self, ra, rb):
-        """ref of AND(ra, rb) with constant/duplicate elision and CSE."""
-        if (ra >> 1) == 0:
-            return rb if ra & 1 else 0
-        if (rb >> 1) == 0:
-            return ra if rb & 1 else 0
-        if ra == rb:
-            return ra
-        if ra == rb ^ 1:
-            return 0
-        if ra & rb & 1:  # OR(u, v): a full adder's carry folds into one majority
-            m = self._try_maj(ra ^ 1, rb ^ 1)
-            if m is not None:
-                return m ^ 1
-        if ra > rb:
-            ra, rb = rb, ra
-        key = (_OP_AND, ra, rb)
-        nid = self._cse.get(key)
-        if nid is not None and self._dormant and nid in self._dormant:
-            self._revive(nid)
-        if nid is None:
-            lvl = 1 + max(self._lvl[ra >> 1], self._lvl[rb >> 1])
-            nid = self._add_node(_OP_AND, ra, rb, 0, lvl, self._new_slot())
-            self._cse[key] = nid
-            self._pending.append(nid)
-        return nid << 1
-
-    def _mk_xor(self, ra, rb):
-        neg = (ra ^ rb) & 1
-        na, nb = ra >> 1, rb >> 1
-        if na == 0:
-            return rb ^ (ra & 1)
-        if nb == 0:
-            return ra ^ (rb & 1)
-        if na == nb:
-            return neg
-        # XOR(XOR(p, q), r) = XOR3(p, q, r): one bootstrap at a lower level
-        # (the deeper XOR operand is absorbed)
-        op = self._op
-        xa, xb = op[na] == _OP_XOR, op[nb] == _OP_XOR
-        if xa or xb:
-            if xa and xb and self._lvl[nb] > self._lvl[na]:
-                xa = False
-            x, y = (na, nb) if xa else (nb, na)
-            p, q = self._a[x] >> 1, self._b[x] >> 1
-            if y == p:
-                return (q << 1) | neg
-            if y == q:
-                return (p << 1) | neg
-            return self._mk_xor3(p, q, y) | neg
-        if na > nb:
-            na, nb = nb, na
-        key = (_OP_XOR, na, nb)
-        nid = self._cse.get(key)
-        if nid is not None and self._dormant and nid in self._dormant:
-            self._revive(nid)
-        if nid is None:
-            lvl = 1 + max(self._lvl[na], self._lvl[nb])
-            nid = self._add_node(_OP_XOR, na << 1, nb << 1, 0, lvl, self._new_slot())
-            self._cse[key] = nid
-            self._pending.append(nid)
-        return (nid << 1) | neg
-
-    def _try_maj(self, u, v):
-        """ref of OR(u, v) as MAJ(x, y, z) when {u, v} = {AND(x, y), AND(XOR(x, y), z)}
-        (reference circuits.py:101-108 builds a full adder's carry this way)."""
-        op, A, B = self._op, self._a, self._b
-        for g, h in ((u, v), (v, u)):
-            if (g | h) & 1:
-                continue
-            G, H = g >> 1, h >> 1
-            if op[G] != _OP_AND or op[H] != _OP_AND:
-                continue
-            x, y = A[G], B[G]
-            pair = {x >> 1, y >> 1}
-            for w, z in ((A[H], B[H]), (B[H], A[H])):
-                W = w >> 1
-                if op[W] == _OP_XOR and {A[W] >> 1, B[W] >> 1} == pair and (w & 1) == ((x ^ y) & 1):
-                    return self._mk_maj(x, y, z)
-        return None
-
-    def _mk_maj(self, x, y, z):
-        """ref of MAJ(x, y, z) (refs with NOT flags) with constant/duplicate elision."""
-        for p, q, r in ((x, y, z), (x, z, y), (y, z, x)):
-            if p == q:
-                return p
-            if p == q ^ 1:
-                return r
-        for p, q, r in ((x, y, z), (y, x, z), (z, x, y)):
-            if (p >> 1) == 0:  # MAJ(0, q, r) = AND(q, r); MAJ(1, q, r) = OR(q, r)
-                return (self._mk_and(q ^ 1, r ^ 1) ^ 1) if p & 1 else self._mk_and(q, r)
-        x, y, z = sorted((x, y, z))
-        key = (_OP_MAJ, x, y, z)
-        nid = self._cse.get(key)
-        if nid is not None and self._dormant and nid in self._dormant:
-            self._revive(nid)
-        if nid is None:
-            lvl = 1 + max(self._lvl[x >> 1], self._lvl[y >> 1], self._lvl[z >> 1])
-            nid = self._add_node(_OP_MAJ, x, y, z, lvl, self._new_slot())
-            self._cse[key] = nid
-            self._pending.append(nid)
-        return nid << 1
-
-    def _mk_xor3(self, p, q, r):
-        """ref of XOR3 of three distinct non-constant nodes."""
-        p, q, r = sorted((p, q, r))
-        key = (_OP_XOR3, p, q, r)
-        nid = self._cse.get(key)
-        if nid is not None and self._dormant and nid in self._dormant:
-            self._revive(nid)
-        if nid is None:
-            lvl = 1 + max(self._lvl[p], self._lvl[q], self._lvl[r])
-            nid = self._add_node(_OP_XOR3, p << 1, q << 1, r << 1, lvl, self._new_slot())
-            self._cse[key] = nid
-            self._pending.append(nid)
-        return nid << 1
-
-    def _mk_mux(self, rs, ra, rb):
-        if rs & 1:  # MUX(~s, a, b) = MUX(s, b, a)
-            rs, ra, rb = rs ^ 1, rb, ra
-        if (rs >> 1) == 0:  # constant selector (only after elision)
-            return ra if rs & 1 else rb
-        if ra == rb:
-            return ra
-        if (ra >> 1) == 0 and (rb >> 1) == 0:  # both constant, a != b
-            return rs if ra & 1 else rs ^ 1
-        if (ra >> 1) == 0:  # s ? 1 : b = s OR b;  s ? 0 : b = ~s AND b
-            return (self._mk_and(rs ^ 1, rb ^ 1) ^ 1) if ra & 1 else self._mk_and(rs ^ 1, rb)
-        if (rb >> 1) == 0:  # s ? a : 1 = ~s OR a;  s ? a : 0 = s AND a
-            return (self._mk_and(rs, ra ^ 1) ^ 1) if rb & 1 else self._mk_and(rs, ra)
-        if ra == rb ^ 1:  # s ? a : ~a = XNOR(s, a)
-            return self._mk_xor(rs, ra) ^ 1
-        if ra == rs:  # s ? s : b = s OR b
-            return self._mk_and(rs ^ 1, rb ^ 1) ^ 1
-        if ra == rs ^ 1:  # s ? ~s : b = ~s AND b
-            return self._mk_and(rs ^ 1, rb)
-        if rb == rs:  # s ? a : s = s AND a
-            return self._mk_and(rs, ra)
-        if rb == rs ^ 1:  # s ? a : ~s = ~s OR a
-            return self._mk_and(rs, ra ^ 1) ^ 1
-        key = (_OP_MUX, rs, ra, rb)
-        nid = self._cse.get(key)
-        if nid is not None and self._dormant and nid in self._dormant:
-            self._revive(nid)
-        if nid is None:
-            lvl = 1 + max(self._lvl[rs >> 1], self._lvl[ra >> 1], self._lvl[rb >> 1])
-            nid = self._add_node(_OP_MUX, rs, ra, rb, lvl, self._new_slot())
-            self._cse[key] = nid
-            self._pending.append(nid)
-        return nid << 1
-
     def _binary_gate(self, kind, a, b):
         """SimContext._binary_gate (backend.py:205-209) on real ciphertexts."""
         if not (isinstance(a, CipherBit) and isinstance(b, CipherBit) and a._ctx is self and b._ctx is self):
@@ -548,18 +350,9 @@ class TfheContext(GateBackend):
             self.global_stats.record(kind, level)
             for scope in self._scopes:
                 scope.record(kind, level)
-            ra, rb = a._value, b._value
-            if kind == AND:
-                r = self._mk_and(ra, rb)
-            elif kind == OR:
-                r = self._mk_and(ra ^ 1, rb ^ 1) ^ 1
-            elif kind == XOR:
-                r = self._mk_xor(ra, rb)
-            else:  # XNOR
-                r = self._mk_xor(ra, rb) ^ 1
-            if self.stream_at and len(self._pending) >= self.stream_at:
+            r = self._dag.gate(_KIND[kind], a._value, b._value)  # counts the handle below
+            if self.stream_at and self._dag.pending_count() >= self.stream_at:
                 self._maybe_stream()
-            self._hcnt[r >> 1] += 1
             return _Bit(self, r, level)
 
     def g_and(self, a, b):
@@ -591,10 +384,10 @@ class TfheContext(GateBackend):
         level = max(s.level, a.level, b.level) + 1
         with self._lock:
             self._record(MUX, level)
-            r = self._mk_mux(s._value, a._value, b._value)
+            r = self._dag.mux(s._value, a._value, b._value)  # counts the handle below
             if self.stream_at:
                 self._maybe_stream()
-            return self._bit(r, level)
+            return _Bit(self, r, level)
 
     # -- scoped stats (backend.py:241-257) --------------------------------------
 
@@ -619,74 +412,20 @@ class TfheContext(GateBackend):
     # -- execution ------------------------------------------------------------------
 
     def pending_count(self):
-        return len(self._pending)
+        return self._dag.pending_count()
 
     def schedule(self):
         """(level, records) batches the next flush would launch."""
         with self._lock:
-            return self._build_schedule(self._live(self._pending))
-
-    def _live(self, pending):
-        """Pending nodes reachable from live handles (through pending operands)."""
-        return self._live_levels(pending) if len(pending) > 2048 else self._live_walk(pending)
-
-    def _live_walk(self, pending):
-        pend = set(pending)
-        hcnt, op, A, B, C = self._hcnt, self._op, self._a, self._b, self._c
-        stack = [n for n in pending if hcnt[n] > 0]
-        need = set()
-        while stack:
-            n = stack.pop()
-            if n in need:
-                continue
-            need.add(n)
-            if op[n] != _OP_INPUT:
-                for r in (A[n], B[n], C[n]):
-                    m = r >> 1
-                    if m in pend and m not in need:
-                        stack.append(m)
-        return [n for n in pending if n in need]
-
-    def _live_levels(self, pending):
-        """_live for large flushes: one numpy sweep per level, deepest first
-        (operands sit at strictly lower levels than their consumers)."""
-        ids = np.asarray(pending, dtype=np.int64)
-        lvl = np.asarray(self._lvl, dtype=np.int64)[ids]
-        pos = np.full(len(self._op), -1, dtype=np.int64)
-        pos[ids] = np.arange(ids.size)
-        opnd = np.stack([np.asarray(self._a, dtype=np.int64)[ids] >> 1, np.asarray(self._b, dtype=np.int64)[ids] >> 1,
-                         np.asarray(self._c, dtype=np.int64)[ids] >> 1], axis=1)
-        opnd[np.asarray(self._op, dtype=np.int8)[ids] == _OP_INPUT] = 0
-        need = np.asarray(self._hcnt, dtype=np.int64)[ids] > 0
-        order = np.argsort(-lvl, kind="stable")
-        bounds = np.flatnonzero(np.diff(lvl[order])) + 1
-        for chunk in np.split(order, bounds):
-            sel = chunk[need[chunk]]
-            if sel.size:
-                q = pos[opnd[sel].reshape(-1)]
-                need[q[q >= 0]] = True
-        return ids[need].tolist()
+            return self._build_schedule(self._dag.live(False))
 
     def _build_schedule(self, pending):
-        if not pending:
+        """Level batches of hb_gate records for node ids `pending` (int64 array)."""
+        ids = np.asarray(pending, dtype=np.int64)
+        if ids.size == 0:
             return []
-        if 8 * len(pending) < len(self._op):
-            # small flush on a large DAG: gather only what the pending nodes touch
-            op = np.fromiter((self._op[i] for i in pending), np.int8, len(pending))
-            a = np.fromiter((self._a[i] for i in pending), np.int64, len(pending))
-            b = np.fromiter((self._b[i] for i in pending), np.int64, len(pending))
-            c = np.fromiter((self._c[i] for i in pending), np.int64, len(pending))
-            lvl = np.fromiter((self._lvl[i] for i in pending), np.int64, len(pending))
-            dst = np.asarray(pending, dtype=np.int64) - 1
-            s_a, s_b, s_c = (a >> 1) - 1, (b >> 1) - 1, (c >> 1) - 1
-        else:
-            ids = np.asarray(pending, dtype=np.int64)
-            op = np.asarray(self._op, dtype=np.int8)[ids]
-            a = np.asarray(self._a, dtype=np.int64)[ids]
-            b = np.asarray(self._b, dtype=np.int64)[ids]
-            c = np.asarray(self._c, dtype=np.int64)[ids]
-            lvl = np.asarray(self._lvl, dtype=np.int64)[ids]
-            dst, s_a, s_b, s_c = ids - 1, (a >> 1) - 1, (b >> 1) - 1, (c >> 1) - 1
+        op, a, b, c, lvl = self._dag.gather(ids)
+        dst, s_a, s_b, s_c = ids - 1, (a >> 1) - 1, (b >> 1) - 1, (c >> 1) - 1
         is_and = op == _OP_AND
         is_xor = op == _OP_XOR
         is_mux = op == _OP_MUX
@@ -727,7 +466,7 @@ class TfheContext(GateBackend):
         """Streaming flush: once `stream_at` gates are pending and the previous
         background batch is done, run them on a background thread while the
         caller keeps building the DAG (device work overlaps host Python)."""
-        if (self.stream_at and len(self._pending) >= self.stream_at
+        if (self.stream_at and self._dag.pending_count() >= self.stream_at
                 and (self._bg is None or not self._bg.is_alive())):
             self._launch(wait=False)
 
@@ -756,18 +495,15 @@ class TfheContext(GateBackend):
         if self._inputs:
             self._upload_inputs(eng, list(self._inputs), [self._inputs[nid] for nid in self._inputs])
             self._inputs.clear()
-        pending = self._live(self._pending)
-        self._dormant.update(set(self._pending).difference(pending))
-        self._pending = []
-        if not pending:
+        pending = self._dag.live(True)  # the rest of the pending gates become dormant
+        if pending.size == 0:
             return
         batches = self._build_schedule(pending)
         self._history.extend(batches)
-        for nid in pending:
-            self._done[nid] = True  # results are read only after _join_bg
+        self._dag.mark_done(pending)  # results are read only after _join_bg
         n_mux = sum(int(np.count_nonzero(r["kind"] == GATE_MUX)) for _, r in batches)
-        self.exec_stats["gates"] += len(pending) * self.lanes
-        self.exec_stats["bootstraps"] += (len(pending) + n_mux) * self.lanes
+        self.exec_stats["gates"] += int(pending.size) * self.lanes
+        self.exec_stats["bootstraps"] += (int(pending.size) + n_mux) * self.lanes
         self.exec_stats["levels"] += len(batches)
         self.exec_stats["flushes"] += 1
         if wait:
@@ -806,10 +542,10 @@ class TfheContext(GateBackend):
         if cts.shape != (len(handles), self.lanes, self.params.n + 1):
             raise ValueError(f"expected [{len(handles)}, {self.lanes}, {self.params.n + 1}] ciphertexts")
         with self._lock:
-            if self._pending:
+            if self._dag.pending_count():
                 self.flush()
             nids = [h._value >> 1 for h in handles]
-            if any(nid == 0 or self._op[nid] != _OP_INPUT for nid in nids) or any(h._value & 1 for h in handles):
+            if any(nid == 0 or self._dag.op(nid) != _OP_INPUT for nid in nids) or any(h._value & 1 for h in handles):
                 raise ValueError("replay inputs must be (non-negated) input handles")
             self._join_bg()
             t0 = time.perf_counter()
@@ -879,9 +615,8 @@ class TfheContext(GateBackend):
                     res[i] = r & 1
             if live:
                 for i in live:
-                    if (refs[i] >> 1) in self._dormant:
-                        self._revive(refs[i] >> 1)
-                if any(not self._done[refs[i] >> 1] for i in live) or self._pending:
+                    self._dag.revive(refs[i] >> 1)
+                if self._dag.pending_count() or any(not self._dag.is_done(refs[i] >> 1) for i in live):
                     self.flush()
                 cts = self._ciphertexts([refs[i] for i in live])
                 bits = self.keys.decrypt(cts.reshape(-1, cts.shape[-1])).reshape(len(live), self.lanes)
@@ -902,9 +637,8 @@ class TfheContext(GateBackend):
         with self._lock:
             if (c._value >> 1) == 0:
                 return None
-            if (c._value >> 1) in self._dormant:
-                self._revive(c._value >> 1)
-            if self._pending:
+            self._dag.revive(c._value >> 1)
+            if self._dag.pending_count():
                 self.flush()
             cts = self._ciphertexts([c._value])[0]
             ph = self.keys.phase(cts).astype(np.int64)

@@ -46,7 +46,33 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+def dag_out():
+    import sysconfig
+
+    return os.path.join(HERE, "_lib", "hb_dag" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_dag(force=False):
+    """The host gate-DAG extension (pybind11, g++): csrc/hb_dag.cpp -> _lib/hb_dag*.so."""
+    import sysconfig
+
+    import pybind11
+
+    out, src = dag_out(), os.path.join(CSRC, "hb_dag.cpp")
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(src),
+                                                                          os.path.getmtime(__file__)):
+        return out
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cxx = shutil.which("g++") or "g++"
+    cmd = [cxx, "-O2", "-std=c++17", "-shared", "-fPIC", "-fvisibility=hidden",
+           "-I", pybind11.get_include(), "-I", sysconfig.get_paths()["include"], src, "-o", out + ".tmp"]
+    subprocess.run(cmd, check=True)
+    os.replace(out + ".tmp", out)
+    return out
+
+
 def build(force=False, verbose=False):
+    build_dag(force)
     if not force and not _stale():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)

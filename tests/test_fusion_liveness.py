@@ -86,16 +86,31 @@ def test_stats_and_values_match_simcontext_on_adder_trees():
         assert outs[0][0] == sum(vals)
 
 
-def test_vectorised_live_filter_matches_traversal():
-    ctx = Ctx(seed=11)
+def test_native_live_filter_matches_python_walk():
+    """The native DAG's live-gate filter (hb_dag.cpp) equals a plain graph walk
+    from the nodes holding live handles through pending operands."""
+    ctx = Ctx(seed=11, stream_at=0)
     rng = np.random.default_rng(3)
-    bits = [ctx.encrypt(int(v)) for v in rng.integers(0, 2, 700)]
+    bits = [ctx.encrypt(int(v)) for v in rng.integers(0, 2, 300)]
     w = reduce_tree_sum(bits)
     keep = [w.bits[-1], ctx.g_and(bits[0], bits[1])]
     del w
-    pending = list(ctx._pending)
-    assert len(pending) > 2048
-    assert sorted(ctx._live_levels(pending)) == sorted(ctx._live_walk(pending))
+    dag = ctx._dag
+    pend = dag.pending()
+    op, a, b, c, _ = dag.gather(pend)
+    fields = {int(n): (int(o), int(x) >> 1, int(y) >> 1, int(z) >> 1) for n, o, x, y, z in zip(pend, op, a, b, c)}
+    stack = [n for n in fields if dag.hcount(n) > 0]
+    need = set()
+    while stack:
+        n = stack.pop()
+        if n in need:
+            continue
+        need.add(n)
+        for m in fields[n][1:]:
+            if m in fields and m not in need:
+                stack.append(m)
+    assert sorted(dag.live(False).tolist()) == sorted(need)
+    assert 0 < len(need) < len(fields)
     assert keep
 
 

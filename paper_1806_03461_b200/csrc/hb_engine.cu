@@ -1349,7 +1349,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) k_blind_rota
     cg::cluster_group cluster = cg::this_cluster();
     const int q = (int)cluster.block_rank();   // TRLWE polynomial owned by this CTA
     BrCluSmemU2 &peer = *cluster.map_shared_rank(&sm, q ^ 1);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
     const int grp = warp >> 1;
     const int t = threadIdx.x & 63;
     const int bar_id = 1 + grp;

@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import re
 import os
 import statistics
 import subprocess
@@ -372,7 +373,10 @@ def last_profiled_traffic(kernel="k_blind_rotate"):
     (written by scripts/ncu_summary.py from an `ncu --set full` capture)."""
     base = os.path.join(ROOT, "profiles")
     best = None
-    for d in sorted(os.listdir(base)) if os.path.isdir(base) else []:
+    def natural(name):  # r01_v11 after r01_v8
+        return [int(t) if t.isdigit() else t for t in re.split(r"(\d+)", name)]
+
+    for d in sorted(os.listdir(base), key=natural) if os.path.isdir(base) else []:
         f = os.path.join(base, d, "traffic.json")
         if os.path.exists(f):
             best = f

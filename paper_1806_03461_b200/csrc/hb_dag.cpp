@@ -52,6 +52,8 @@ class Dag {
 
     // ref of a 2-input gate of the reference API; one live handle is counted on it
     int64_t gate(int kind, int64_t ra, int64_t rb) {
+        check_ref(ra);
+        check_ref(rb);
         int64_t r;
         switch (kind) {
             case K_AND: r = mk_and(ra, rb); break;
@@ -63,21 +65,24 @@ class Dag {
         return r;
     }
     int64_t mux(int64_t rs, int64_t ra, int64_t rb) {
+        check_ref(rs);
+        check_ref(ra);
+        check_ref(rb);
         const int64_t r = mk_mux(rs, ra, rb);
         hcnt_[r >> 1]++;
         return r;
     }
 
-    void hinc(int64_t n) { hcnt_[n]++; }
-    void hdec(int64_t n) { hcnt_[n]--; }
-    int32_t hcount(int64_t n) const { return hcnt_[n]; }
-    int op(int64_t n) const { return op_[n]; }
-    bool is_done(int64_t n) const { return state_[n] == DONE; }
-    bool is_dormant(int64_t n) const { return state_[n] == DORMANT; }
+    void hinc(int64_t n) { hcnt_[check(n)]++; }
+    void hdec(int64_t n) { hcnt_[check(n)]--; }
+    int32_t hcount(int64_t n) const { return hcnt_[check(n)]; }
+    int op(int64_t n) const { return op_[check(n)]; }
+    bool is_done(int64_t n) const { return state_[check(n)] == DONE; }
+    bool is_dormant(int64_t n) const { return state_[check(n)] == DORMANT; }
 
     // dormant node (and its dormant operands) back to pending
     void revive(int64_t n) {
-        std::vector<int64_t> stack{n};
+        std::vector<int64_t> stack{check(n)};
         while (!stack.empty()) {
             const int64_t m = stack.back();
             stack.pop_back();
@@ -125,7 +130,7 @@ class Dag {
 
     void mark_done(py::array_t<int64_t, py::array::c_style | py::array::forcecast> ids) {
         auto v = ids.unchecked<1>();
-        for (py::ssize_t i = 0; i < v.shape(0); i++) state_[v(i)] = DONE;
+        for (py::ssize_t i = 0; i < v.shape(0); i++) state_[check(v(i))] = DONE;
     }
 
     // node fields of ids: (op int8, a, b, c int64 refs, lvl int64)
@@ -138,7 +143,7 @@ class Dag {
         auto A = a.mutable_unchecked<1>(), B = b.mutable_unchecked<1>(), C = c.mutable_unchecked<1>();
         auto L = l.mutable_unchecked<1>();
         for (py::ssize_t i = 0; i < n; i++) {
-            const int64_t k = v(i);
+            const int64_t k = check(v(i));
             O(i) = op_[k];
             A(i) = a_[k];
             B(i) = b_[k];
@@ -158,6 +163,12 @@ class Dag {
     std::vector<uint32_t> mark_;
     uint32_t epoch_ = 0;
     std::unordered_map<Key, int64_t, KeyHash> cse_;
+
+    int64_t check(int64_t n) const {
+        if (n < 0 || n >= (int64_t)op_.size()) throw py::index_error("gate DAG: node id out of range");
+        return n;
+    }
+    void check_ref(int64_t r) const { check(r >> 1); }
 
     static py::array_t<int64_t> to_array(const std::vector<int64_t> &v) {
         py::array_t<int64_t> out((py::ssize_t)v.size());

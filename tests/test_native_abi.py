@@ -86,3 +86,15 @@ def test_engine_without_gpu_is_a_device_error(keys):
         pytest.skip("a GPU is present")
     with pytest.raises(_native.DeviceError):
         tfhe.Engine(keys, device=0)
+
+
+def test_gate_dag_rejects_foreign_node_ids():
+    """The native gate DAG raises IndexError (never crashes) on ids it does not own."""
+    import pytest as _pytest
+
+    d = _native.dag_module().Dag()
+    n = d.add_input()
+    assert d.gate(0, n << 1, 1) == n << 1  # AND(x, true) = x, no node
+    for call in (lambda: d.revive(n + 5), lambda: d.gate(0, (n + 5) << 1, 2), lambda: d.hinc(-1)):
+        with _pytest.raises(IndexError):
+            call()

@@ -450,6 +450,48 @@ struct BrArgs {
     unsigned long long *margin;  // if set: max |v - round(v)| as double bits
 };
 
+// K1: linear combination (0, c0) + alpha A + beta B (+ gamma C) of work item e's
+// gate inputs and modulus switch of its n+1 coefficients to Z_2N (bar[0..n]);
+// threads tid = 0..nthreads-1 of the caller share the loop.
+__device__ __forceinline__ void k1_modswitch(const BrArgs &args, uint32_t e, uint16_t *bar, int tid, int nthreads) {
+    const int n = args.n;
+    const uint32_t lanes = args.lanes;
+    const BrItem it = args.items[e / lanes];
+    const uint32_t lane_id = e % lanes;
+    const int alpha = (int8_t)(it.coef & 0xFF), beta = (int8_t)((it.coef >> 8) & 0xFF);
+    const int gamma = (int8_t)((it.coef >> 16) & 0xFF);
+    const uint32_t *A = args.pool + ((size_t)it.src_a * lanes + lane_id) * args.pool_stride;
+    const uint32_t *B = args.pool + ((size_t)it.src_b * lanes + lane_id) * args.pool_stride;
+    const uint32_t *C = args.pool + ((size_t)it.src_c * lanes + lane_id) * args.pool_stride;
+    for (int c = tid; c <= n; c += nthreads) {
+        uint32_t v = (uint32_t)alpha * __ldg(&A[c]);
+        if (beta) v += (uint32_t)beta * __ldg(&B[c]);
+        if (gamma) v += (uint32_t)gamma * __ldg(&C[c]);
+        if (c == n) v += it.c0;
+        bar[c] = (uint16_t)(((v + (1u << 20)) >> 21) & (2 * kN - 1));
+    }
+}
+
+// ACC = X^{-barb} (0, mu...mu): the A polynomial zero, B the rotated test vector
+__device__ __forceinline__ void acc_init(uint32_t *accA, uint32_t *accB, int barb, uint32_t mu, int tid, int nthreads) {
+    for (int i = tid; i < kN; i += nthreads) {
+        if (accA) accA[i] = 0;
+        if (accB) accB[i] = (((i + barb) & kN) ? 0u - mu : mu);
+    }
+}
+
+// K3: sample extraction at index 0 of (A, B) into the big-LWE scratch row
+__device__ __forceinline__ void sample_extract(const uint32_t *accA, const uint32_t *accB, uint32_t *out, int tid,
+                                               int nthreads) {
+    for (int c = tid; c <= kN; c += nthreads) {
+        uint32_t v;
+        if (c == 0) v = accA[0];
+        else if (c < kN) v = 0u - accA[kN - c];
+        else v = accB[0];
+        out[c] = v;
+    }
+}
+
 constexpr int kStages = 3;  // BK rows in the shared-memory ring
 #ifndef HB_PAIR_UNROLL
 #define HB_PAIR_UNROLL 3  // fully unrolled pair loop: rows (q, p) become compile-time
@@ -520,33 +562,9 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
     double2 *xch = &sm.xch[g][0][0][0];
     uint16_t *bar = sm.bar[g];
 
-    // K1: linear combination of the gate inputs + modulus switch to Z_2N
-    {
-        const uint32_t lanes = args.lanes;
-        const BrItem it = args.items[e / lanes];
-        const uint32_t lane_id = e % lanes;
-        const int alpha = (int8_t)(it.coef & 0xFF), beta = (int8_t)((it.coef >> 8) & 0xFF);
-        const int gamma = (int8_t)((it.coef >> 16) & 0xFF);
-        const uint32_t *A = args.pool + ((size_t)it.src_a * lanes + lane_id) * args.pool_stride;
-        const uint32_t *B = args.pool + ((size_t)it.src_b * lanes + lane_id) * args.pool_stride;
-        const uint32_t *C = args.pool + ((size_t)it.src_c * lanes + lane_id) * args.pool_stride;
-        for (int c = t; c <= n; c += 64) {
-            uint32_t v = (uint32_t)alpha * __ldg(&A[c]);
-            if (beta) v += (uint32_t)beta * __ldg(&B[c]);
-            if (gamma) v += (uint32_t)gamma * __ldg(&C[c]);
-            if (c == n) v += it.c0;
-            bar[c] = (uint16_t)(((v + (1u << 20)) >> 21) & (2 * kN - 1));
-        }
-    }
+    k1_modswitch(args, e, bar, t, 64);  // K1
     group_bar(bar_id);
-    // ACC = X^{-barb} * (0, mu...mu)
-    {
-        const int barb = bar[n];
-        for (int i = t; i < kN; i += 64) {
-            accA[i] = 0;
-            accB[i] = (((i + barb) & kN) ? 0u - args.mu : args.mu);
-        }
-    }
+    acc_init(accA, accB, bar[n], args.mu, t, 64);  // ACC = X^{-barb} (0, mu...mu)
     group_bar(bar_id);
 
     double max_err = 0.0;
@@ -688,14 +706,7 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
         for (int c = t; c < 2 * kN; c += 64) dst[c] = (c < kN) ? accA[c] : accB[c - kN];
     }
     // K3: sample extract at index 0
-    uint32_t *out = args.big + (size_t)e * kBigStride;
-    for (int c = t; c <= kN; c += 64) {
-        uint32_t v;
-        if (c == 0) v = accA[0];
-        else if (c < kN) v = 0u - accA[kN - c];
-        else v = accB[0];
-        out[c] = v;
-    }
+    sample_extract(accA, accB, args.big + (size_t)e * kBigStride, t, 64);
 }
 
 // ---------------------------------------------------------------------------
@@ -751,31 +762,9 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_lat(const BrArgs args) 
             bulk_g2s(sm.bk[grp], bk_src + (size_t)(2 * grp) * kRowBytes, 2 * kRowBytes, &sm.full[grp]);
         }
     }
-    {   // K1: linear combination + modulus switch (all 192 threads)
-        const uint32_t lanes = args.lanes;
-        const BrItem it = args.items[e / lanes];
-        const uint32_t lane_id = e % lanes;
-        const int alpha = (int8_t)(it.coef & 0xFF), beta = (int8_t)((it.coef >> 8) & 0xFF);
-        const int gamma = (int8_t)((it.coef >> 16) & 0xFF);
-        const uint32_t *A = args.pool + ((size_t)it.src_a * lanes + lane_id) * args.pool_stride;
-        const uint32_t *B = args.pool + ((size_t)it.src_b * lanes + lane_id) * args.pool_stride;
-        const uint32_t *C = args.pool + ((size_t)it.src_c * lanes + lane_id) * args.pool_stride;
-        for (int c = threadIdx.x; c <= n; c += 192) {
-            uint32_t v = (uint32_t)alpha * __ldg(&A[c]);
-            if (beta) v += (uint32_t)beta * __ldg(&B[c]);
-            if (gamma) v += (uint32_t)gamma * __ldg(&C[c]);
-            if (c == n) v += it.c0;
-            sm.bar[c] = (uint16_t)(((v + (1u << 20)) >> 21) & (2 * kN - 1));
-        }
-    }
+    k1_modswitch(args, e, sm.bar, threadIdx.x, 192);  // K1
     __syncthreads();
-    {
-        const int barb = sm.bar[n];
-        for (int i = threadIdx.x; i < kN; i += 192) {
-            accA[i] = 0;
-            accB[i] = (((i + barb) & kN) ? 0u - args.mu : args.mu);
-        }
-    }
+    acc_init(accA, accB, sm.bar[n], args.mu, threadIdx.x, 192);  // ACC = X^{-barb} (0, mu...mu)
     __syncthreads();
 
     double max_err = 0.0;
@@ -853,14 +842,7 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_lat(const BrArgs args) 
         uint32_t *dst = args.acc_dump + (size_t)e * 2 * kN;
         for (int c = threadIdx.x; c < 2 * kN; c += 192) dst[c] = (c < kN) ? accA[c] : accB[c - kN];
     }
-    uint32_t *out = args.big + (size_t)e * kBigStride;
-    for (int c = threadIdx.x; c <= kN; c += 192) {
-        uint32_t v;
-        if (c == 0) v = accA[0];
-        else if (c < kN) v = 0u - accA[kN - c];
-        else v = accB[0];
-        out[c] = v;
-    }
+    sample_extract(accA, accB, args.big + (size_t)e * kBigStride, threadIdx.x, 192);
 }
 
 // ---------------------------------------------------------------------------
@@ -951,31 +933,9 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate_u2(const BrArgs args
     double2 *xch = &sm.xch[g][0][0];
     uint16_t *bar = sm.bar[g];
 
-    {   // K1: linear combination + modulus switch
-        const uint32_t lanes = args.lanes;
-        const BrItem it = args.items[e / lanes];
-        const uint32_t lane_id = e % lanes;
-        const int alpha = (int8_t)(it.coef & 0xFF), beta = (int8_t)((it.coef >> 8) & 0xFF);
-        const int gamma = (int8_t)((it.coef >> 16) & 0xFF);
-        const uint32_t *A = args.pool + ((size_t)it.src_a * lanes + lane_id) * args.pool_stride;
-        const uint32_t *B = args.pool + ((size_t)it.src_b * lanes + lane_id) * args.pool_stride;
-        const uint32_t *C = args.pool + ((size_t)it.src_c * lanes + lane_id) * args.pool_stride;
-        for (int c = t; c <= n; c += 64) {
-            uint32_t v = (uint32_t)alpha * __ldg(&A[c]);
-            if (beta) v += (uint32_t)beta * __ldg(&B[c]);
-            if (gamma) v += (uint32_t)gamma * __ldg(&C[c]);
-            if (c == n) v += it.c0;
-            bar[c] = (uint16_t)(((v + (1u << 20)) >> 21) & (2 * kN - 1));
-        }
-    }
+    k1_modswitch(args, e, bar, t, 64);  // K1
     group_bar(bar_id);
-    {
-        const int barb = bar[n];
-        for (int i = t; i < kN; i += 64) {
-            accA[i] = 0;
-            accB[i] = (((i + barb) & kN) ? 0u - args.mu : args.mu);
-        }
-    }
+    acc_init(accA, accB, bar[n], args.mu, t, 64);  // ACC = X^{-barb} (0, mu...mu)
     group_bar(bar_id);
 
     double max_err = 0.0;
@@ -1091,14 +1051,7 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate_u2(const BrArgs args
         uint32_t *dst = args.acc_dump + (size_t)e * 2 * kN;
         for (int c = t; c < 2 * kN; c += 64) dst[c] = (c < kN) ? accA[c] : accB[c - kN];
     }
-    uint32_t *out = args.big + (size_t)e * kBigStride;
-    for (int c = t; c <= kN; c += 64) {
-        uint32_t v;
-        if (c == 0) v = accA[0];
-        else if (c < kN) v = 0u - accA[kN - c];
-        else v = accB[0];
-        out[c] = v;
-    }
+    sample_extract(accA, accB, args.big + (size_t)e * kBigStride, t, 64);
 }
 
 // ---------------------------------------------------------------------------
@@ -1163,31 +1116,9 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_u2_lat(const BrArgs arg
             bulk_g2s(sm.bk[grp][issued], stage_src(issued), kRowBytes, &full[issued]);
         }
     }
-    {   // K1: linear combination + modulus switch (all 192 threads)
-        const uint32_t lanes = args.lanes;
-        const BrItem it = args.items[e / lanes];
-        const uint32_t lane_id = e % lanes;
-        const int alpha = (int8_t)(it.coef & 0xFF), beta = (int8_t)((it.coef >> 8) & 0xFF);
-        const int gamma = (int8_t)((it.coef >> 16) & 0xFF);
-        const uint32_t *A = args.pool + ((size_t)it.src_a * lanes + lane_id) * args.pool_stride;
-        const uint32_t *B = args.pool + ((size_t)it.src_b * lanes + lane_id) * args.pool_stride;
-        const uint32_t *C = args.pool + ((size_t)it.src_c * lanes + lane_id) * args.pool_stride;
-        for (int c = threadIdx.x; c <= n; c += 192) {
-            uint32_t v = (uint32_t)alpha * __ldg(&A[c]);
-            if (beta) v += (uint32_t)beta * __ldg(&B[c]);
-            if (gamma) v += (uint32_t)gamma * __ldg(&C[c]);
-            if (c == n) v += it.c0;
-            sm.bar[c] = (uint16_t)(((v + (1u << 20)) >> 21) & (2 * kN - 1));
-        }
-    }
+    k1_modswitch(args, e, sm.bar, threadIdx.x, 192);  // K1
     __syncthreads();
-    {
-        const int barb = sm.bar[n];
-        for (int i = threadIdx.x; i < kN; i += 192) {
-            accA[i] = 0;
-            accB[i] = (((i + barb) & kN) ? 0u - args.mu : args.mu);
-        }
-    }
+    acc_init(accA, accB, sm.bar[n], args.mu, threadIdx.x, 192);  // ACC = X^{-barb} (0, mu...mu)
     __syncthreads();
 
     double max_err = 0.0;
@@ -1298,14 +1229,7 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_u2_lat(const BrArgs arg
         uint32_t *dst = args.acc_dump + (size_t)e * 2 * kN;
         for (int c = threadIdx.x; c < 2 * kN; c += 192) dst[c] = (c < kN) ? accA[c] : accB[c - kN];
     }
-    uint32_t *out = args.big + (size_t)e * kBigStride;
-    for (int c = threadIdx.x; c <= kN; c += 192) {
-        uint32_t v;
-        if (c == 0) v = accA[0];
-        else if (c < kN) v = 0u - accA[kN - c];
-        else v = accB[0];
-        out[c] = v;
-    }
+    sample_extract(accA, accB, args.big + (size_t)e * kBigStride, threadIdx.x, 192);
 }
 
 // ---------------------------------------------------------------------------
@@ -1383,29 +1307,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) k_blind_rota
             }
         }
     }
-    {   // K1: linear combination + modulus switch (both CTAs)
-        const uint32_t lanes = args.lanes;
-        const BrItem it = args.items[e / lanes];
-        const uint32_t lane_id = e % lanes;
-        const int alpha = (int8_t)(it.coef & 0xFF), beta = (int8_t)((it.coef >> 8) & 0xFF);
-        const int gamma = (int8_t)((it.coef >> 16) & 0xFF);
-        const uint32_t *A = args.pool + ((size_t)it.src_a * lanes + lane_id) * args.pool_stride;
-        const uint32_t *B = args.pool + ((size_t)it.src_b * lanes + lane_id) * args.pool_stride;
-        const uint32_t *C = args.pool + ((size_t)it.src_c * lanes + lane_id) * args.pool_stride;
-        for (int c = threadIdx.x; c <= n; c += 192) {
-            uint32_t v = (uint32_t)alpha * __ldg(&A[c]);
-            if (beta) v += (uint32_t)beta * __ldg(&B[c]);
-            if (gamma) v += (uint32_t)gamma * __ldg(&C[c]);
-            if (c == n) v += it.c0;
-            sm.bar[c] = (uint16_t)(((v + (1u << 20)) >> 21) & (2 * kN - 1));
-        }
-    }
+    k1_modswitch(args, e, sm.bar, threadIdx.x, 192);  // K1
     __syncthreads();
-    {
-        const int barb = sm.bar[n];
-        for (int i = threadIdx.x; i < kN; i += 192)
-            sm.acc[i] = q == 0 ? 0u : (((i + barb) & kN) ? 0u - args.mu : args.mu);
-    }
+    acc_init(q == 0 ? sm.acc : nullptr, q == 0 ? nullptr : sm.acc, sm.bar[n], args.mu, threadIdx.x, 192);  // ACC_q
     cluster.sync();  // peer smem live (DSMEM), ACC initialised
 
     double max_err = 0.0;

@@ -396,6 +396,8 @@ def run_ours(args, dist):
         raise SystemExit("bench.py: no CUDA device (the engine has no CPU fallback)")
     dev = dist.local_rank
     keys = tfhe.KeySet(seed=args.seed)
+    from paper_1806_03461_b200 import backend as _backend
+    _backend._KEY_CACHE.setdefault(args.seed, keys)  # the BNN leg's contexts reuse these keys
     eng = tfhe.Engine(keys, device=dev)
     n = args.gates
     rng = np.random.default_rng(1000 + dist.rank)

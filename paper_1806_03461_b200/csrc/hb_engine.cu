@@ -878,20 +878,23 @@ __constant__ double2 c_w8[8] = {{1.0, 0.0},
                                 {0.0, -1.0},
                                 {0.70710678118654752440, -0.70710678118654752440}};
 
-template <int G>
+template <int G, int R = kStagesU2>
 struct BrSmemU2 {
-    double2 bk[kStagesU2][2 * kNH];          // stage ring: [output poly][bin]
-    uint64_t full[kStagesU2], empty[kStagesU2];
+    double2 bk[R][2 * kNH];                  // stage ring: [output poly][bin]
+    uint64_t full[R], empty[R];
     uint32_t acc[G][2][kN];
     double2 xch[G][2][kXchStride];           // single-buffered dual-FFT exchange
     uint16_t bar[G][kMaxLweN + 1];
     TwSeeds tws[64];
 };
 
-template <int G, bool kDebug>
-__global__ void __launch_bounds__(64 * G, 1) k_blind_rotate_u2(const BrArgs args) {
+// R: ring stages; MB: resident CTAs per SM the launch bounds target.  A ring
+// shallower than one row pair (R < 7) is refilled after every consumed stage.
+template <int G, bool kDebug, int R = kStagesU2, int MB = 1>
+__global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs args) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    BrSmemU2<G> &sm = *reinterpret_cast<BrSmemU2<G> *>(smem_raw);
+    BrSmemU2<G, R> &sm = *reinterpret_cast<BrSmemU2<G, R> *>(smem_raw);
+    constexpr bool kMidIssue = R < kRows + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = args.n;
     const int pairs = min(n, args.iters) / 2;
@@ -910,12 +913,12 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate_u2(const BrArgs args
     }
     int issued = 0;  // producer (thread 0) state: stages issued so far
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStagesU2; s++) {
+        for (int s = 0; s < R; s++) {
             mbar_init(&sm.full[s], 1);
             mbar_init(&sm.empty[s], 2 * G);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (; issued < kStagesU2 && issued < stages_needed; issued++) {
+        for (; issued < R && issued < stages_needed; issued++) {
             mbar_arrive_expect_tx(&sm.full[issued], kRowBytes);
             bulk_g2s(sm.bk[issued], bk_src + u2_stage(issued) * kRowBytes, kRowBytes, &sm.full[issued]);
         }
@@ -954,12 +957,12 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate_u2(const BrArgs args
         double2 f0[8], f1[8];
 #pragma unroll 1
         for (int rp = 0; rp < kRows / 2; rp++) {
-            // producer: refill the ring up to kStagesU2 stages ahead of this row pair
+            // producer: refill the ring up to R stages ahead of this row pair
             if (threadIdx.x == 0) {
 #pragma unroll 1
-                for (; issued < st + kStagesU2 && issued < stages_needed; issued++) {
-                    const int s2 = issued % kStagesU2;
-                    mbar_wait(&sm.empty[s2], ((issued / kStagesU2) - 1) & 1);
+                for (; issued < st + R && issued < stages_needed; issued++) {
+                    const int s2 = issued % R;
+                    mbar_wait(&sm.empty[s2], ((issued / R) - 1) & 1);
                     mbar_arrive_expect_tx(&sm.full[s2], kRowBytes);
                     bulk_g2s(sm.bk[s2], bk_src + u2_stage(issued) * kRowBytes, kRowBytes, &sm.full[s2]);
                 }
@@ -998,8 +1001,8 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate_u2(const BrArgs args
                 }
 #pragma unroll
                 for (int h = 0; h < 2; h++, st++) {
-                    const int s = st % kStagesU2;
-                    mbar_wait(&sm.full[s], (st / kStagesU2) & 1);
+                    const int s = st % R;
+                    mbar_wait(&sm.full[s], (st / R) & 1);
                     const double2 *bk0 = sm.bk[s];
                     const double2 *bk1 = sm.bk[s] + kNH;
 #pragma unroll
@@ -1015,6 +1018,16 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate_u2(const BrArgs args
                     }
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&sm.empty[s]);
+                    if (kMidIssue && threadIdx.x == 0) {  // shallow ring: refill behind consumption
+#pragma unroll 1
+                        for (; issued < st + 1 + R && issued < stages_needed; issued++) {
+                            const int s2 = issued % R;
+                            mbar_wait(&sm.empty[s2], ((issued / R) - 1) & 1);
+                            mbar_arrive_expect_tx(&sm.full[s2], kRowBytes);
+                            bulk_g2s(sm.bk[s2], bk_src + u2_stage(issued) * kRowBytes, kRowBytes, &sm.full[s2]);
+                        }
+                    }
+                    __syncwarp();
                 }
             }
         }
@@ -1714,10 +1727,10 @@ int launch_br(hb_engine *e, const BrArgs &a) {
     return HB_OK;
 }
 
-template <int G, bool kDebug>
+template <int G, bool kDebug, int R = kStagesU2, int MB = 1>
 int launch_br_u2(hb_engine *e, const BrArgs &a) {
     const unsigned grid = (a.n_work + G - 1) / G;
-    k_blind_rotate_u2<G, kDebug><<<grid, 64 * G, sizeof(BrSmemU2<G>), e->stream>>>(a);
+    k_blind_rotate_u2<G, kDebug, R, MB><<<grid, 64 * G, sizeof(BrSmemU2<G, R>), e->stream>>>(a);
     HB_CUDA_TRY(cudaGetLastError());
     e->n_launch++;
     return HB_OK;
@@ -1738,6 +1751,14 @@ int launch_ks(hb_engine *e, const KsArgs &a) {
     e->n_launch++;
     return HB_OK;
 }
+
+#ifndef HB_U2_PAIRED
+#define HB_U2_PAIRED 0  // experiment: wide levels as two independent 2-gate CTAs per SM
+#endif
+#ifndef HB_PAIRED_RING
+#define HB_PAIRED_RING 3
+#endif
+constexpr int kPairedRing = HB_PAIRED_RING;
 
 // Blind-rotation launch for a level of a.n_work bootstraps: narrow levels
 // (latency-bound) get one bootstrap per CTA split over three thread groups
@@ -1762,6 +1783,9 @@ int launch_br_auto(hb_engine *e, const BrArgs &a, int force_g = 0) {
         }
         if (gsel == 1) return launch_br_u2<1, kDebug>(e, a);
         if (gsel == 2) return launch_br_u2<2, kDebug>(e, a);
+#if HB_U2_PAIRED
+        if (!force_g) return launch_br_u2<2, kDebug, kPairedRing, 2>(e, a);  // two 2-gate CTAs per SM
+#endif
         return launch_br_u2<kBrGates, kDebug>(e, a);
     }
     if (!force_g && gsel == 1 && e->latency_mode) return launch_br_lat<kDebug>(e, a);
@@ -1861,6 +1885,11 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
                                      (int)br_smem_bytes<1>()));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)br_smem_bytes<kBrGates>()));
+#if HB_U2_PAIRED
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<2, false, kPairedRing, 2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrSmemU2<2, kPairedRing>)));
+#endif
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(BrSmemU2<kBrGates>)));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

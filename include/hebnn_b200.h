@@ -86,14 +86,16 @@ int hb_abi_version(void);
 const char *hb_last_error(void);
 void hb_default_params(hb_params *p);
 size_t hb_lwe_words(const hb_params *p);   /* n + 1 */
-size_t hb_bk_words(const hb_params *p);    /* n * (k+1)l * (k+1) * N */
+size_t hb_bk_words(const hb_params *p);    /* T * (k+1)l * (k+1) * N, T = n (bk_unroll 1) or 3n/2 (2) */
 size_t hb_ksk_words(const hb_params *p);   /* kN * t * (base-1) * (n+1) */
 
 /* ---- host key material / encryption (replaces SimContext plaintext store) ---- */
 
 /* Deterministic keygen from `seed` (ChaCha20 streams).
- * lwe_key[n], trlwe_key[k*N] (bits as u32), bk[n][(k+1)l][k+1][N] (coefficient
- * domain), ksk[kN][t][base-1][n+1]. threads <= 0 selects all host cores. */
+ * lwe_key[n], trlwe_key[k*N] (bits as u32), bk[T][(k+1)l][k+1][N] (coefficient
+ * domain; T = n TGSW(s_i) for bk_unroll 1, T = 3n/2 for key pairs: TGSW(s_i s_j),
+ * TGSW(s_i (1-s_j)), TGSW((1-s_i) s_j) per pair), ksk[kN][t][base-1][n+1].
+ * threads <= 0 selects all host cores. */
 int hb_keygen(const hb_params *p, uint64_t seed, uint32_t *lwe_key, uint32_t *trlwe_key,
               uint32_t *bk, uint32_t *ksk, int threads);
 
@@ -167,8 +169,8 @@ int hb_measure_fp64_peak(hb_engine *e, double *tflops);
 
 /* ---- stage entry points for bit-level parity (synchronous, host buffers) ---- */
 
-/* ACC after the first `iters` CMux steps of the blind rotation of lwe[n+1]
- * with test vector mu: acc_out[(k+1)N]. */
+/* ACC after the first `iters` key bits of the blind rotation of lwe[n+1]
+ * (key pairs: iters/2 pair steps) with test vector mu: acc_out[(k+1)N]. */
 int hb_debug_blind_rotate(hb_engine *e, const uint32_t *lwe, uint32_t mu, int32_t iters,
                           uint32_t *acc_out);
 /* count independent bootstraps without key switch: lin[count][n+1] -> out[count][kN+1] */
@@ -180,7 +182,8 @@ int hb_debug_keyswitch(hb_engine *e, const uint32_t *in, size_t count, uint32_t 
 int hb_debug_fft_margin(hb_engine *e, double *max_err);
 /* which = 0: forward negacyclic FFT (scaled by 1/512) of count u32 polynomials
  * polys[count][N] -> out[count][N/2][2]; which = 1: copy the first `count`
- * polynomials of the device BK Fourier table (polys ignored). */
+ * polynomials of the device BK Fourier table (polys ignored; key pairs store
+ * it in ring-stage order). */
 int hb_debug_fourier(hb_engine *e, const uint32_t *polys, size_t count, double *out, int which);
 
 #ifdef __cplusplus

@@ -846,6 +846,35 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_lat(const BrArgs args) 
 }
 
 // ---------------------------------------------------------------------------
+// Tensor memory (TMEM) as per-thread private storage: each thread of a warp
+// owns one TMEM lane (warp w -> lanes 32 (w % 4) ..); 32x32b loads / stores
+// move 32 consecutive 32-bit columns of that lane to / from registers.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};"
+                 :: "r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+                 : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// one warp allocates `cols` columns (power of two >= 32) and publishes the base
+__device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem, uint32_t cols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_addr(dst_smem)), "r"(cols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t base, uint32_t cols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(base), "r"(cols) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
 // K1+K2+K3 with the key-pair bootstrapping key (bk_unroll 2).  One external
 // product per key pair (i, j) = (2m, 2m+1):
 //   ACC <- ACC + BK_m [x] ACC,  BK_m = sum_c (X^{e_c} - 1) BK_{m,c},
@@ -878,23 +907,29 @@ __constant__ double2 c_w8[8] = {{1.0, 0.0},
                                 {0.0, -1.0},
                                 {0.70710678118654752440, -0.70710678118654752440}};
 
-template <int G, int R = kStagesU2>
+template <int G, int R = kStagesU2, bool TM = false>
 struct BrSmemU2 {
     double2 bk[R][2 * kNH];                  // stage ring: [output poly][bin]
     uint64_t full[R], empty[R];
-    uint32_t acc[G][2][kN];
+    uint32_t acc[TM ? 1 : G][2][TM ? 1 : kN];  // TRLWE accumulators (TM: in tensor memory instead)
     double2 xch[G][2][kXchStride];           // single-buffered dual-FFT exchange
     uint16_t bar[G][kMaxLweN + 1];
     TwSeeds tws[64];
+    uint32_t tmem_base;
 };
 
 // R: ring stages; MB: resident CTAs per SM the launch bounds target.  A ring
 // shallower than one row pair (R < 7) is refilled after every consumed stage.
-template <int G, bool kDebug, int R = kStagesU2, int MB = 1>
+// TM: the accumulators live in tensor memory.  In this kernel every thread
+// reads and updates only its own ACC coefficients (bins t + 64 m of both
+// polynomials, no rotation), so ACC is thread-private: 32 TMEM columns of the
+// thread's lane, and the 32 KiB of shared memory go to the BK ring.
+template <int G, bool kDebug, int R = kStagesU2, int MB = 1, bool TM = false>
 __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs args) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    BrSmemU2<G, R> &sm = *reinterpret_cast<BrSmemU2<G, R> *>(smem_raw);
+    BrSmemU2<G, R, TM> &sm = *reinterpret_cast<BrSmemU2<G, R, TM> *>(smem_raw);
     constexpr bool kMidIssue = R < kRows + 1;
+    constexpr uint32_t kTmemCols = G > 2 ? 64 : 32;  // warps w and w + 4 share a lane quarter
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = args.n;
     const int pairs = min(n, args.iters) / 2;
@@ -923,7 +958,12 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
             bulk_g2s(sm.bk[issued], bk_src + u2_stage(issued) * kRowBytes, kRowBytes, &sm.full[issued]);
         }
     }
+    if (TM && warp == 0) tmem_alloc(&sm.tmem_base, kTmemCols);
+    if (TM) tmem_fence_before();
     __syncthreads();
+    if (TM) tmem_fence_after();
+    // this thread's 32 ACC columns: A at +0..15, B at +16..31 (lo bins m, then hi bins m)
+    const uint32_t tacc = TM ? sm.tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + 32u * (uint32_t)(warp >> 2) : 0u;
 
     const int g = warp >> 1;
     const int t = threadIdx.x & 63;
@@ -931,15 +971,29 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
     const uint32_t e_raw = blockIdx.x * G + g;
     const bool active = e_raw < args.n_work;
     const uint32_t e = active ? e_raw : args.n_work - 1;
-    uint32_t *accA = sm.acc[g][0];
-    uint32_t *accB = sm.acc[g][1];
+    uint32_t *accA = sm.acc[TM ? 0 : g][0];
+    uint32_t *accB = sm.acc[TM ? 0 : g][1];
     double2 *xch = &sm.xch[g][0][0];
     uint16_t *bar = sm.bar[g];
 
     k1_modswitch(args, e, bar, t, 64);  // K1
     group_bar(bar_id);
-    acc_init(accA, accB, bar[n], args.mu, t, 64);  // ACC = X^{-barb} (0, mu...mu)
-    group_bar(bar_id);
+    if (TM) {  // ACC = X^{-barb} (0, mu...mu) at this thread's bins
+        const int barb = bar[n];
+        uint32_t v[32];
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+            const int j = t + 64 * m;
+            v[m] = 0;
+            v[8 + m] = 0;
+            v[16 + m] = ((j + barb) & kN) ? 0u - args.mu : args.mu;
+            v[24 + m] = ((j + kNH + barb) & kN) ? 0u - args.mu : args.mu;
+        }
+        tmem_st32(tacc, v);
+    } else {
+        acc_init(accA, accB, bar[n], args.mu, t, 64);  // ACC = X^{-barb} (0, mu...mu)
+        group_bar(bar_id);
+    }
 
     double max_err = 0.0;
     int st = 0;  // next stage to consume
@@ -969,16 +1023,32 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
             }
             __syncwarp();
             double2 x[2][8];
+            if (TM) {
+                uint32_t v[32];
+                tmem_ld32(tacc, v);
 #pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const int row = 2 * rp + h;
-                const int q = row / kL, p = row % kL;
-                const uint32_t *P = q ? accB : accA;
+                for (int h = 0; h < 2; h++) {
+                    const int row = 2 * rp + h;
+                    const int q = row / kL, p = row % kL;
 #pragma unroll
-                for (int m = 0; m < 8; m++) {
-                    const int j = t + 64 * m;
-                    x[h][m] = make_double2(small_int_to_double(gadget_digit(P[j], p)),
-                                           small_int_to_double(gadget_digit(P[j + kNH], p)));
+                    for (int m = 0; m < 8; m++) {
+                        const uint32_t lo = q ? v[16 + m] : v[m], hi = q ? v[24 + m] : v[8 + m];
+                        x[h][m] = make_double2(small_int_to_double(gadget_digit(lo, p)),
+                                               small_int_to_double(gadget_digit(hi, p)));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const int row = 2 * rp + h;
+                    const int q = row / kL, p = row % kL;
+                    const uint32_t *P = q ? accB : accA;
+#pragma unroll
+                    for (int m = 0; m < 8; m++) {
+                        const int j = t + 64 * m;
+                        x[h][m] = make_double2(small_int_to_double(gadget_digit(P[j], p)),
+                                               small_int_to_double(gadget_digit(P[j + kNH], p)));
+                    }
                 }
             }
             nega_fft_fwd_n<2, true>(x, xch, t, sm.tws[t], bar_id);
@@ -1039,25 +1109,79 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
                 x[1][m] = f1[m];
             }
             nega_fft_inv_n<2, true>(x, xch, t, sm.tws[t], bar_id);
+            if (kDebug) {
 #pragma unroll
-            for (int q = 0; q < 2; q++) {
-                uint32_t *P = q ? accB : accA;
+                for (int q = 0; q < 2; q++)
 #pragma unroll
-                for (int m = 0; m < 8; m++) {
-                    const double lo = x[q][m].x, hi = x[q][m].y;
-                    if (kDebug) {
-                        max_err = fmax(max_err, fabs(lo - rint(lo)));
-                        max_err = fmax(max_err, fabs(hi - rint(hi)));
+                    for (int m = 0; m < 8; m++) {
+                        max_err = fmax(max_err, fabs(x[q][m].x - rint(x[q][m].x)));
+                        max_err = fmax(max_err, fabs(x[q][m].y - rint(x[q][m].y)));
                     }
-                    const int j = t + 64 * m;
-                    P[j] += round_to_torus(lo);
-                    P[j + kNH] += round_to_torus(hi);
+            }
+            if (TM) {
+                uint32_t v[32];
+                tmem_ld32(tacc, v);
+#pragma unroll
+                for (int q = 0; q < 2; q++)
+#pragma unroll
+                    for (int m = 0; m < 8; m++) {
+                        v[16 * q + m] += round_to_torus(x[q][m].x);
+                        v[16 * q + 8 + m] += round_to_torus(x[q][m].y);
+                    }
+                tmem_st32(tacc, v);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 2; q++) {
+                    uint32_t *P = q ? accB : accA;
+#pragma unroll
+                    for (int m = 0; m < 8; m++) {
+                        const int j = t + 64 * m;
+                        P[j] += round_to_torus(x[q][m].x);
+                        P[j + kNH] += round_to_torus(x[q][m].y);
+                    }
                 }
             }
         }
-        group_bar(bar_id);
+        if (!TM) group_bar(bar_id);  // TM: ACC is thread-private; the next FFT starts with a barrier
     }
 
+    if (TM) {
+        uint32_t v[32];
+        tmem_ld32(tacc, v);
+        if (active) {
+            if (kDebug && args.margin) atomicMax(args.margin, (unsigned long long)__double_as_longlong(max_err));
+            if (kDebug && args.acc_dump) {
+                uint32_t *dst = args.acc_dump + (size_t)e * 2 * kN;
+#pragma unroll
+                for (int m = 0; m < 8; m++) {
+                    const int j = t + 64 * m;
+                    dst[j] = v[m];
+                    dst[j + kNH] = v[8 + m];
+                    dst[kN + j] = v[16 + m];
+                    dst[kN + j + kNH] = v[24 + m];
+                }
+            }
+            // K3: sample extraction at index 0 from this thread's coefficients:
+            // a'_0 = A_0, a'_c = -A_{N-c}, b' = B_0
+            uint32_t *out = args.big + (size_t)e * kBigStride;
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                const int j = t + 64 * m;
+                if (j == 0) {
+                    out[0] = v[0];
+                    out[kN] = v[16];
+                } else {
+                    out[kN - j] = 0u - v[m];
+                }
+                out[kNH - j] = 0u - v[8 + m];  // coefficient j + 512
+            }
+        }
+        tmem_fence_before();
+        __syncthreads();
+        tmem_fence_after();
+        if (warp == 0) tmem_dealloc(sm.tmem_base, kTmemCols);
+        return;
+    }
     if (!active) return;
     if (kDebug && args.margin) atomicMax(args.margin, (unsigned long long)__double_as_longlong(max_err));
     if (kDebug && args.acc_dump) {
@@ -1727,10 +1851,10 @@ int launch_br(hb_engine *e, const BrArgs &a) {
     return HB_OK;
 }
 
-template <int G, bool kDebug, int R = kStagesU2, int MB = 1>
+template <int G, bool kDebug, int R = kStagesU2, int MB = 1, bool TM = false>
 int launch_br_u2(hb_engine *e, const BrArgs &a) {
     const unsigned grid = (a.n_work + G - 1) / G;
-    k_blind_rotate_u2<G, kDebug, R, MB><<<grid, 64 * G, sizeof(BrSmemU2<G, R>), e->stream>>>(a);
+    k_blind_rotate_u2<G, kDebug, R, MB, TM><<<grid, 64 * G, sizeof(BrSmemU2<G, R, TM>), e->stream>>>(a);
     HB_CUDA_TRY(cudaGetLastError());
     e->n_launch++;
     return HB_OK;
@@ -1759,6 +1883,13 @@ int launch_ks(hb_engine *e, const KsArgs &a) {
 #define HB_PAIRED_RING 3
 #endif
 constexpr int kPairedRing = HB_PAIRED_RING;
+#ifndef HB_U2_TMEM
+#define HB_U2_TMEM 0  // wide key-pair levels: accumulators in tensor memory, deeper BK ring
+#endif
+#ifndef HB_TMEM_RING
+#define HB_TMEM_RING 9
+#endif
+constexpr int kStagesU2Tmem = HB_TMEM_RING;
 
 // Blind-rotation launch for a level of a.n_work bootstraps: narrow levels
 // (latency-bound) get one bootstrap per CTA split over three thread groups
@@ -1786,7 +1917,11 @@ int launch_br_auto(hb_engine *e, const BrArgs &a, int force_g = 0) {
 #if HB_U2_PAIRED
         if (!force_g) return launch_br_u2<2, kDebug, kPairedRing, 2>(e, a);  // two 2-gate CTAs per SM
 #endif
+#if HB_U2_TMEM
+        return launch_br_u2<kBrGates, kDebug, kStagesU2Tmem, 1, true>(e, a);
+#else
         return launch_br_u2<kBrGates, kDebug>(e, a);
+#endif
     }
     if (!force_g && gsel == 1 && e->latency_mode) return launch_br_lat<kDebug>(e, a);
     if (gsel == 1) return launch_br<1, kDebug>(e, a);
@@ -1885,6 +2020,14 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
                                      (int)br_smem_bytes<1>()));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)br_smem_bytes<kBrGates>()));
+#if HB_U2_TMEM
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, false, kStagesU2Tmem, 1, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrSmemU2<kBrGates, kStagesU2Tmem, true>)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, true, kStagesU2Tmem, 1, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrSmemU2<kBrGates, kStagesU2Tmem, true>)));
+#endif
 #if HB_U2_PAIRED
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<2, false, kPairedRing, 2>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,

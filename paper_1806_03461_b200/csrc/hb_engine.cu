@@ -1607,6 +1607,7 @@ struct KsArgs {
     uint32_t *pool;
     uint32_t pool_stride;
     int32_t n;
+    uint32_t *partial;       // narrow levels: [splits][n_work][kKskStride] raw sums (else null)
 };
 
 constexpr int kKsCols = 8;                               // output columns per chunk
@@ -1634,8 +1635,11 @@ __global__ void __launch_bounds__(kKsThreads) k_keyswitch(const KsArgs args) {
     const uint32_t *b0 = args.big + ((size_t)it.i0 * lanes + lane_id) * kBigStride;
     const uint32_t *b1 = it.i1 != 0xFFFFFFFFu ? args.big + ((size_t)it.i1 * lanes + lane_id) * kBigStride : nullptr;
     const int chunk = blockIdx.y;
-    const char *tab_src = reinterpret_cast<const char *>(args.ksk) + (size_t)chunk * kN * kKsT * 4 * kKsCols * 4;
-    constexpr int kBlocks = kN / kKsIBlock;  // 128
+    // blockIdx.z splits the coefficient range (narrow levels: more CTAs, shorter streams)
+    const int kBlocks = (kN / kKsIBlock) / gridDim.z;
+    const int blk0 = blockIdx.z * kBlocks;
+    const char *tab_src = reinterpret_cast<const char *>(args.ksk) + (size_t)chunk * kN * kKsT * 4 * kKsCols * 4 +
+                          (size_t)blk0 * kKsStageBytes;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kKsStages; s++) {
@@ -1643,7 +1647,7 @@ __global__ void __launch_bounds__(kKsThreads) k_keyswitch(const KsArgs args) {
             mbar_init(&ks.empty[s], kKsThreads / 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int b = 0; b < kKsStages - 1; b++) {
+        for (int b = 0; b < kKsStages - 1 && b < kBlocks; b++) {
             mbar_arrive_expect_tx(&ks.full[b], kKsStageBytes);
             bulk_g2s(ks.tab[b], tab_src + (size_t)b * kKsStageBytes, kKsStageBytes, &ks.full[b]);
         }
@@ -1653,8 +1657,8 @@ __global__ void __launch_bounds__(kKsThreads) k_keyswitch(const KsArgs args) {
     uint32_t acc[kKsCols];
 #pragma unroll
     for (int c = 0; c < kKsCols; c++) acc[c] = 0;
-    const uint4 *wsrc0 = reinterpret_cast<const uint4 *>(b0);
-    const uint4 *wsrc1 = reinterpret_cast<const uint4 *>(b1);
+    const uint4 *wsrc0 = reinterpret_cast<const uint4 *>(b0) + 2 * blk0;
+    const uint4 *wsrc1 = b1 ? reinterpret_cast<const uint4 *>(b1) + 2 * blk0 : nullptr;
     uint4 wa = __ldg(wsrc0), wb = __ldg(wsrc0 + 1);
     if (b1) {
         const uint4 xa = __ldg(wsrc1), xb = __ldg(wsrc1 + 1);
@@ -1703,6 +1707,12 @@ __global__ void __launch_bounds__(kKsThreads) k_keyswitch(const KsArgs args) {
     }
     if (!active) return;
     const int c0 = chunk * kKsCols;
+    if (args.partial) {  // split sums, combined by k_keyswitch_reduce
+        uint32_t *dst = args.partial + ((size_t)blockIdx.z * args.n_work + e) * kKskStride + c0;
+#pragma unroll
+        for (int c = 0; c < kKsCols; c++) dst[c] = acc[c];
+        return;
+    }
     uint32_t bval = 0;
     if (c0 + kKsCols > args.n) {
         bval = b0[kN];
@@ -1714,6 +1724,24 @@ __global__ void __launch_bounds__(kKsThreads) k_keyswitch(const KsArgs args) {
         const int col = c0 + c;
         if (col <= args.n) dst[col] = (col == args.n ? bval : 0u) - acc[c];
     }
+}
+
+// Narrow levels: out = (0.., b) - sum over the coefficient splits of k_keyswitch.
+__global__ void __launch_bounds__(kKskStride) k_keyswitch_reduce(const KsArgs args, int splits) {
+    const uint32_t e = blockIdx.x;
+    const int col = threadIdx.x;
+    if (col > args.n) return;
+    const uint32_t lanes = args.lanes;
+    const KsItem it = args.items[e / lanes];
+    const uint32_t lane_id = e % lanes;
+    uint32_t sum = 0;
+    for (int sp = 0; sp < splits; sp++) sum += args.partial[((size_t)sp * args.n_work + e) * kKskStride + col];
+    uint32_t bval = 0;
+    if (col == args.n) {
+        bval = args.big[((size_t)it.i0 * lanes + lane_id) * kBigStride + kN];
+        if (it.i1 != 0xFFFFFFFFu) bval += args.big[((size_t)it.i1 * lanes + lane_id) * kBigStride + kN] + it.cadd;
+    }
+    args.pool[((size_t)it.dst * lanes + lane_id) * args.pool_stride + col] = bval - sum;
 }
 
 // FP64 roofline probe: 8 independent DFMA chains per thread.
@@ -1793,6 +1821,8 @@ struct hb_engine {
     size_t ks_cap = 0;
     uint32_t *d_tmp = nullptr;
     size_t tmp_cap = 0;  // words
+    uint32_t *d_kspart = nullptr;
+    size_t kspart_cap = 0;  // words: narrow-level key-switch partial sums
     void *h_stage = nullptr;
     size_t h_stage_cap = 0;
     unsigned long long *d_margin = nullptr;
@@ -1868,11 +1898,29 @@ int launch_br_lat(hb_engine *e, const BrArgs &a) {
     return HB_OK;
 }
 
-int launch_ks(hb_engine *e, const KsArgs &a) {
-    const dim3 grid((a.n_work + kKsThreads - 1) / kKsThreads, kKsChunks);
+// narrow levels (<= kKsNarrow key switches): the coefficient range is split
+// over kKsSplits CTAs per column chunk and the partial sums are reduced
+constexpr uint32_t kKsNarrow = 32;
+constexpr int kKsSplits = 8;
+
+int launch_ks(hb_engine *e, const KsArgs &a0) {
+    KsArgs a = a0;
+    const bool narrow = a.n_work <= kKsNarrow;
+    if (narrow) {
+        int rc = ensure_dev((void **)&e->d_kspart, &e->kspart_cap, (size_t)kKsSplits * a.n_work * kKskStride,
+                            sizeof(uint32_t), false, e->stream);
+        if (rc) return rc;
+        a.partial = e->d_kspart;
+    }
+    const dim3 grid((a.n_work + kKsThreads - 1) / kKsThreads, kKsChunks, narrow ? kKsSplits : 1);
     k_keyswitch<<<grid, kKsThreads, 0, e->stream>>>(a);
     HB_CUDA_TRY(cudaGetLastError());
     e->n_launch++;
+    if (narrow) {
+        k_keyswitch_reduce<<<a.n_work, kKskStride, 0, e->stream>>>(a, kKsSplits);
+        HB_CUDA_TRY(cudaGetLastError());
+        e->n_launch++;
+    }
     return HB_OK;
 }
 
@@ -2098,7 +2146,7 @@ int hb_engine_destroy(hb_engine *e) {
     cudaSetDevice(e->device);
     if (e->stream) cudaStreamSynchronize(e->stream);
     for (void *ptr : {(void *)e->d_W, (void *)e->d_TW, (void *)e->d_PSI, (void *)e->d_bkf, (void *)e->d_ksk, (void *)e->d_pool,
-                      (void *)e->d_big, (void *)e->d_br, (void *)e->d_ks, (void *)e->d_tmp, (void *)e->d_margin,
+                      (void *)e->d_big, (void *)e->d_br, (void *)e->d_ks, (void *)e->d_tmp, (void *)e->d_kspart, (void *)e->d_margin,
                       e->d_flush})
         if (ptr) cudaFree(ptr);
     if (e->h_stage) cudaFreeHost(e->h_stage);

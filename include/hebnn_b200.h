@@ -142,6 +142,13 @@ int hb_pool_upload_async(hb_engine *e, size_t first_slot, size_t count, const ui
 int hb_pool_download_async(hb_engine *e, size_t first_slot, size_t count, uint32_t *host,
                            size_t host_stride);
 /* scattered slots -> host (gathered on the device, one copy) */
+/* Device-resident exchange (multi-GPU all-gather without host staging): copy
+ * pool slots `slots[count]` into / consecutive slots from a device buffer of
+ * this engine's GPU with row stride dev_stride (>= n+1 words); synchronous. */
+int hb_pool_gather_device(hb_engine *e, const uint32_t *slots, size_t count, uint32_t *dev_out,
+                          size_t dev_stride);
+int hb_pool_put_device(hb_engine *e, size_t first_slot, size_t count, const uint32_t *dev_in,
+                       size_t dev_stride);
 int hb_pool_gather(hb_engine *e, const uint32_t *slots, size_t count, uint32_t *host,
                    size_t host_stride);
 

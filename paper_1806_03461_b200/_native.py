@@ -32,7 +32,7 @@ EXPORTED = (
     "hb_pool_download", "hb_pool_gather", "hb_run_gates", "hb_sync", "hb_last_timing",
     "hb_counters", "hb_debug_blind_rotate", "hb_debug_bootstrap_wo_ks", "hb_debug_keyswitch",
     "hb_debug_fft_margin", "hb_debug_fourier", "hb_flush_l2", "hb_measure_fp64_peak",
-    "hb_pool_upload_async", "hb_pool_download_async",
+    "hb_pool_upload_async", "hb_pool_download_async", "hb_pool_gather_device", "hb_pool_put_device",
 )
 
 
@@ -121,6 +121,8 @@ def lib():
         "hb_pool_upload": ([vp, sz, sz, u32p, sz], ctypes.c_int),
         "hb_pool_download": ([vp, sz, sz, u32p, sz], ctypes.c_int),
         "hb_pool_gather": ([vp, u32p, sz, u32p, sz], ctypes.c_int),
+        "hb_pool_gather_device": ([vp, u32p, sz, vp, sz], ctypes.c_int),
+        "hb_pool_put_device": ([vp, sz, sz, vp, sz], ctypes.c_int),
         "hb_pool_upload_async": ([vp, sz, sz, u32p, sz], ctypes.c_int),
         "hb_pool_download_async": ([vp, sz, sz, u32p, sz], ctypes.c_int),
         "hb_run_gates": ([vp, vp, sz, ctypes.c_uint32], ctypes.c_int),

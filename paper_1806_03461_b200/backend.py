@@ -328,6 +328,60 @@ class TfheContext(GateBackend):
                     out[i] = (0 - out[i].astype(np.int64)).astype(np.uint32)
             return out
 
+    def export_ciphertexts_device(self, handles):
+        """export_ciphertexts into a torch.int32 CUDA tensor [count][lanes][n+1]
+        on this context's GPU, without host staging (multi-GPU exchange)."""
+        import torch
+
+        self._check(*handles)
+        with self._lock:
+            refs = [h._value for h in handles]
+            for r in refs:
+                self._dag.revive(r >> 1)
+            if self._dag.pending_count():
+                self.flush()
+            self._join_bg()
+            words = self.params.n + 1
+            out = torch.zeros((len(refs), self.lanes, words), dtype=torch.int32, device=f"cuda:{self.device}")
+            host_inputs = [i for i, r in enumerate(refs) if (r >> 1) in self._inputs]
+            dev = [i for i, r in enumerate(refs) if (r >> 1) != 0 and (r >> 1) not in self._inputs]
+            if dev:
+                eng = self._ensure_engine()
+                slots = self._map_slots([(refs[i] >> 1) - 1 for i in dev])
+                phys = (slots[:, None] * self.lanes + np.arange(self.lanes)[None, :]).reshape(-1)
+                buf = torch.empty((len(dev) * self.lanes, words), dtype=torch.int32, device=out.device)
+                eng.gather_device(phys.astype(np.uint32), buf.data_ptr(), words)
+                out[dev] = buf.view(len(dev), self.lanes, words)
+            for i in host_inputs:
+                out[i] = torch.from_numpy(self._inputs[refs[i] >> 1].view(np.int32)).to(out.device)
+            for i, r in enumerate(refs):
+                if (r >> 1) == 0:
+                    out[i, :, -1] = EIGHTH if r & 1 else -EIGHTH
+                elif r & 1:
+                    out[i] = -out[i]  # two's complement negation = mod-2^32 negation
+            return out
+
+    def import_ciphertexts_device(self, cts):
+        """import_ciphertexts from a torch.int32 CUDA tensor [count][lanes][n+1]
+        on this context's GPU: copied device-to-device into fresh pool slots."""
+        with self._lock:
+            if cts.dim() == 2:
+                cts = cts[:, None, :]
+            if tuple(cts.shape[1:]) != (self.lanes, self.params.n + 1):
+                raise ValueError(f"expected [count, {self.lanes}, {self.params.n + 1}] ciphertexts, got {tuple(cts.shape)}")
+            cts = cts.contiguous()
+            nids = [self._dag.add_input() for _ in range(cts.shape[0])]
+            if nids:
+                eng = self._ensure_engine()
+                phys = np.asarray(self._map_slots(np.asarray(nids, dtype=np.int64) - 1), dtype=np.int64)
+                breaks = np.flatnonzero(np.diff(phys) != 1) + 1
+                words = self.params.n + 1
+                row = self.lanes * words * 4
+                for run in np.split(np.arange(phys.size), breaks):
+                    eng.put_device(int(phys[run[0]]) * self.lanes, run.size * self.lanes,
+                                   cts.data_ptr() + int(run[0]) * row, words)
+            return [self._bit(nid << 1, 0) for nid in nids]
+
     def _encrypt_host(self, bits, idx0):
         # one ChaCha stream per context; the ciphertext index continues across calls
         return self.keys.encrypt(bits, seed=self.enc_seed, stream=self.enc_stream, first_index=idx0)

@@ -1760,11 +1760,11 @@ __global__ void __launch_bounds__(256) k_dfma_peak(double *out, int iters, doubl
 }
 
 __global__ void k_gather(const uint32_t *__restrict__ pool, uint32_t stride, const uint32_t *__restrict__ slots,
-                         uint32_t count, uint32_t words, uint32_t *__restrict__ out) {
+                         uint32_t count, uint32_t words, uint32_t *__restrict__ out, size_t out_stride) {
     const uint32_t s = blockIdx.x;
     if (s >= count) return;
     const uint32_t *src = pool + (size_t)slots[s] * stride;
-    for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) out[(size_t)s * words + w] = src[w];
+    for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) out[(size_t)s * out_stride + w] = src[w];
 }
 
 // KSK host layout [kN][t][3][n+1] -> device lookup table
@@ -2203,6 +2203,46 @@ int hb_pool_download(hb_engine *e, size_t first, size_t count, uint32_t *host, s
     return HB_OK;
 }
 
+int hb_pool_gather_device(hb_engine *e, const uint32_t *slots, size_t count, uint32_t *dev_out, size_t dev_stride) {
+    if (!e || (count && (!slots || !dev_out)) || dev_stride < (size_t)e->p.n + 1) {
+        set_error("hb_pool_gather_device: bad arguments");
+        return HB_EINVAL;
+    }
+    if (!count) return HB_OK;
+    for (size_t i = 0; i < count; i++)
+        if (slots[i] >= e->pool_cap) {
+            set_error("hb_pool_gather_device: slot beyond pool capacity");
+            return HB_EINVAL;
+        }
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    int rc = ensure_dev((void **)&e->d_tmp, &e->tmp_cap, count, sizeof(uint32_t), false, e->stream);
+    if (rc) return rc;
+    rc = ensure_host_stage(e, count * sizeof(uint32_t));
+    if (rc) return rc;
+    HB_CUDA_TRY(cudaEventSynchronize(e->ev_stage));
+    std::memcpy(e->h_stage, slots, count * sizeof(uint32_t));
+    HB_CUDA_TRY(cudaMemcpyAsync(e->d_tmp, e->h_stage, count * sizeof(uint32_t), cudaMemcpyHostToDevice, e->stream));
+    k_gather<<<(unsigned)count, 256, 0, e->stream>>>(e->d_pool, e->pool_stride, e->d_tmp, (uint32_t)count,
+                                                    (uint32_t)e->p.n + 1, dev_out, dev_stride);
+    HB_CUDA_TRY(cudaGetLastError());
+    HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    e->n_launch++;
+    return HB_OK;
+}
+
+int hb_pool_put_device(hb_engine *e, size_t first_slot, size_t count, const uint32_t *dev_in, size_t dev_stride) {
+    if (!e || (count && !dev_in) || dev_stride < (size_t)e->p.n + 1 || first_slot + count > e->pool_cap) {
+        set_error("hb_pool_put_device: bad arguments or slots beyond pool capacity");
+        return HB_EINVAL;
+    }
+    if (!count) return HB_OK;
+    HB_CUDA_TRY(cudaSetDevice(e->device));
+    HB_CUDA_TRY(cudaMemcpy2DAsync(e->d_pool + first_slot * e->pool_stride, (size_t)e->pool_stride * 4, dev_in,
+                                  dev_stride * 4, ((size_t)e->p.n + 1) * 4, count, cudaMemcpyDeviceToDevice, e->stream));
+    HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return HB_OK;
+}
+
 int hb_pool_gather(hb_engine *e, const uint32_t *slots, size_t count, uint32_t *host, size_t host_stride) {
     if (!e || (count && (!slots || !host)) || host_stride < (size_t)e->p.n + 1) {
         set_error("hb_pool_gather: bad arguments");
@@ -2225,7 +2265,8 @@ int hb_pool_gather(hb_engine *e, const uint32_t *slots, size_t count, uint32_t *
     std::memcpy(e->h_stage, slots, count * sizeof(uint32_t));
     uint32_t *d_slots = e->d_tmp, *d_out = e->d_tmp + count;
     HB_CUDA_TRY(cudaMemcpyAsync(d_slots, e->h_stage, count * sizeof(uint32_t), cudaMemcpyHostToDevice, e->stream));
-    k_gather<<<(unsigned)count, 256, 0, e->stream>>>(e->d_pool, e->pool_stride, d_slots, (uint32_t)count, words, d_out);
+    k_gather<<<(unsigned)count, 256, 0, e->stream>>>(e->d_pool, e->pool_stride, d_slots, (uint32_t)count, words, d_out,
+                                                    words);
     HB_CUDA_TRY(cudaGetLastError());
     HB_CUDA_TRY(cudaMemcpy2DAsync(host, host_stride * 4, d_out, (size_t)words * 4, (size_t)words * 4, count,
                                   cudaMemcpyDeviceToHost, e->stream));

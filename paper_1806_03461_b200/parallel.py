@@ -113,7 +113,9 @@ class OutPEvaluator:
             costs = unit_costs(block, self.options) if self.balance == "gates" else None
             lo, hi = partition(_units(block), self.comm.world, costs)[self.comm.rank]
             ctx = self.ctx_factory()
-            x = ctx.import_ciphertexts(cts)
+            dev_path = getattr(self.comm, "device_tensors", False) and hasattr(ctx, "import_ciphertexts_device")
+            x = ctx.import_ciphertexts_device(cts) if dev_path and not isinstance(cts, np.ndarray) \
+                else ctx.import_ciphertexts(self._host(cts))
             outs = []
             if hi > lo:
                 sub = _sub_block_model(block, lo, hi, model.output_mode, is_last)
@@ -135,6 +137,13 @@ class OutPEvaluator:
                     for w, sg in zip(w_r, s_r):
                         result.append((cts_r[off:off + w], bool(sg)))
                         off += w
+            elif dev_path:  # NCCL all-gather of device-resident ciphertexts (no host staging)
+                import torch
+
+                local = ctx.export_ciphertexts_device(outs) if outs else \
+                    torch.zeros((0, ctx.lanes, ctx.params.n + 1), dtype=torch.int32, device=f"cuda:{ctx.device}")
+                cts = torch.cat(self.comm.all_gather_tensor(local), dim=0)
+                result = [c.cpu().numpy().view(np.uint32) for c in cts] if is_last else None
             else:
                 local = ctx.export_ciphertexts(outs) if outs else np.zeros((0, ctx.lanes, ctx.params.n + 1), np.uint32)
                 gathered = self.comm.all_gather(local)
@@ -142,9 +151,17 @@ class OutPEvaluator:
                 result = list(cts)
         return result
 
+    @staticmethod
+    def _host(cts):
+        if isinstance(cts, np.ndarray):
+            return cts
+        return cts.cpu().numpy().view(np.uint32)
+
 
 class TorchComm:
-    """all-gather of variable-length uint32 arrays over torch.distributed."""
+    """all-gather of variable-length uint32 arrays over torch.distributed; with
+    NCCL (device_tensors) layer outputs are gathered as CUDA tensors straight
+    from and into the engine pools (hb_pool_gather_device / hb_pool_put_device)."""
 
     def __init__(self, device=None):
         import torch
@@ -155,6 +172,22 @@ class TorchComm:
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
         self.device = device if device is not None else ("cuda" if dist.get_backend() == "nccl" else "cpu")
+        self.device_tensors = str(self.device).startswith("cuda")
+
+    def all_gather_tensor(self, t):
+        """all-gather of a device tensor with a variable leading dimension."""
+        torch, dist = self.torch, self.dist
+        lead = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+        sizes = [torch.zeros_like(lead) for _ in range(self.world)]
+        dist.all_gather(sizes, lead)
+        sizes = [int(v.item()) for v in sizes]
+        mx = max(sizes) if sizes else 0
+        pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[: t.shape[0]] = t
+        bufs = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(bufs, pad)
+        torch.cuda.synchronize(t.device)
+        return [b[:n] for b, n in zip(bufs, sizes)]
 
     def all_gather(self, arr):
         torch, dist = self.torch, self.dist

@@ -168,6 +168,20 @@ class Engine:
         check(lib().hb_pool_download_async(self._e, int(first), out.shape[0], u32p(out), out.shape[1]))
 
     @_locked
+    def gather_device(self, slots, dev_ptr, dev_stride):
+        """Pool slots -> device buffer at `dev_ptr` (this engine's GPU, rows of
+        dev_stride >= n+1 u32 words); synchronous."""
+        slots = np.ascontiguousarray(slots, dtype=np.uint32)
+        check(lib().hb_pool_gather_device(self._e, u32p(slots), slots.size, ctypes.c_void_p(int(dev_ptr)),
+                                          int(dev_stride)))
+
+    @_locked
+    def put_device(self, first, count, dev_ptr, dev_stride):
+        """Device buffer rows -> pool slots [first, first+count); synchronous."""
+        check(lib().hb_pool_put_device(self._e, int(first), int(count), ctypes.c_void_p(int(dev_ptr)),
+                                       int(dev_stride)))
+
+    @_locked
     def gather(self, slots):
         slots = np.ascontiguousarray(slots, dtype=np.uint32)
         out = np.zeros((slots.size, self.params.n + 1), np.uint32)

@@ -399,7 +399,7 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
     HB_CUDA_TRY(cudaMalloc(&d_kin, ksk_rows * (p->n + 1) * sizeof(uint32_t)));
     HB_CUDA_TRY(cudaMemcpy(d_kin, ksk, ksk_rows * (p->n + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice));
     HB_CUDA_TRY(cudaMalloc(&e->d_ksk, kKsTableWords * sizeof(uint32_t)));
-    k_ksk_relayout<<<(unsigned)(ksk_rows / kKsVals), 256, 0, e->stream>>>(d_kin, e->d_ksk, p->n);
+    k_ksk_relayout<<<kKsRelayoutBlocks, 256, 0, e->stream>>>(d_kin, e->d_ksk, p->n);
     HB_CUDA_TRY(cudaGetLastError());
     HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
     cudaFree(d_kin);

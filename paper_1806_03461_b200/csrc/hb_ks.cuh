@@ -5,20 +5,32 @@
 
 // ---------------------------------------------------------------------------
 // K4: batched key switch.  For coefficient i the CGGI digits are the eight
-// base-4 digits of w_i = (a'_i + 2^15) >> 16.  The device KSK is laid out as a
-// lookup table per 8-column chunk, T[chunk][i][j][d][8] with T[..][0][..] = 0,
-// so one digit costs two LDS.128 (the 4 candidate rows of an (i, j) fill one
-// 128-B line: lanes with different digits hit different banks) and 8 IADDs.
-// CTA = 128 gates (one per thread) x one 8-column chunk; the chunk's 1 MiB
-// table streams through a shared-memory ring fed by cp.async.bulk, so every
-// table byte fetched from L2 serves 128 gates.
+// base-4 digits of w_i = (a'_i + 2^15) >> 16, and the key switch subtracts
+// KS[i][j][d_j] (d_j = 0 contributes nothing) from (0.., b).
+//
+// HB_KS_PAIR = 1 (default): digits are consumed in pairs.  The device table
+// holds, per coefficient i, digit pair p and output column c, the 16 sums
+//   T[chunk][i][p][c][d] = KS[i][2p][d >> 2] + KS[i][2p+1][d & 3]  (mod 2^32)
+// (64 B: 16 consecutive banks), so one digit pair costs one conflict-free
+// LDS.32 per column (lanes with equal d broadcast, different d hit different
+// banks): 8 wavefronts per warp per digit PAIR, half of the one-digit layout,
+// and half the integer adds.  Sums mod 2^32 are exact in any order, so the
+// result is bit-identical to the digit-by-digit key switch.
+// HB_KS_PAIR = 0: T[chunk][i][j][d][8] with T[..][0][..] = 0; one digit costs
+// two LDS.128 (the 4 candidate rows of an (i, j) fill one 128-B line).
+// CTA = 128 gates (one per thread) x one 8-column chunk; the chunk's table
+// streams through a shared-memory ring fed by cp.async.bulk, so every table
+// byte fetched from L2 serves 128 gates.
 // ---------------------------------------------------------------------------
+#ifndef HB_KS_PAIR
+#define HB_KS_PAIR 1
+#endif
 struct KsArgs {
     const uint32_t *big;     // [n_br_work][kBigStride]
     const KsItem *items;     // [n_items]
     uint32_t lanes;
     uint32_t n_work;         // n_items * lanes
-    const uint32_t *ksk;     // [kKsChunks][kN][t][4][kKsCols] lookup table
+    const uint32_t *ksk;     // device lookup table (layout above)
     uint32_t *pool;
     uint32_t pool_stride;
     int32_t n;
@@ -28,10 +40,11 @@ struct KsArgs {
 constexpr int kKsCols = 8;                               // output columns per chunk
 constexpr int kKsChunks = kKskStride / kKsCols;           // 80
 constexpr int kKsThreads = 128;                           // one gate per thread
-constexpr int kKsIBlock = 8;                              // coefficients per ring stage
-constexpr uint32_t kKsStageBytes = kKsIBlock * kKsT * 4 * kKsCols * 4;  // 8 KiB
-constexpr int kKsStages = 4;
-constexpr size_t kKsTableWords = (size_t)kKsChunks * kN * kKsT * 4 * kKsCols;
+constexpr int kKsRowsPerI = HB_KS_PAIR ? (kKsT / 2) * 16 : kKsT * 4;  // table rows per coefficient
+constexpr int kKsIBlock = HB_KS_PAIR ? 4 : 8;             // coefficients per ring stage
+constexpr uint32_t kKsStageBytes = kKsIBlock * kKsRowsPerI * kKsCols * 4;  // 8 KiB
+constexpr int kKsStages = HB_KS_PAIR ? 5 : 4;
+constexpr size_t kKsTableWords = (size_t)kKsChunks * kN * kKsRowsPerI * kKsCols;
 
 struct KsSmem {
     uint4 tab[kKsStages][kKsStageBytes / 16];
@@ -53,7 +66,7 @@ __global__ void __launch_bounds__(kKsThreads) k_keyswitch(const KsArgs args) {
     // blockIdx.z splits the coefficient range (narrow levels: more CTAs, shorter streams)
     const int kBlocks = (kN / kKsIBlock) / gridDim.z;
     const int blk0 = blockIdx.z * kBlocks;
-    const char *tab_src = reinterpret_cast<const char *>(args.ksk) + (size_t)chunk * kN * kKsT * 4 * kKsCols * 4 +
+    const char *tab_src = reinterpret_cast<const char *>(args.ksk) + (size_t)chunk * kN * kKsRowsPerI * kKsCols * 4 +
                           (size_t)blk0 * kKsStageBytes;
 
     if (threadIdx.x == 0) {
@@ -72,13 +85,18 @@ __global__ void __launch_bounds__(kKsThreads) k_keyswitch(const KsArgs args) {
     uint32_t acc[kKsCols];
 #pragma unroll
     for (int c = 0; c < kKsCols; c++) acc[c] = 0;
-    const uint4 *wsrc0 = reinterpret_cast<const uint4 *>(b0) + 2 * blk0;
-    const uint4 *wsrc1 = b1 ? reinterpret_cast<const uint4 *>(b1) + 2 * blk0 : nullptr;
-    uint4 wa = __ldg(wsrc0), wb = __ldg(wsrc0 + 1);
-    if (b1) {
-        const uint4 xa = __ldg(wsrc1), xb = __ldg(wsrc1 + 1);
-        wa = make_uint4(wa.x + xa.x, wa.y + xa.y, wa.z + xa.z, wa.w + xa.w);
-        wb = make_uint4(wb.x + xb.x, wb.y + xb.y, wb.z + xb.z, wb.w + xb.w);
+    // this thread's extracted-LWE coefficients, kKsIBlock per block (uint4 loads)
+    constexpr int kW4 = kKsIBlock / 4;
+    const uint4 *wsrc0 = reinterpret_cast<const uint4 *>(b0) + kW4 * blk0;
+    const uint4 *wsrc1 = b1 ? reinterpret_cast<const uint4 *>(b1) + kW4 * blk0 : nullptr;
+    uint4 w[kW4];
+#pragma unroll
+    for (int q = 0; q < kW4; q++) {
+        w[q] = __ldg(wsrc0 + q);
+        if (b1) {
+            const uint4 x = __ldg(wsrc1 + q);
+            w[q] = make_uint4(w[q].x + x.x, w[q].y + x.y, w[q].z + x.z, w[q].w + x.w);
+        }
     }
 #pragma unroll 1
     for (int blk = 0; blk < kBlocks; blk++) {
@@ -92,18 +110,37 @@ __global__ void __launch_bounds__(kKsThreads) k_keyswitch(const KsArgs args) {
             }
         }
         __syncwarp();
-        const uint32_t v[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+        uint32_t v[kKsIBlock];
+#pragma unroll
+        for (int q = 0; q < kW4; q++) {
+            v[4 * q] = w[q].x; v[4 * q + 1] = w[q].y; v[4 * q + 2] = w[q].z; v[4 * q + 3] = w[q].w;
+        }
         if (blk + 1 < kBlocks) {  // prefetch the next block's coefficients
-            wa = __ldg(wsrc0 + 2 * blk + 2);
-            wb = __ldg(wsrc0 + 2 * blk + 3);
-            if (b1) {
-                const uint4 xa = __ldg(wsrc1 + 2 * blk + 2), xb = __ldg(wsrc1 + 2 * blk + 3);
-                wa = make_uint4(wa.x + xa.x, wa.y + xa.y, wa.z + xa.z, wa.w + xa.w);
-                wb = make_uint4(wb.x + xb.x, wb.y + xb.y, wb.z + xb.z, wb.w + xb.w);
+#pragma unroll
+            for (int q = 0; q < kW4; q++) {
+                w[q] = __ldg(wsrc0 + kW4 * (blk + 1) + q);
+                if (b1) {
+                    const uint4 x = __ldg(wsrc1 + kW4 * (blk + 1) + q);
+                    w[q] = make_uint4(w[q].x + x.x, w[q].y + x.y, w[q].z + x.z, w[q].w + x.w);
+                }
             }
         }
         const int s = blk % kKsStages;
         mbar_wait(&ks.full[s], (blk / kKsStages) & 1);
+#if HB_KS_PAIR
+        const uint32_t *tab = reinterpret_cast<const uint32_t *>(ks.tab[s]);
+#pragma unroll
+        for (int ii = 0; ii < kKsIBlock; ii++) {
+            const uint32_t word = (v[ii] + (1u << 15)) >> 16;
+#pragma unroll
+            for (int jp = 0; jp < kKsT / 2; jp++) {
+                const uint32_t d = (word >> (12 - 4 * jp)) & 15u;
+                const uint32_t *row = tab + (ii * (kKsT / 2) + jp) * (kKsCols * 16) + d;
+#pragma unroll
+                for (int c = 0; c < kKsCols; c++) acc[c] += row[16 * c];
+            }
+        }
+#else
         const uint4 *tab = ks.tab[s];
 #pragma unroll
         for (int ii = 0; ii < kKsIBlock; ii++) {
@@ -117,6 +154,7 @@ __global__ void __launch_bounds__(kKsThreads) k_keyswitch(const KsArgs args) {
                 acc[4] += hi.x; acc[5] += hi.y; acc[6] += hi.z; acc[7] += hi.w;
             }
         }
+#endif
         __syncwarp();
         if (lane == 0) mbar_arrive(&ks.empty[s]);
     }
@@ -182,9 +220,27 @@ __global__ void k_gather(const uint32_t *__restrict__ pool, uint32_t stride, con
     for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) out[(size_t)s * out_stride + w] = src[w];
 }
 
-// KSK host layout [kN][t][3][n+1] -> device lookup table
-// T[chunk][i][j][d][kKsCols] = KS[i][j][d] columns chunk*8 .. chunk*8+7 (d = 0 row is 0).
+// KSK host layout [kN][t][3][n+1] -> device lookup table (layout: K4 above).
+// HB_KS_PAIR: T[chunk][i][p][cc][d] = KS[i][2p][d >> 2] + KS[i][2p+1][d & 3].
+// HB_KS_PAIR = 0: T[chunk][i][j][d][kKsCols] = KS[i][j][d] (d = 0 row is 0).
 __global__ void k_ksk_relayout(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, int n) {
+#if HB_KS_PAIR
+    const size_t ip = blockIdx.x;  // i * (t / 2) + p
+    const size_t i = ip / (kKsT / 2), p = ip % (kKsT / 2);
+    const uint32_t *src0 = in + (i * kKsT + 2 * p) * 3 * (size_t)(n + 1);
+    const uint32_t *src1 = src0 + 3 * (size_t)(n + 1);
+    for (int w = threadIdx.x; w < kKskStride * 16; w += blockDim.x) {
+        const int d = w / kKskStride, col = w % kKskStride;
+        const int d0 = d >> 2, d1 = d & 3;
+        uint32_t val = 0;
+        if (col <= n) {
+            if (d0) val += src0[(size_t)(d0 - 1) * (n + 1) + col];
+            if (d1) val += src1[(size_t)(d1 - 1) * (n + 1) + col];
+        }
+        const int chunk = col / kKsCols, cc = col % kKsCols;
+        out[(((size_t)chunk * kN * (kKsT / 2) + ip) * kKsCols + cc) * 16 + d] = val;
+    }
+#else
     const size_t ij = blockIdx.x;  // i * t + j
     const uint32_t *src = in + ij * 3 * (size_t)(n + 1);
     for (int w = threadIdx.x; w < kKskStride * 4; w += blockDim.x) {
@@ -193,7 +249,9 @@ __global__ void k_ksk_relayout(const uint32_t *__restrict__ in, uint32_t *__rest
         const int chunk = col / kKsCols, cc = col % kKsCols;
         out[(((size_t)chunk * kN * kKsT + ij) * 4 + d) * kKsCols + cc] = val;
     }
+#endif
 }
+constexpr unsigned kKsRelayoutBlocks = kN * (HB_KS_PAIR ? kKsT / 2 : kKsT);
 
 constexpr int kBrGates = 4;  // bootstraps per CTA (64 threads each)
 

@@ -226,7 +226,7 @@ def run_reference(args, dist):
     if dist.rank != 0:
         return None
     threads = os.cpu_count() or 1
-    sample = 8 * threads  # ~1.3 s of wall time per step (~20 core-seconds)
+    sample = 24 * threads  # ~2 s of wall time per step (~30 core-seconds)
     step, ok = cpu_nand_sample(args.seed, sample, threads)
     for _ in range(args.warmup):
         step()
@@ -534,15 +534,15 @@ def run_ours(args, dist):
             line["bnn"] = {"error": repr(exc)}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        sample = 8 * threads  # ~20 core-seconds of exact CGGI on the host
+        sample = 128 * threads  # ~10 s of wall time (~150 core-seconds) of exact CGGI on the host
         step, ok = cpu_nand_sample(args.seed, sample, threads)
         dt = step()
         line["cpu_baseline"] = {"value": sample / dt, "unit": "gates/s", "cores": threads, "kind": "port",
                                 "sample": f"{sample} NAND gates on {threads} threads ({cpu_model()}), "
                                           f"{dt:.1f} s; exact-integer CGGI oracle (reference has no crypto)",
                                 "correct": ok()}
-        step1, _ = cpu_nand_sample(args.seed + 1, 8, 1)
-        line["cpu_baseline"]["single_thread_value"] = 8 / step1()
+        step1, _ = cpu_nand_sample(args.seed + 1, 32, 1)
+        line["cpu_baseline"]["single_thread_value"] = 32 / step1()
     eng.close()
     return line
 

@@ -51,6 +51,9 @@ constexpr int kStagesPerPair = 3 * kRows;  // (row pair, component, row) stages 
 #ifndef HB_TRACE
 #define HB_TRACE 0  // per-phase clock64 trace of the cluster latency kernel (printf, one pair)
 #endif
+#ifndef HB_EXP_NO_BK_LDS
+#define HB_EXP_NO_BK_LDS 0
+#endif
 #ifndef HB_EXP_BK_SAME
 #define HB_EXP_BK_SAME 0  // timing experiment only (results wrong): every pair re-reads pair 0's stages
 #endif
@@ -233,17 +236,27 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
                     mbar_wait(&sm.full[s], (st / R) & 1);
                     const double2 *bk0 = sm.bk[s];
                     const double2 *bk1 = sm.bk[s] + kNH;
+#if HB_EXP_NO_BK_LDS  // timing experiment only (results wrong): one BK value per thread and stage
+                    const double2 b0c = bk0[t], b1c = bk1[t];
+#define HB_BK0(m) b0c
+#define HB_BK1(m) b1c
+#else
+#define HB_BK0(m) bk0[t + 64 * (m)]
+#define HB_BK1(m) bk1[t + 64 * (m)]
+#endif
 #pragma unroll
                     for (int m = 0; m < 8; m++) {
                         const double2 y = cmul(x[h][m], F[m]);
                         if (rp == 0 && c == 0 && h == 0) {
-                            f0[m] = cmul(y, bk0[t + 64 * m]);
-                            f1[m] = cmul(y, bk1[t + 64 * m]);
+                            f0[m] = cmul(y, HB_BK0(m));
+                            f1[m] = cmul(y, HB_BK1(m));
                         } else {
-                            cmac(f0[m], y, bk0[t + 64 * m]);
-                            cmac(f1[m], y, bk1[t + 64 * m]);
+                            cmac(f0[m], y, HB_BK0(m));
+                            cmac(f1[m], y, HB_BK1(m));
                         }
                     }
+#undef HB_BK0
+#undef HB_BK1
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&sm.empty[s]);
                     if (kMidIssue && threadIdx.x == 0) {  // shallow ring: refill behind consumption

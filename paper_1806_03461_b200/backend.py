@@ -72,7 +72,7 @@ class _Bit(CipherBit):
 
     def __del__(self):
         try:
-            self._ctx._drop(self._value >> 1)
+            self._ctx._dag.hdec(self._value >> 1)
         except Exception:  # interpreter shutdown
             pass
 
@@ -167,11 +167,17 @@ class TfheContext(GateBackend):
     keys:     an explicit `KeySet` (overrides ``seed``)
     stream_at: pending gates that start a background flush while the DAG is
               still being built (0 disables; flush points are unchanged)
+    stream_min_width: bootstraps a level needs in a background flush; narrower
+              levels (and the gates that depend on them) stay pending and
+              merge with later gates of the same level (the final flush runs
+              everything).  A narrow launch costs about as much as a full
+              wave, so this keeps streamed launches wide.  0 disables.
     """
 
     _CHUNK = 4096  # logical slots reserved at a time
 
-    def __init__(self, seed=0, device=0, lanes=1, enc_seed=None, keys=None, enc_stream=None, stream_at=16384):
+    def __init__(self, seed=0, device=0, lanes=1, enc_seed=None, keys=None, enc_stream=None, stream_at=16384,
+                 stream_min_width=592):
         if lanes < 1:
             raise ValueError("lanes must be >= 1")
         self.global_stats = GateStats(label="global")
@@ -198,6 +204,10 @@ class TfheContext(GateBackend):
         self._chunks = []
         self._finalizer = None
         self.stream_at = int(stream_at)  # pending gates that start a background flush (0: off)
+        self.stream_min_width = int(stream_min_width)
+        # gates between two streaming checks (a countdown instead of a native call per gate)
+        self._tick_every = max(1, min(256, self.stream_at // 8))
+        self._tick = self._tick_every
         self._bg = None
         self._bg_error = []
         # execution statistics
@@ -244,9 +254,6 @@ class TfheContext(GateBackend):
         """A handle on ref r (counted for the live-gate filter of flush)."""
         self._dag.hinc(r >> 1)
         return _Bit(self, r, level, trivial)
-
-    def _drop(self, nid):
-        self._dag.hdec(nid)
 
     def encrypt(self, b):
         """Fresh encryption of bit b (all lanes) — SimContext.encrypt, backend.py:178-181."""
@@ -405,8 +412,11 @@ class TfheContext(GateBackend):
             for scope in self._scopes:
                 scope.record(kind, level)
             r = self._dag.gate(_KIND[kind], a._value, b._value)  # counts the handle below
-            if self.stream_at and self._dag.pending_count() >= self.stream_at:
-                self._maybe_stream()
+            if self.stream_at:
+                self._tick -= 1
+                if self._tick <= 0:
+                    self._tick = self._tick_every
+                    self._maybe_stream()
             return _Bit(self, r, level)
 
     def g_and(self, a, b):
@@ -440,7 +450,10 @@ class TfheContext(GateBackend):
             self._record(MUX, level)
             r = self._dag.mux(s._value, a._value, b._value)  # counts the handle below
             if self.stream_at:
-                self._maybe_stream()
+                self._tick -= 1
+                if self._tick <= 0:
+                    self._tick = self._tick_every
+                    self._maybe_stream()
             return _Bit(self, r, level)
 
     # -- scoped stats (backend.py:241-257) --------------------------------------
@@ -550,6 +563,9 @@ class TfheContext(GateBackend):
             self._upload_inputs(eng, list(self._inputs), [self._inputs[nid] for nid in self._inputs])
             self._inputs.clear()
         pending = self._dag.live(True)  # the rest of the pending gates become dormant
+        if not wait and self.stream_min_width:
+            pending, deferred = self._select_wide(pending)
+            self._dag.requeue(deferred)
         if pending.size == 0:
             return
         batches = self._build_schedule(pending)
@@ -570,6 +586,28 @@ class TfheContext(GateBackend):
                                         daemon=True)
             self._bg.start()
         self.exec_stats["flush_s"] += time.perf_counter() - t0
+
+    def _select_wide(self, pending):
+        """Split a background flush's live pending gates into (run, deferred):
+        level by level, the gates whose operands are all done or run in this
+        flush run if there are at least `stream_min_width` bootstraps of them;
+        otherwise they, and everything depending on them, are deferred."""
+        if pending.size == 0:
+            return pending, pending
+        op, a, b, c, lvl = self._dag.gather(pending)
+        blocked = np.zeros(self._dag.size(), dtype=bool)
+        run = np.zeros(pending.size, dtype=bool)
+        order = np.argsort(lvl, kind="stable")
+        bounds = np.flatnonzero(np.diff(lvl[order])) + 1
+        cost = 1 + (op == _OP_MUX)  # bootstraps per record
+        for idx in np.split(order, bounds):
+            ok = ~(blocked[a[idx] >> 1] | blocked[b[idx] >> 1] | blocked[c[idx] >> 1])
+            if int(cost[idx][ok].sum()) * self.lanes >= self.stream_min_width:
+                run[idx[ok]] = True
+                blocked[pending[idx[~ok]]] = True
+            else:
+                blocked[pending[idx]] = True
+        return pending[run], pending[~run]
 
     def _upload_inputs(self, eng, nids, cts):
         """Host ciphertexts of input nodes -> their pool slots, one copy per run

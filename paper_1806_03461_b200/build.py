@@ -53,10 +53,10 @@ def dag_out():
 
 
 def build_dag(force=False):
-    """The host gate-DAG extension (pybind11, g++): csrc/hb_dag.cpp -> _lib/hb_dag*.so."""
+    """The host gate-DAG extension (CPython + numpy C API, g++): csrc/hb_dag.cpp -> _lib/hb_dag*.so."""
     import sysconfig
 
-    import pybind11
+    import numpy
 
     out, src = dag_out(), os.path.join(CSRC, "hb_dag.cpp")
     if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(src),
@@ -65,7 +65,7 @@ def build_dag(force=False):
     os.makedirs(os.path.dirname(out), exist_ok=True)
     cxx = shutil.which("g++") or "g++"
     cmd = [cxx, "-O2", "-std=c++17", "-shared", "-fPIC", "-fvisibility=hidden",
-           "-I", pybind11.get_include(), "-I", sysconfig.get_paths()["include"], src, "-o", out + ".tmp"]
+           "-I", numpy.get_include(), "-I", sysconfig.get_paths()["include"], src, "-o", out + ".tmp"]
     subprocess.run(cmd, check=True)
     os.replace(out + ".tmp", out)
     return out

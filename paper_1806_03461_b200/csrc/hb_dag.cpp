@@ -5,39 +5,85 @@
 // reference contract (handles, GateStats, scopes, errors) and the engine
 // calls; every gate of the reference API lands here once.
 //
+// Binding: the raw CPython API (vectorcall-style METH_FASTCALL methods, numpy
+// C API for the bulk arrays), so one gate costs one cheap native call rather
+// than a pybind11 dispatch (~0.3 us) — the host DAG build is on the critical
+// path of a BNN's first evaluation.
+//
 // Refs are (node << 1) | not_flag; node 0 is the constant 0 (ref 0 = false,
 // ref 1 = true).  Node operands: AND / MUX / MAJ store refs; XOR / XOR3 store
 // node << 1 and push NOT flags to the output ref.  Node n owns logical pool
 // slot n - 1.
-#include <pybind11/numpy.h>
-#include <pybind11/pybind11.h>
+#define PY_SSIZE_T_CLEAN
+#include <Python.h>
+#define NPY_NO_DEPRECATED_API NPY_1_7_API_VERSION
+#include <numpy/arrayobject.h>
 
 #include <algorithm>
 #include <array>
 #include <cstdint>
-#include <unordered_map>
 #include <vector>
 
-namespace py = pybind11;
-
 namespace {
+
+struct IndexErr {};  // node id out of range -> IndexError
 
 enum Op : int8_t { CONST = 0, INPUT = 1, AND = 2, XOR = 3, MUX = 4, MAJ = 5, XOR3 = 6 };
 enum State : uint8_t { PENDING = 0, DONE = 1, DORMANT = 2 };
 // gate kinds of the reference API (hebnn.backend AND/OR/XOR/XNOR)
 enum Kind : int { K_AND = 0, K_OR = 1, K_XOR = 2, K_XNOR = 3 };
 
-struct Key {
-    int64_t op, a, b, c;
-    bool operator==(const Key &o) const { return op == o.op && a == o.a && b == o.b && c == o.c; }
-};
-struct KeyHash {
-    size_t operator()(const Key &k) const {
-        uint64_t h = (uint64_t)k.op * 0x9E3779B97F4A7C15ull;
-        for (int64_t v : {k.a, k.b, k.c}) {
-            h ^= (uint64_t)v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+// Hash-consing table: open addressing with linear probing over a flat,
+// power-of-two array (load <= 1/2), keyed by (op, a, b, c) refs.  A flat
+// table keeps a lookup at ~one cache line; a node-based std::unordered_map
+// cost ~0.6 us per gate on the cfg2l DAG (565k nodes).
+class CseTable {
+  public:
+    CseTable() : slots_(1u << 12) {}
+
+    // node id of the key, or -1
+    int64_t find(int8_t op, int64_t a, int64_t b, int64_t c) const {
+        const size_t mask = slots_.size() - 1;
+        for (size_t i = hash(op, a, b, c) & mask;; i = (i + 1) & mask) {
+            const Slot &e = slots_[i];
+            if (e.node < 0) return -1;
+            if (e.op == op && e.a == a && e.b == b && e.c == c) return e.node;
         }
-        return (size_t)h;
+    }
+
+    void insert(int8_t op, int64_t a, int64_t b, int64_t c, int64_t node) {
+        if (2 * (used_ + 1) > slots_.size()) grow();
+        place(Slot{a, b, c, node, op});
+        used_++;
+    }
+
+  private:
+    struct Slot {
+        int64_t a = 0, b = 0, c = 0;
+        int64_t node = -1;
+        int8_t op = 0;
+    };
+    std::vector<Slot> slots_;
+    size_t used_ = 0;
+
+    static size_t hash(int8_t op, int64_t a, int64_t b, int64_t c) {
+        uint64_t h = (uint64_t)a * 0x9E3779B97F4A7C15ull;
+        h ^= (uint64_t)b * 0xC2B2AE3D27D4EB4Full + (h >> 29);
+        h ^= (uint64_t)c * 0x165667B19E3779F9ull + (uint64_t)op + (h >> 32);
+        h *= 0xD6E8FEB86659FD93ull;
+        return (size_t)(h ^ (h >> 32));
+    }
+    void place(const Slot &s) {
+        const size_t mask = slots_.size() - 1;
+        size_t i = hash(s.op, s.a, s.b, s.c) & mask;
+        while (slots_[i].node >= 0) i = (i + 1) & mask;
+        slots_[i] = s;
+    }
+    void grow() {
+        std::vector<Slot> old(slots_.size() * 2);
+        old.swap(slots_);
+        for (const Slot &s : old)
+            if (s.node >= 0) place(s);
     }
 };
 
@@ -96,7 +142,7 @@ class Dag {
 
     // pending nodes reachable from live handles through pending operands, in
     // pending order; with take: the rest become dormant and pending empties
-    py::array_t<int64_t> live(bool take) {
+    std::vector<int64_t> live(bool take) {
         const uint32_t ep = ++epoch_;
         if (mark_.size() < op_.size()) mark_.resize(op_.size(), 0);
         std::vector<int64_t> stack;
@@ -123,34 +169,33 @@ class Dag {
             }
         }
         if (take) pending_.clear();
-        return to_array(out);
+        return out;
     }
 
-    py::array_t<int64_t> pending() const { return to_array(pending_); }
+    const std::vector<int64_t> &pending() const { return pending_; }
 
-    void mark_done(py::array_t<int64_t, py::array::c_style | py::array::forcecast> ids) {
-        auto v = ids.unchecked<1>();
-        for (py::ssize_t i = 0; i < v.shape(0); i++) state_[check(v(i))] = DONE;
+    // pending nodes taken by live(true) but not run: back into the pending list
+    void requeue(const int64_t *ids, int64_t n) {
+        for (int64_t i = 0; i < n; i++)
+            if (state_[check(ids[i])] != PENDING) throw IndexErr{};
+        pending_.insert(pending_.end(), ids, ids + n);
     }
 
-    // node fields of ids: (op int8, a, b, c int64 refs, lvl int64)
-    py::tuple gather(py::array_t<int64_t, py::array::c_style | py::array::forcecast> ids) const {
-        auto v = ids.unchecked<1>();
-        const py::ssize_t n = v.shape(0);
-        py::array_t<int8_t> o(n);
-        py::array_t<int64_t> a(n), b(n), c(n), l(n);
-        auto O = o.mutable_unchecked<1>();
-        auto A = a.mutable_unchecked<1>(), B = b.mutable_unchecked<1>(), C = c.mutable_unchecked<1>();
-        auto L = l.mutable_unchecked<1>();
-        for (py::ssize_t i = 0; i < n; i++) {
-            const int64_t k = check(v(i));
-            O(i) = op_[k];
-            A(i) = a_[k];
-            B(i) = b_[k];
-            C(i) = c_[k];
-            L(i) = lvl_[k];
+    void mark_done(const int64_t *ids, int64_t n) {
+        for (int64_t i = 0; i < n; i++) check(ids[i]);
+        for (int64_t i = 0; i < n; i++) state_[ids[i]] = DONE;
+    }
+
+    // node fields of ids: op int8, a, b, c int64 refs, lvl int64
+    void gather(const int64_t *ids, int64_t n, int8_t *o, int64_t *a, int64_t *b, int64_t *c, int64_t *l) const {
+        for (int64_t i = 0; i < n; i++) {
+            const int64_t k = check(ids[i]);
+            o[i] = op_[k];
+            a[i] = a_[k];
+            b[i] = b_[k];
+            c[i] = c_[k];
+            l[i] = lvl_[k];
         }
-        return py::make_tuple(o, a, b, c, l);
     }
 
   private:
@@ -162,19 +207,13 @@ class Dag {
     std::vector<int64_t> pending_;
     std::vector<uint32_t> mark_;
     uint32_t epoch_ = 0;
-    std::unordered_map<Key, int64_t, KeyHash> cse_;
+    CseTable cse_;
 
     int64_t check(int64_t n) const {
-        if (n < 0 || n >= (int64_t)op_.size()) throw py::index_error("gate DAG: node id out of range");
+        if (n < 0 || n >= (int64_t)op_.size()) throw IndexErr{};
         return n;
     }
     void check_ref(int64_t r) const { check(r >> 1); }
-
-    static py::array_t<int64_t> to_array(const std::vector<int64_t> &v) {
-        py::array_t<int64_t> out((py::ssize_t)v.size());
-        std::copy(v.begin(), v.end(), out.mutable_data());
-        return out;
-    }
 
     int64_t push(int8_t op, int64_t a, int64_t b, int64_t c, int32_t lvl, uint8_t state) {
         const int64_t n = (int64_t)op_.size();
@@ -190,17 +229,16 @@ class Dag {
 
     // CSE lookup or a new pending node; dormant hits and dormant operands revive
     int64_t node(int8_t op, int64_t a, int64_t b, int64_t c, int32_t lvl) {
-        const Key key{op, a, b, c};
-        auto it = cse_.find(key);
-        if (it != cse_.end()) {
-            if (state_[it->second] == DORMANT) revive(it->second);
-            return it->second;
+        const int64_t hit = cse_.find(op, a, b, c);
+        if (hit >= 0) {
+            if (state_[hit] == DORMANT) revive(hit);
+            return hit;
         }
         for (int64_t r : {a, b, c})
             if (state_[r >> 1] == DORMANT) revive(r >> 1);
         const int64_t n = push(op, a, b, c, lvl, PENDING);
         pending_.push_back(n);
-        cse_.emplace(key, n);
+        cse_.insert(op, a, b, c, n);
         return n;
     }
 
@@ -306,31 +344,245 @@ class Dag {
 
 }  // namespace
 
-PYBIND11_MODULE(hb_dag, m) {
-    m.doc() = "native gate DAG of paper_1806_03461_b200.backend.TfheContext";
-    m.attr("OP_CONST") = (int)CONST;
-    m.attr("OP_INPUT") = (int)INPUT;
-    m.attr("OP_AND") = (int)AND;
-    m.attr("OP_XOR") = (int)XOR;
-    m.attr("OP_MUX") = (int)MUX;
-    m.attr("OP_MAJ") = (int)MAJ;
-    m.attr("OP_XOR3") = (int)XOR3;
-    py::class_<Dag>(m, "Dag")
-        .def(py::init<>())
-        .def("size", &Dag::size)
-        .def("pending_count", &Dag::pending_count)
-        .def("add_input", &Dag::add_input)
-        .def("gate", &Dag::gate)
-        .def("mux", &Dag::mux)
-        .def("hinc", &Dag::hinc)
-        .def("hdec", &Dag::hdec)
-        .def("hcount", &Dag::hcount)
-        .def("op", &Dag::op)
-        .def("is_done", &Dag::is_done)
-        .def("is_dormant", &Dag::is_dormant)
-        .def("revive", &Dag::revive)
-        .def("live", &Dag::live, py::arg("take"))
-        .def("pending", &Dag::pending)
-        .def("mark_done", &Dag::mark_done)
-        .def("gather", &Dag::gather);
+// ---------------------------------------------------------------------------
+// CPython binding
+// ---------------------------------------------------------------------------
+namespace {
+
+struct PyDag {
+    PyObject_HEAD
+    Dag *dag;
+};
+
+PyObject *index_error() {
+    PyErr_SetString(PyExc_IndexError, "gate DAG: node id out of range");
+    return nullptr;
+}
+
+bool args_i64(PyObject *const *args, Py_ssize_t nargs, Py_ssize_t want, int64_t *out, const char *name) {
+    if (nargs != want) {
+        PyErr_Format(PyExc_TypeError, "Dag.%s() takes %zd arguments (%zd given)", name, want, nargs);
+        return false;
+    }
+    for (Py_ssize_t i = 0; i < want; i++) {
+        const long long v = PyLong_AsLongLong(args[i]);
+        if (v == -1 && PyErr_Occurred()) return false;
+        out[i] = (int64_t)v;
+    }
+    return true;
+}
+
+PyObject *to_array(const std::vector<int64_t> &v) {
+    npy_intp dims[1] = {(npy_intp)v.size()};
+    PyObject *arr = PyArray_SimpleNew(1, dims, NPY_INT64);
+    if (arr && !v.empty()) std::copy(v.begin(), v.end(), (int64_t *)PyArray_DATA((PyArrayObject *)arr));
+    return arr;
+}
+
+// int64 C-contiguous view of a 1-d array-like (new reference)
+PyArrayObject *as_ids(PyObject *obj) {
+    return (PyArrayObject *)PyArray_FROMANY(obj, NPY_INT64, 1, 1, NPY_ARRAY_IN_ARRAY | NPY_ARRAY_FORCECAST);
+}
+
+PyObject *Dag_new(PyTypeObject *type, PyObject *, PyObject *) {
+    PyDag *self = (PyDag *)type->tp_alloc(type, 0);
+    if (!self) return nullptr;
+    try {
+        self->dag = new Dag();
+    } catch (const std::bad_alloc &) {
+        Py_DECREF(self);
+        return PyErr_NoMemory();
+    }
+    return (PyObject *)self;
+}
+
+void Dag_dealloc(PyDag *self) {
+    delete self->dag;
+    Py_TYPE(self)->tp_free((PyObject *)self);
+}
+
+#define HB_DAG_TRY(expr)                     \
+    try {                                    \
+        expr;                                \
+    } catch (const IndexErr &) {             \
+        return index_error();                \
+    } catch (const std::bad_alloc &) {       \
+        return PyErr_NoMemory();             \
+    }
+
+PyObject *Dag_size(PyDag *self, PyObject *) { return PyLong_FromLongLong(self->dag->size()); }
+PyObject *Dag_pending_count(PyDag *self, PyObject *) { return PyLong_FromLongLong(self->dag->pending_count()); }
+PyObject *Dag_add_input(PyDag *self, PyObject *) {
+    int64_t r;
+    HB_DAG_TRY(r = self->dag->add_input());
+    return PyLong_FromLongLong(r);
+}
+
+PyObject *Dag_gate(PyDag *self, PyObject *const *args, Py_ssize_t nargs) {
+    int64_t v[3];
+    if (!args_i64(args, nargs, 3, v, "gate")) return nullptr;
+    int64_t r;
+    HB_DAG_TRY(r = self->dag->gate((int)v[0], v[1], v[2]));
+    return PyLong_FromLongLong(r);
+}
+
+PyObject *Dag_mux(PyDag *self, PyObject *const *args, Py_ssize_t nargs) {
+    int64_t v[3];
+    if (!args_i64(args, nargs, 3, v, "mux")) return nullptr;
+    int64_t r;
+    HB_DAG_TRY(r = self->dag->mux(v[0], v[1], v[2]));
+    return PyLong_FromLongLong(r);
+}
+
+// one-argument node methods
+template <typename F>
+PyObject *node_call(PyDag *self, PyObject *arg, F f) {
+    const long long n = PyLong_AsLongLong(arg);
+    if (n == -1 && PyErr_Occurred()) return nullptr;
+    HB_DAG_TRY(return f(self->dag, (int64_t)n));
+}
+
+PyObject *Dag_hinc(PyDag *self, PyObject *arg) {
+    return node_call(self, arg, [](Dag *d, int64_t n) { d->hinc(n); Py_RETURN_NONE; });
+}
+PyObject *Dag_hdec(PyDag *self, PyObject *arg) {
+    return node_call(self, arg, [](Dag *d, int64_t n) { d->hdec(n); Py_RETURN_NONE; });
+}
+PyObject *Dag_hcount(PyDag *self, PyObject *arg) {
+    return node_call(self, arg, [](Dag *d, int64_t n) { return PyLong_FromLong(d->hcount(n)); });
+}
+PyObject *Dag_op(PyDag *self, PyObject *arg) {
+    return node_call(self, arg, [](Dag *d, int64_t n) { return PyLong_FromLong(d->op(n)); });
+}
+PyObject *Dag_is_done(PyDag *self, PyObject *arg) {
+    return node_call(self, arg, [](Dag *d, int64_t n) { return PyBool_FromLong(d->is_done(n)); });
+}
+PyObject *Dag_is_dormant(PyDag *self, PyObject *arg) {
+    return node_call(self, arg, [](Dag *d, int64_t n) { return PyBool_FromLong(d->is_dormant(n)); });
+}
+PyObject *Dag_revive(PyDag *self, PyObject *arg) {
+    return node_call(self, arg, [](Dag *d, int64_t n) { d->revive(n); Py_RETURN_NONE; });
+}
+
+PyObject *Dag_live(PyDag *self, PyObject *args, PyObject *kwds) {
+    static const char *kwlist[] = {"take", nullptr};
+    int take = 0;
+    if (!PyArg_ParseTupleAndKeywords(args, kwds, "p", (char **)kwlist, &take)) return nullptr;
+    HB_DAG_TRY(return to_array(self->dag->live(take != 0)));
+}
+
+PyObject *Dag_pending(PyDag *self, PyObject *) { HB_DAG_TRY(return to_array(self->dag->pending())); }
+
+PyObject *Dag_mark_done(PyDag *self, PyObject *arg) {
+    PyArrayObject *ids = as_ids(arg);
+    if (!ids) return nullptr;
+    try {
+        self->dag->mark_done((const int64_t *)PyArray_DATA(ids), (int64_t)PyArray_SIZE(ids));
+    } catch (const IndexErr &) {
+        Py_DECREF(ids);
+        return index_error();
+    }
+    Py_DECREF(ids);
+    Py_RETURN_NONE;
+}
+
+PyObject *Dag_requeue(PyDag *self, PyObject *arg) {
+    PyArrayObject *ids = as_ids(arg);
+    if (!ids) return nullptr;
+    try {
+        self->dag->requeue((const int64_t *)PyArray_DATA(ids), (int64_t)PyArray_SIZE(ids));
+    } catch (const IndexErr &) {
+        Py_DECREF(ids);
+        PyErr_SetString(PyExc_IndexError, "gate DAG: requeue of a node that is not pending");
+        return nullptr;
+    }
+    Py_DECREF(ids);
+    Py_RETURN_NONE;
+}
+
+PyObject *Dag_gather(PyDag *self, PyObject *arg) {
+    PyArrayObject *ids = as_ids(arg);
+    if (!ids) return nullptr;
+    npy_intp dims[1] = {PyArray_SIZE(ids)};
+    PyObject *o = PyArray_SimpleNew(1, dims, NPY_INT8);
+    PyObject *a = PyArray_SimpleNew(1, dims, NPY_INT64), *b = PyArray_SimpleNew(1, dims, NPY_INT64);
+    PyObject *c = PyArray_SimpleNew(1, dims, NPY_INT64), *l = PyArray_SimpleNew(1, dims, NPY_INT64);
+    PyObject *res = nullptr;
+    if (o && a && b && c && l) {
+        try {
+            self->dag->gather((const int64_t *)PyArray_DATA(ids), (int64_t)dims[0],
+                              (int8_t *)PyArray_DATA((PyArrayObject *)o), (int64_t *)PyArray_DATA((PyArrayObject *)a),
+                              (int64_t *)PyArray_DATA((PyArrayObject *)b), (int64_t *)PyArray_DATA((PyArrayObject *)c),
+                              (int64_t *)PyArray_DATA((PyArrayObject *)l));
+            res = PyTuple_Pack(5, o, a, b, c, l);
+        } catch (const IndexErr &) {
+            index_error();
+        }
+    }
+    Py_DECREF(ids);
+    Py_XDECREF(o);
+    Py_XDECREF(a);
+    Py_XDECREF(b);
+    Py_XDECREF(c);
+    Py_XDECREF(l);
+    return res;
+}
+
+PyMethodDef Dag_methods[] = {
+    {"size", (PyCFunction)Dag_size, METH_NOARGS, "number of nodes (node 0 is the constant)"},
+    {"pending_count", (PyCFunction)Dag_pending_count, METH_NOARGS, "pending (not yet executed) nodes"},
+    {"add_input", (PyCFunction)Dag_add_input, METH_NOARGS, "new input node id"},
+    {"gate", (PyCFunction)(void (*)(void))Dag_gate, METH_FASTCALL,
+     "gate(kind, ref_a, ref_b) -> ref of a 2-input gate of the reference API (counts one live handle)"},
+    {"mux", (PyCFunction)(void (*)(void))Dag_mux, METH_FASTCALL,
+     "mux(ref_s, ref_a, ref_b) -> ref of s ? a : b (counts one live handle)"},
+    {"hinc", (PyCFunction)Dag_hinc, METH_O, "one more live handle on node n"},
+    {"hdec", (PyCFunction)Dag_hdec, METH_O, "one live handle fewer on node n"},
+    {"hcount", (PyCFunction)Dag_hcount, METH_O, "live handles on node n"},
+    {"op", (PyCFunction)Dag_op, METH_O, "op code of node n"},
+    {"is_done", (PyCFunction)Dag_is_done, METH_O, "node n executed"},
+    {"is_dormant", (PyCFunction)Dag_is_dormant, METH_O, "node n skipped by a flush (unreachable then)"},
+    {"revive", (PyCFunction)Dag_revive, METH_O, "dormant node n (and dormant operands) back to pending"},
+    {"live", (PyCFunction)(void (*)(void))Dag_live, METH_VARARGS | METH_KEYWORDS,
+     "live(take) -> int64 ids of pending nodes reachable from live handles"},
+    {"pending", (PyCFunction)Dag_pending, METH_NOARGS, "int64 ids of pending nodes"},
+    {"mark_done", (PyCFunction)Dag_mark_done, METH_O, "mark node ids executed"},
+    {"requeue", (PyCFunction)Dag_requeue, METH_O, "pending node ids taken by live(True) but not run"},
+    {"gather", (PyCFunction)Dag_gather, METH_O, "gather(ids) -> (op int8, a, b, c, lvl int64 arrays)"},
+    {nullptr, nullptr, 0, nullptr}};
+
+PyTypeObject DagType = {PyVarObject_HEAD_INIT(nullptr, 0)};
+
+PyModuleDef dag_module = {PyModuleDef_HEAD_INIT, "hb_dag",
+                          "native gate DAG of paper_1806_03461_b200.backend.TfheContext", -1, nullptr};
+
+}  // namespace
+
+PyMODINIT_FUNC PyInit_hb_dag(void) {
+    import_array();
+    DagType.tp_name = "hb_dag.Dag";
+    DagType.tp_basicsize = sizeof(PyDag);
+    DagType.tp_flags = Py_TPFLAGS_DEFAULT;
+    DagType.tp_doc = "gate DAG: node store, elision, CSE, full-adder fusion, live-handle filter";
+    DagType.tp_new = Dag_new;
+    DagType.tp_dealloc = (destructor)Dag_dealloc;
+    DagType.tp_methods = Dag_methods;
+    if (PyType_Ready(&DagType) < 0) return nullptr;
+    PyObject *m = PyModule_Create(&dag_module);
+    if (!m) return nullptr;
+    Py_INCREF(&DagType);
+    if (PyModule_AddObject(m, "Dag", (PyObject *)&DagType) < 0) {
+        Py_DECREF(&DagType);
+        Py_DECREF(m);
+        return nullptr;
+    }
+    const std::pair<const char *, int> ops[] = {{"OP_CONST", CONST}, {"OP_INPUT", INPUT}, {"OP_AND", AND},
+                                                {"OP_XOR", XOR},     {"OP_MUX", MUX},     {"OP_MAJ", MAJ},
+                                                {"OP_XOR3", XOR3}};
+    for (const auto &kv : ops)
+        if (PyModule_AddIntConstant(m, kv.first, kv.second) < 0) {
+            Py_DECREF(m);
+            return nullptr;
+        }
+    return m;
 }

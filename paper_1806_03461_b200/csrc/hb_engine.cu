@@ -160,26 +160,35 @@ int launch_br_lat(hb_engine *e, const BrArgs &a) {
     return HB_OK;
 }
 
-// narrow levels (<= kKsNarrow key switches): the coefficient range is split
-// over kKsSplits CTAs per column chunk and the partial sums are reduced
-constexpr uint32_t kKsNarrow = 32;
-constexpr int kKsSplits = 8;
+// narrow levels: the coefficient range is split over `splits` CTAs per column
+// chunk (8, 4 or 2, so that a level launches >= ~640 CTAs) and the partial
+// sums are reduced by k_keyswitch_reduce
+constexpr int kKsMaxSplits = 8;
+constexpr uint32_t kKsTargetCtas = 8 * kKsChunks;
+
+int ks_splits(uint32_t n_work) {
+    const uint32_t ctas = ((n_work + kKsThreads - 1) / kKsThreads) * kKsChunks;
+    int s = 1;
+    while (s < kKsMaxSplits && ctas * (uint32_t)(2 * s) <= kKsTargetCtas) s *= 2;
+    return s;
+}
 
 int launch_ks(hb_engine *e, const KsArgs &a0) {
     KsArgs a = a0;
-    const bool narrow = a.n_work <= kKsNarrow;
+    const int splits = ks_splits(a.n_work);
+    const bool narrow = splits > 1;
     if (narrow) {
-        int rc = ensure_dev((void **)&e->d_kspart, &e->kspart_cap, (size_t)kKsSplits * a.n_work * kKskStride,
+        int rc = ensure_dev((void **)&e->d_kspart, &e->kspart_cap, (size_t)splits * a.n_work * kKskStride,
                             sizeof(uint32_t), false, e->stream);
         if (rc) return rc;
         a.partial = e->d_kspart;
     }
-    const dim3 grid((a.n_work + kKsThreads - 1) / kKsThreads, kKsChunks, narrow ? kKsSplits : 1);
+    const dim3 grid((a.n_work + kKsThreads - 1) / kKsThreads, kKsChunks, splits);
     k_keyswitch<<<grid, kKsThreads, 0, e->stream>>>(a);
     HB_CUDA_TRY(cudaGetLastError());
     e->n_launch++;
     if (narrow) {
-        k_keyswitch_reduce<<<a.n_work, kKskStride, 0, e->stream>>>(a, kKsSplits);
+        k_keyswitch_reduce<<<a.n_work, kKskStride, 0, e->stream>>>(a, splits);
         HB_CUDA_TRY(cudaGetLastError());
         e->n_launch++;
     }

@@ -47,7 +47,12 @@ for rep in sorted(f for f in os.listdir(src) if f.endswith(".ncu-rep")):
         tmult = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
         ti = h.index("gpu__time_duration.sum")
         dur = float(v[ti]) * tmult.get(units[ti], 1e-3)
-        hbm = 6547.5  # MEASURED_PEAKS.json hbm_gbs
+        try:  # driver-written, per pod
+            import json
+            hbm = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                              "MEASURED_PEAKS.json")))["hbm_gbs"]
+        except (OSError, KeyError, ValueError):
+            hbm = 6547.5  # B200_PROFILING.md fallback
         lines.insert(-1, f"- DRAM bandwidth: {(rd + wr) / dur / 1e9:.1f} GB/s = {100 * (rd + wr) / dur / 1e9 / hbm:.2f}% "
                          f"of the measured {hbm} GB/s")
 launch = os.path.join(src, "launches.csv")

@@ -121,7 +121,7 @@ def test_streaming_flush_matches_single_flush():
     vals = rng.integers(0, 2, 300).tolist()
     res = []
     for stream_at in (0, 200):
-        ctx = Ctx(seed=13, stream_at=stream_at)
+        ctx = Ctx(seed=13, stream_at=stream_at, stream_min_width=0)
         bits = [ctx.encrypt(v) for v in vals]
         w = reduce_tree_sum(bits)
         x = rc_add(w, encrypt_word(ctx, 77, w.width))
@@ -137,7 +137,7 @@ def test_concurrent_gate_issue_with_streaming():
     backend.py:174,200) while background flushes run (small stream_at)."""
     import threading
 
-    ctx = Ctx(seed=21, stream_at=64)
+    ctx = Ctx(seed=21, stream_at=64, stream_min_width=0)
     rng = np.random.default_rng(5)
     data = [rng.integers(0, 2, 40).tolist() for _ in range(4)]
     results = {}
@@ -154,3 +154,43 @@ def test_concurrent_gate_issue_with_streaming():
     for i in range(4):
         assert decrypt_word(results[i]) == sum(data[i])
     assert ctx.exec_stats["flushes"] > 1
+
+
+def test_streaming_defers_narrow_levels():
+    """stream_min_width: a background flush runs only levels with enough
+    bootstraps whose operands are done or run with them; the rest stay
+    pending (values and stats unchanged, fewer and wider launches)."""
+    rng = np.random.default_rng(31)
+    vals = [rng.integers(0, 2, 120).tolist() for _ in range(6)]
+    res = []
+    for width in (0, 24):
+        ctx = Ctx(seed=17, stream_at=150, stream_min_width=width)
+        words = []
+        for v in vals:
+            words.append(reduce_tree_sum([ctx.encrypt(x) for x in v]))
+        got = [decrypt_word(w) for w in words]
+        res.append((got, ctx.global_stats.as_dict(), ctx.exec_stats["levels"], ctx.exec_stats["flushes"]))
+    assert res[0][:2] == res[1][:2] and res[0][0] == [sum(v) for v in vals]
+    assert res[1][3] > 1                 # background flushes still happened
+    assert res[1][2] < res[0][2]         # and the narrow levels were merged
+
+
+def test_select_wide_respects_dependencies():
+    """Every gate _select_wide runs has its operands done or run with it, every
+    run level is wide enough, and run + deferred is the live pending set."""
+    ctx = Ctx(seed=19, stream_at=0, stream_min_width=20)
+    rng = np.random.default_rng(4)
+    words = [reduce_tree_sum([ctx.encrypt(int(x)) for x in rng.integers(0, 2, n)]) for n in (90, 40, 7)]
+    dag = ctx._dag
+    live = dag.live(False)
+    run, deferred = ctx._select_wide(live)
+    assert sorted(np.concatenate([run, deferred]).tolist()) == sorted(live.tolist())
+    assert run.size > 0 and deferred.size > 0
+    runset = set(run.tolist())
+    op, a, b, c, lvl = dag.gather(run)
+    for x in (a, b, c):
+        for m in (x >> 1).tolist():
+            assert m == 0 or dag.is_done(m) or m in runset
+    _, counts = np.unique(lvl, return_counts=True)
+    assert counts.min() >= 20
+    assert words

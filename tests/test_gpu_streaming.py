@@ -21,13 +21,14 @@ def test_streaming_flush_bit_identical():
     model = validate_model(TernaryModel(d, (DenseLayer(rows, (0,) * p), SignActivation()), "sign_bits"))
     xs = [rng.choice((0, 1)) for _ in range(d)]
     outs = []
-    for stream_at in (0, 300):
-        ctx = TfheContext(seed=42, enc_stream=77, stream_at=stream_at)
+    for stream_at, width in ((0, 0), (300, 0), (300, 64)):
+        ctx = TfheContext(seed=42, enc_stream=77, stream_at=stream_at, stream_min_width=width)
         handles = [ctx.encrypt(v) for v in xs]
         res, _ = eval_model(ctx, model, handles)
         outs.append((ctx.export_ciphertexts(res), [ctx.decrypt(h) for h in res], ctx.exec_stats["flushes"]))
-    assert np.array_equal(outs[0][0], outs[1][0])
-    assert outs[0][1] == outs[1][1]
+    for o in outs[1:]:  # streamed (all levels / wide levels only) == one flush, bit for bit
+        assert np.array_equal(outs[0][0], o[0])
+        assert outs[0][1] == o[1]
     want = oracle_eval(model, [1 if v else -1 for v in xs])
     assert [1 if b else -1 for b in outs[0][1]] == want
     assert outs[1][2] > outs[0][2]

@@ -39,7 +39,10 @@ struct KsArgs {
 
 constexpr int kKsCols = 8;                               // output columns per chunk
 constexpr int kKsChunks = kKskStride / kKsCols;           // 80
-constexpr int kKsThreads = 128;                           // one gate per thread
+#ifndef HB_KS_THREADS
+#define HB_KS_THREADS 128
+#endif
+constexpr int kKsThreads = HB_KS_THREADS;                 // one gate per thread
 constexpr int kKsRowsPerI = HB_KS_PAIR ? (kKsT / 2) * 16 : kKsT * 4;  // table rows per coefficient
 constexpr int kKsIBlock = HB_KS_PAIR ? 4 : 8;             // coefficients per ring stage
 constexpr uint32_t kKsStageBytes = kKsIBlock * kKsRowsPerI * kKsCols * 4;  // 8 KiB

@@ -68,6 +68,13 @@ typedef struct hb_params {
  *                      one bootstrap for 3-input threshold gates, e.g. majority
  *                      (c0 0, 1 1 1: a full adder's carry) and 3-input XOR
  *                      (c0 0, -2 -2 -2: a full adder's sum).
+ *   kind HB_GATE_HA  : half adder from ONE blind rotation of
+ *                      psi = (0,c0) + alpha*pool[src_a] + beta*pool[src_b], c0 = -1/8
+ *                      (the AND of the literals alpha*A, beta*B); the accumulator
+ *                      is extracted at index 0 (S0) and N/2 (S1):
+ *                        pool[dst]   = KS(S0)                                 (AND)
+ *                        pool[src_c] = KS(gamma (S1 - S0) + (0, -gamma/8))     (XOR,
+ *                      gamma = +1; gamma = -1 its negation).  2 key switches.
  * Slot numbers address the engine pool; with `lanes` > 1 every record is run
  * for lanes l = 0..lanes-1 on slots (slot * lanes + l). */
 typedef struct hb_gate {
@@ -79,6 +86,7 @@ typedef struct hb_gate {
 #define HB_GATE_LIN2 0
 #define HB_GATE_MUX 1
 #define HB_GATE_LIN3 2
+#define HB_GATE_HA 3
 
 typedef struct hb_engine hb_engine;
 

@@ -616,6 +616,15 @@ static void sample_extract(int N, int k, const uint32_t *acc, uint32_t *out) {
     out[(size_t)k * N] = acc[(size_t)k * N];
 }
 
+/* SampleExtract at index j: a'_i = A_{j-i} (i <= j), -A_{N+j-i} (i > j); b' = B_j */
+static void sample_extract_at(int N, int k, const uint32_t *acc, int j, uint32_t *out) {
+    for (int q = 0; q < k; q++) {
+        const uint32_t *A = acc + (size_t)q * N;
+        for (int i = 0; i < N; i++) out[(size_t)q * N + i] = i <= j ? A[j - i] : 0u - A[N + j - i];
+    }
+    out[(size_t)k * N] = acc[(size_t)k * N + j];
+}
+
 void or_bootstrap_wo_ks(const or_ctx *c, const uint32_t *lwe, uint32_t mu, uint32_t *out) {
     const int N = c->p.N, kp1 = c->p.k + 1;
     uint32_t *acc = malloc(sizeof(uint32_t) * (size_t)kp1 * N);
@@ -678,6 +687,32 @@ void or_gate3(const or_ctx *c, uint32_t c0, int32_t alpha, const uint32_t *A, in
     free(lin); free(big);
 }
 
+/* Half adder from one blind rotation (hb_gate kind HA): psi = (0,c0) + alpha*A + beta*B
+ * with c0 = -1/8 is the AND of the literals (alpha A, beta B).  The accumulator
+ * X^{-psi} * (mu...mu) is extracted twice: at index 0 (S0 = +-1/8 by psi in
+ * [0, 1/2): the AND) and at index N/2 (S1 = +-1/8 by psi in [-1/4, 1/4)).  Over the
+ * three phases psi in {-3/8, -1/8, 1/8} of the literal sum, S1 - S0 - 1/8 is the XOR
+ * of the literals; sigma = +-1 orients it:
+ *   out_and = KS(S0),  out_xor = KS(sigma (S1 - S0) + (0, -sigma/8)). */
+void or_half_adder(const or_ctx *c, uint32_t c0, int32_t alpha, const uint32_t *A, int32_t beta,
+                   const uint32_t *B, int32_t sigma, uint32_t *out_and, uint32_t *out_xor) {
+    const int n = c->p.n, N = c->p.N, kp1 = c->p.k + 1, nb = c->p.k * c->p.N;
+    const uint32_t eighth = 1u << 29;
+    uint32_t *lin = malloc(sizeof(uint32_t) * (n + 1));
+    uint32_t *acc = malloc(sizeof(uint32_t) * (size_t)kp1 * N);
+    uint32_t *s0 = malloc(sizeof(uint32_t) * (nb + 1));
+    uint32_t *s1 = malloc(sizeof(uint32_t) * (nb + 1));
+    lin_comb(n, c0, alpha, A, beta, B, lin);
+    or_blind_rotate(c, lin, eighth, n, acc);
+    sample_extract_at(N, c->p.k, acc, 0, s0);
+    sample_extract_at(N, c->p.k, acc, N / 2, s1);
+    or_keyswitch(c, s0, out_and);
+    for (int i = 0; i <= nb; i++) s1[i] = sigma > 0 ? s1[i] - s0[i] : s0[i] - s1[i];
+    s1[nb] += sigma > 0 ? 0u - eighth : eighth;
+    or_keyswitch(c, s1, out_xor);
+    free(lin); free(acc); free(s0); free(s1);
+}
+
 void or_mux(const or_ctx *c, const uint32_t *S, const uint32_t *A, const uint32_t *B,
             uint32_t *out) {
     const int n = c->p.n, nb = c->p.k * c->p.N;
@@ -727,6 +762,9 @@ static void run_one(const or_ctx *c, const or_gate_rec *g, uint32_t *pool, size_
         or_keyswitch(c, u1, dst);
     } else if (g->kind == 2) {
         or_gate3(c, g->c0, g->alpha, A, g->beta, B, g->gamma, pool + (size_t)g->src_c * stride, dst);
+    } else if (g->kind == 3) {
+        /* HA: dst = AND of the literals, src_c = their XOR (gamma = orientation) */
+        or_half_adder(c, g->c0, g->alpha, A, g->beta, B, g->gamma, dst, pool + (size_t)g->src_c * stride);
     } else {
         or_gate(c, g->c0, g->alpha, A, g->beta, g->beta ? B : NULL, dst);
     }

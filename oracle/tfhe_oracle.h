@@ -103,6 +103,11 @@ void or_gate(const or_ctx *c, uint32_t c0, int32_t alpha, const uint32_t *A, int
 /* Three-input bootstrapped threshold gate: out = KS(BS((0,c0) + alpha*A + beta*B + gamma*C)). */
 void or_gate3(const or_ctx *c, uint32_t c0, int32_t alpha, const uint32_t *A, int32_t beta,
               const uint32_t *B, int32_t gamma, const uint32_t *C, uint32_t *out);
+/* Half adder from one blind rotation (kind HA): out_and = KS(S0),
+ * out_xor = KS(sigma (S1 - S0) + (0, -sigma/8)), S0 / S1 the extractions at index
+ * 0 / N/2 of BR((0,c0) + alpha*A + beta*B) (c0 = -1/8: the AND of the literals). */
+void or_half_adder(const or_ctx *c, uint32_t c0, int32_t alpha, const uint32_t *A, int32_t beta,
+                   const uint32_t *B, int32_t sigma, uint32_t *out_and, uint32_t *out_xor);
 /* Native CGGI MUX: S ? A : B = KS((0,1/8) + BS((0,-1/8)+S+A) + BS((0,-1/8)-S+B)). */
 void or_mux(const or_ctx *c, const uint32_t *S, const uint32_t *A, const uint32_t *B,
             uint32_t *out);
@@ -112,7 +117,8 @@ void or_mux(const or_ctx *c, const uint32_t *S, const uint32_t *A, const uint32_
 typedef struct or_gate_rec {
     uint32_t dst, src_a, src_b, src_c;
     uint32_t c0;
-    int8_t alpha, beta, kind, gamma;  /* kind 0 LIN2, 1 MUX, 2 LIN3 (gamma * src_c) */
+    int8_t alpha, beta, kind, gamma;  /* kind 0 LIN2, 1 MUX, 2 LIN3 (gamma * src_c),
+                                         3 HA (dst = AND, src_c = XOR, gamma = XOR orientation) */
 } or_gate_rec;
 int or_run_gates(const or_ctx *c, const or_gate_rec *gates, size_t n, uint32_t *pool,
                  size_t pool_stride, int threads);

@@ -23,6 +23,7 @@ HB_ENOMEM = -3
 GATE_LIN2 = 0
 GATE_MUX = 1
 GATE_LIN3 = 2
+GATE_HA = 3
 
 # Every symbol the header declares (tests check the library exports them all).
 EXPORTED = (

@@ -39,7 +39,7 @@ import weakref
 import numpy as np
 
 from . import gate_api as api
-from ._native import GATE_DTYPE, GATE_LIN2, GATE_LIN3, GATE_MUX, dag_module
+from ._native import GATE_DTYPE, GATE_HA, GATE_LIN2, GATE_LIN3, GATE_MUX, dag_module
 from .gate_api import AND, MUX, OR, XNOR, XOR, CipherBit, ContextMismatchError, GateBackend, GateStats, ScopeError
 from .tfhe import EIGHTH, MASK32, Engine, KeySet
 
@@ -167,6 +167,10 @@ class TfheContext(GateBackend):
     keys:     an explicit `KeySet` (overrides ``seed``)
     stream_at: pending gates that start a background flush while the DAG is
               still being built (0 disables; flush points are unchanged)
+    fuse_half_adders: an XOR and an AND/OR of the same two nodes in one flush
+              run as one HA record: one blind rotation extracted twice (the
+              AND at index 0, the XOR from the difference of the index-N/2 and
+              index-0 extractions), two key switches.
     stream_min_width: bootstraps a level needs in a background flush; narrower
               levels (and the gates that depend on them) stay pending and
               merge with later gates of the same level (the final flush runs
@@ -177,7 +181,7 @@ class TfheContext(GateBackend):
     _CHUNK = 4096  # logical slots reserved at a time
 
     def __init__(self, seed=0, device=0, lanes=1, enc_seed=None, keys=None, enc_stream=None, stream_at=16384,
-                 stream_min_width=592):
+                 stream_min_width=592, fuse_half_adders=True):
         if lanes < 1:
             raise ValueError("lanes must be >= 1")
         self.global_stats = GateStats(label="global")
@@ -205,6 +209,7 @@ class TfheContext(GateBackend):
         self._finalizer = None
         self.stream_at = int(stream_at)  # pending gates that start a background flush (0: off)
         self.stream_min_width = int(stream_min_width)
+        self.fuse_half_adders = bool(fuse_half_adders)
         # gates between two streaming checks (a countdown instead of a native call per gate)
         self._tick_every = max(1, min(256, self.stream_at // 8))
         self._tick = self._tick_every
@@ -516,6 +521,10 @@ class TfheContext(GateBackend):
         recs["alpha"] = np.where(is_and | is_maj, sa, np.where(is_xor, 2, np.where(is_x3, -2, sb)))
         recs["beta"] = np.where(is_and | is_maj, sb, np.where(is_xor, 2, np.where(is_x3, -2, sc)))
         recs["gamma"] = np.where(is_maj, sc, np.where(is_x3, -2, 0))
+        if self.fuse_half_adders:
+            keep = self._fuse_half_adders(recs, is_and, is_xor, a >> 1, b >> 1)
+            if keep is not None:
+                recs, lvl = recs[keep], lvl[keep]
         order = np.argsort(lvl, kind="stable")
         lvl_sorted = lvl[order]
         bounds = np.flatnonzero(np.diff(lvl_sorted)) + 1
@@ -523,6 +532,32 @@ class TfheContext(GateBackend):
         for chunk in np.split(order, bounds):
             out.append((int(lvl[chunk[0]]), recs[chunk]))
         return out
+
+    @staticmethod
+    def _fuse_half_adders(recs, is_and, is_xor, na, nb):
+        """Pair every XOR node with an AND node (AND/OR of literals) on the same
+        two operand nodes, rewrite the AND record into an HA record
+        whose second output (src_c) is the XOR node's slot, and return the mask
+        of records to keep (None: no pair).  XOR(la, lb) = XOR(a, b) xor
+        [alpha < 0] xor [beta < 0], so gamma = alpha * beta makes the second
+        output the XOR node's own value."""
+        ia, ix = np.flatnonzero(is_and), np.flatnonzero(is_xor)
+        if ia.size == 0 or ix.size == 0:
+            return None
+        # both nodes of a pair have level 1 + max(operand levels): the operand pair is the key
+        lo, hi = np.minimum(na, nb).astype(np.int64), np.maximum(na, nb).astype(np.int64)
+        key = lo * (int(hi.max()) + 1) + hi
+        ka, first = np.unique(key[ia], return_index=True)  # one AND per operand pair
+        _, pos_x, pos_a = np.intersect1d(key[ix], ka, assume_unique=False, return_indices=True)
+        if pos_x.size == 0:
+            return None
+        xi, ai = ix[pos_x], ia[first[pos_a]]
+        recs["kind"][ai] = GATE_HA
+        recs["src_c"][ai] = recs["dst"][xi]
+        recs["gamma"][ai] = recs["alpha"][ai] * recs["beta"][ai]
+        keep = np.ones(recs.size, dtype=bool)
+        keep[xi] = False
+        return keep
 
     def flush(self):
         """Execute every pending gate on the device (level by level)."""
@@ -572,8 +607,10 @@ class TfheContext(GateBackend):
         self._history.extend(batches)
         self._dag.mark_done(pending)  # results are read only after _join_bg
         n_mux = sum(int(np.count_nonzero(r["kind"] == GATE_MUX)) for _, r in batches)
+        n_ha = sum(int(np.count_nonzero(r["kind"] == GATE_HA)) for _, r in batches)
         self.exec_stats["gates"] += int(pending.size) * self.lanes
-        self.exec_stats["bootstraps"] += (int(pending.size) + n_mux) * self.lanes
+        self.exec_stats["bootstraps"] += (int(pending.size) + n_mux - n_ha) * self.lanes
+        self.exec_stats["half_adders"] = self.exec_stats.get("half_adders", 0) + n_ha * self.lanes
         self.exec_stats["levels"] += len(batches)
         self.exec_stats["flushes"] += 1
         if wait:

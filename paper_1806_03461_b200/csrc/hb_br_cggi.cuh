@@ -104,6 +104,23 @@ __device__ __forceinline__ void sample_extract(const uint32_t *accA, const uint3
     }
 }
 
+// HA records (hb_gate kind HA): a second extraction of the same accumulator at
+// index N/2 (a'_i = A_{N/2-i} for i <= N/2, -A_{3N/2-i} above; b' = B_{N/2}) into
+// big row x2 of the item (oracle/tfhe_oracle.c sample_extract_at).
+__device__ __forceinline__ uint32_t *x2_row(const BrArgs &args, uint32_t e) {
+    const uint32_t x2 = args.items[e / args.lanes].x2;
+    return x2 == kNoItem ? nullptr : args.big + ((size_t)x2 * args.lanes + e % args.lanes) * kBigStride;
+}
+__device__ __forceinline__ void sample_extract_half(const uint32_t *accA, const uint32_t *accB, uint32_t *out,
+                                                    int tid, int nthreads) {
+    for (int c = tid; c <= kN; c += nthreads) {
+        uint32_t v;
+        if (c < kN) v = c <= kNH ? accA[kNH - c] : 0u - accA[kN + kNH - c];
+        else v = accB[kNH];
+        out[c] = v;
+    }
+}
+
 constexpr int kStages = 3;  // BK rows in the shared-memory ring
 #ifndef HB_PAIR_UNROLL
 #define HB_PAIR_UNROLL 3  // fully unrolled pair loop: rows (q, p) become compile-time
@@ -319,6 +336,7 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
     }
     // K3: sample extract at index 0
     sample_extract(accA, accB, args.big + (size_t)e * kBigStride, t, 64);
+    if (uint32_t *o2 = x2_row(args, e)) sample_extract_half(accA, accB, o2, t, 64);
 }
 
 // ---------------------------------------------------------------------------
@@ -455,4 +473,5 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_lat(const BrArgs args) 
         for (int c = threadIdx.x; c < 2 * kN; c += 192) dst[c] = (c < kN) ? accA[c] : accB[c - kN];
     }
     sample_extract(accA, accB, args.big + (size_t)e * kBigStride, threadIdx.x, 192);
+    if (uint32_t *o2 = x2_row(args, e)) sample_extract_half(accA, accB, o2, threadIdx.x, 192);
 }

@@ -346,6 +346,19 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
                 }
                 out[kNH - j] = 0u - v[8 + m];  // coefficient j + 512
             }
+            if (uint32_t *o2 = x2_row(args, e)) {  // HA: extraction at index N/2
+#pragma unroll
+                for (int m = 0; m < 8; m++) {
+                    const int j = t + 64 * m;  // A_j -> a'_{512-j}; A_{j+512} -> a'_{1024-j} (j > 0), -sign
+                    o2[kNH - j] = v[m];
+                    if (j > 0) {
+                        o2[kN - j] = 0u - v[8 + m];
+                    } else {
+                        o2[0] = v[8];     // a'_0 = A_512
+                        o2[kN] = v[24];   // b' = B_512
+                    }
+                }
+            }
         }
         tmem_fence_before();
         __syncthreads();
@@ -360,6 +373,7 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
         for (int c = t; c < 2 * kN; c += 64) dst[c] = (c < kN) ? accA[c] : accB[c - kN];
     }
     sample_extract(accA, accB, args.big + (size_t)e * kBigStride, t, 64);
+    if (uint32_t *o2 = x2_row(args, e)) sample_extract_half(accA, accB, o2, t, 64);
 }
 
 // ---------------------------------------------------------------------------
@@ -538,6 +552,7 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_u2_lat(const BrArgs arg
         for (int c = threadIdx.x; c < 2 * kN; c += 192) dst[c] = (c < kN) ? accA[c] : accB[c - kN];
     }
     sample_extract(accA, accB, args.big + (size_t)e * kBigStride, threadIdx.x, 192);
+    if (uint32_t *o2 = x2_row(args, e)) sample_extract_half(accA, accB, o2, threadIdx.x, 192);
 }
 
 // ---------------------------------------------------------------------------
@@ -752,9 +767,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) k_blind_rota
         for (int c = threadIdx.x; c < kN; c += 192) dst[c] = sm.acc[c];
     }
     uint32_t *out = args.big + (size_t)e * kBigStride;
+    uint32_t *out2 = x2_row(args, e);  // HA: second extraction at index N/2
     if (q == 0) {
         for (int c = threadIdx.x; c < kN; c += 192) out[c] = c == 0 ? sm.acc[0] : 0u - sm.acc[kN - c];
+        if (out2)
+            for (int c = threadIdx.x; c < kN; c += 192) out2[c] = c <= kNH ? sm.acc[kNH - c] : 0u - sm.acc[kN + kNH - c];
     } else if (threadIdx.x == 0) {
         out[kN] = sm.acc[0];
+        if (out2) out2[kN] = sm.acc[kNH];
     }
 }

@@ -93,6 +93,7 @@ struct hb_engine {
     uint64_t flush_gen = 1;
     cudaEvent_t ev[4]{};
     cudaEvent_t ev_stage = nullptr;  // item copies out of h_stage done
+    cudaEvent_t ev_grow = nullptr;   // pool growth fences between the engine and copy streams
     uint64_t n_br = 0, n_ks = 0, n_launch = 0;
     int num_sms = 148;
     size_t max_work = kMaxWorkPerLaunch;  // HEBNN_B200_MAX_WORK overrides (tests)
@@ -102,21 +103,21 @@ struct hb_engine {
 
 namespace {
 
+// Grow a device scratch buffer used only by work on stream `st`: stream-ordered
+// allocation and free (the old buffer is released after the queued kernels that
+// use it), so a level wider than any before does not stall the host.
 int ensure_dev(void **ptr, size_t *cap, size_t need, size_t elem, bool preserve, cudaStream_t st) {
     if (need <= *cap) return HB_OK;
     size_t ncap = std::max(need, *cap + *cap / 2);
     void *np = nullptr;
-    cudaError_t err = cudaMalloc(&np, ncap * elem);
+    cudaError_t err = cudaMallocAsync(&np, ncap * elem, st);
     if (err != cudaSuccess) {
-        set_error(std::string("cudaMalloc(") + std::to_string(ncap * elem) + " B): " + cudaGetErrorString(err));
+        set_error(std::string("cudaMallocAsync(") + std::to_string(ncap * elem) + " B): " + cudaGetErrorString(err));
         return HB_ENOMEM;
     }
     if (*ptr) {
-        if (preserve && *cap) {
-            HB_CUDA_TRY(cudaMemcpyAsync(np, *ptr, *cap * elem, cudaMemcpyDeviceToDevice, st));
-            HB_CUDA_TRY(cudaStreamSynchronize(st));
-        }
-        cudaFree(*ptr);
+        if (preserve && *cap) HB_CUDA_TRY(cudaMemcpyAsync(np, *ptr, *cap * elem, cudaMemcpyDeviceToDevice, st));
+        HB_CUDA_TRY(cudaFreeAsync(*ptr, st));
     }
     *ptr = np;
     *cap = ncap;
@@ -127,7 +128,7 @@ int ensure_host_stage(hb_engine *e, size_t bytes) {
     if (bytes <= e->h_stage_cap) return HB_OK;
     HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
     if (e->h_stage) cudaFreeHost(e->h_stage);
-    size_t ncap = std::max(bytes, e->h_stage_cap * 2);
+    size_t ncap = std::max({bytes, e->h_stage_cap * 2, (size_t)32 << 20});  // >= 32 MiB: rare regrowth
     HB_CUDA_TRY(cudaHostAlloc(&e->h_stage, ncap, cudaHostAllocDefault));
     e->h_stage_cap = ncap;
     return HB_OK;
@@ -303,8 +304,15 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
     e->p = *p;
     e->pool_stride = (uint32_t)((p->n + 1 + 3) & ~3);
     HB_CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    {  // stream-ordered scratch / pool growth: keep freed blocks in the pool instead of unmapping them
+        cudaMemPool_t mp;
+        HB_CUDA_TRY(cudaDeviceGetDefaultMemPool(&mp, device));
+        uint64_t keep = UINT64_MAX;
+        HB_CUDA_TRY(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     for (auto &ev : e->ev) HB_CUDA_TRY(cudaEventCreate(&ev));
     HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_stage, cudaEventDisableTiming));
+    HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_grow, cudaEventDisableTiming));
     HB_CUDA_TRY(cudaStreamCreateWithFlags(&e->h2d_stream, cudaStreamNonBlocking));
     HB_CUDA_TRY(cudaStreamCreateWithFlags(&e->d2h_stream, cudaStreamNonBlocking));
     HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_upload, cudaEventDisableTiming));
@@ -428,6 +436,7 @@ int hb_engine_destroy(hb_engine *e) {
     for (auto &ev : e->ev)
         if (ev) cudaEventDestroy(ev);
     if (e->ev_stage) cudaEventDestroy(e->ev_stage);
+    if (e->ev_grow) cudaEventDestroy(e->ev_grow);
     for (cudaStream_t st : {e->h2d_stream, e->d2h_stream})
         if (st) {
             cudaStreamSynchronize(st);
@@ -440,13 +449,37 @@ int hb_engine_destroy(hb_engine *e) {
     return HB_OK;
 }
 
+// Pool growth is stream-ordered (cudaMallocAsync / copy / cudaFreeAsync on the
+// engine stream, fenced against both copy streams), so growing the pool while
+// levels are queued never blocks the host: the gate DAG keeps being built while
+// a background flush runs.
 int hb_pool_reserve(hb_engine *e, size_t slots) {
     if (!e) return HB_EINVAL;
+    if (slots <= e->pool_cap) return HB_OK;
     HB_CUDA_TRY(cudaSetDevice(e->device));
-    size_t cap_words = e->pool_cap * e->pool_stride;
-    int rc = ensure_dev((void **)&e->d_pool, &cap_words, slots * e->pool_stride, sizeof(uint32_t), true, e->stream);
-    if (rc) return rc;
-    e->pool_cap = cap_words / e->pool_stride;
+    const size_t ncap = std::max(slots, e->pool_cap + e->pool_cap / 2);
+    uint32_t *np = nullptr;
+    cudaError_t err = cudaMallocAsync((void **)&np, ncap * e->pool_stride * sizeof(uint32_t), e->stream);
+    if (err != cudaSuccess) {
+        set_error(std::string("cudaMallocAsync(pool, ") + std::to_string(ncap * e->pool_stride * 4) +
+                  " B): " + cudaGetErrorString(err));
+        return HB_ENOMEM;
+    }
+    if (e->d_pool) {
+        // copies already queued on the copy streams read / write the old buffer: order them first
+        for (cudaStream_t st : {e->h2d_stream, e->d2h_stream}) {
+            HB_CUDA_TRY(cudaEventRecord(e->ev_grow, st));
+            HB_CUDA_TRY(cudaStreamWaitEvent(e->stream, e->ev_grow, 0));
+        }
+        HB_CUDA_TRY(cudaMemcpyAsync(np, e->d_pool, e->pool_cap * e->pool_stride * sizeof(uint32_t),
+                                    cudaMemcpyDeviceToDevice, e->stream));
+        HB_CUDA_TRY(cudaFreeAsync(e->d_pool, e->stream));
+        // later copies on the copy streams address the new buffer after its contents arrived
+        HB_CUDA_TRY(cudaEventRecord(e->ev_grow, e->stream));
+        for (cudaStream_t st : {e->h2d_stream, e->d2h_stream}) HB_CUDA_TRY(cudaStreamWaitEvent(st, e->ev_grow, 0));
+    }
+    e->d_pool = np;
+    e->pool_cap = ncap;
     return HB_OK;
 }
 
@@ -575,13 +608,18 @@ int hb_run_gates(hb_engine *e, const hb_gate *gates, size_t n, uint32_t lanes) {
 
 static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_t lanes) {
     // expand records into blind-rotation and key-switch work items
-    size_t nbr = 0;
+    size_t nbr = 0, nha = 0;
     for (size_t i = 0; i < n; i++) {
         const hb_gate &g = gates[i];
-        if (g.kind != HB_GATE_LIN2 && g.kind != HB_GATE_MUX && g.kind != HB_GATE_LIN3) {
+        if (g.kind != HB_GATE_LIN2 && g.kind != HB_GATE_MUX && g.kind != HB_GATE_LIN3 && g.kind != HB_GATE_HA) {
             set_error("hb_run_gates: unknown gate kind " + std::to_string((int)g.kind));
             return HB_EINVAL;
         }
+        if (g.kind == HB_GATE_HA && ((g.gamma != 1 && g.gamma != -1) || g.dst == g.src_c)) {
+            set_error("hb_run_gates: HA record needs gamma = +-1 and dst != src_c");
+            return HB_EINVAL;
+        }
+        nha += g.kind == HB_GATE_HA;
         const size_t top = (size_t)std::max(std::max(g.dst, g.src_a), std::max(g.src_b, g.src_c)) + 1;
         if (top * lanes > e->pool_cap) {
             set_error("hb_run_gates: slot beyond pool capacity");
@@ -589,7 +627,9 @@ static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_
         }
         nbr += (g.kind == HB_GATE_MUX) ? 2 : 1;
     }
-    const size_t br_bytes = nbr * sizeof(BrItem), ks_bytes = n * sizeof(KsItem);
+    // big-LWE rows: one per blind rotation, then one per HA second extraction
+    const size_t nks = n + nha, nbig = nbr + nha;
+    const size_t br_bytes = nbr * sizeof(BrItem), ks_bytes = nks * sizeof(KsItem);
     int rc = ensure_host_stage(e, br_bytes + ks_bytes);
     if (rc) return rc;
     // the pinned stage fed the previous level's item copies; wait for those copies only,
@@ -597,28 +637,38 @@ static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_
     HB_CUDA_TRY(cudaEventSynchronize(e->ev_stage));
     BrItem *hbr = reinterpret_cast<BrItem *>(e->h_stage);
     KsItem *hks = reinterpret_cast<KsItem *>(reinterpret_cast<char *>(e->h_stage) + br_bytes);
-    size_t b = 0;
+    size_t b = 0, h = 0;
     const uint32_t eighth = 1u << 29;
     for (size_t i = 0; i < n; i++) {
         const hb_gate &g = gates[i];
         if (g.kind == HB_GATE_LIN2) {
-            hbr[b] = BrItem{g.src_a, g.src_b, g.src_a, g.c0, pack_coef(g.alpha, g.beta)};
+            hbr[b] = BrItem{g.src_a, g.src_b, g.src_a, g.c0, pack_coef(g.alpha, g.beta), kNoItem};
             hks[i] = KsItem{g.dst, (uint32_t)b, 0xFFFFFFFFu, 0u};
             b += 1;
+        } else if (g.kind == HB_GATE_HA) {
+            // one blind rotation, extractions S0 (row b) and S1 (row nbr + h); AND = KS(S0),
+            // XOR = KS(gamma (S1 - S0) + (0, -gamma/8)) (oracle/tfhe_oracle.c or_half_adder)
+            const uint32_t s0 = (uint32_t)b, s1 = (uint32_t)(nbr + h);
+            hbr[b] = BrItem{g.src_a, g.src_b, g.src_a, g.c0, pack_coef(g.alpha, g.beta), s1};
+            hks[i] = KsItem{g.dst, s0, 0xFFFFFFFFu, 0u};
+            hks[n + h] = g.gamma > 0 ? KsItem{g.src_c, s1, s0 | kKsSub, 0u - eighth}
+                                     : KsItem{g.src_c, s0, s1 | kKsSub, eighth};
+            b += 1;
+            h += 1;
         } else if (g.kind == HB_GATE_LIN3) {
-            hbr[b] = BrItem{g.src_a, g.src_b, g.src_c, g.c0, pack_coef(g.alpha, g.beta, g.gamma)};
+            hbr[b] = BrItem{g.src_a, g.src_b, g.src_c, g.c0, pack_coef(g.alpha, g.beta, g.gamma), kNoItem};
             hks[i] = KsItem{g.dst, (uint32_t)b, 0xFFFFFFFFu, 0u};
             b += 1;
         } else {
-            hbr[b] = BrItem{g.src_a, g.src_b, g.src_a, 0u - eighth, pack_coef(1, g.alpha)};
-            hbr[b + 1] = BrItem{g.src_a, g.src_c, g.src_a, 0u - eighth, pack_coef(-1, g.beta)};
+            hbr[b] = BrItem{g.src_a, g.src_b, g.src_a, 0u - eighth, pack_coef(1, g.alpha), kNoItem};
+            hbr[b + 1] = BrItem{g.src_a, g.src_c, g.src_a, 0u - eighth, pack_coef(-1, g.beta), kNoItem};
             hks[i] = KsItem{g.dst, (uint32_t)b, (uint32_t)(b + 1), eighth};
             b += 2;
         }
     }
     if ((rc = ensure_dev((void **)&e->d_br, &e->br_cap, nbr, sizeof(BrItem), false, e->stream))) return rc;
-    if ((rc = ensure_dev((void **)&e->d_ks, &e->ks_cap, n, sizeof(KsItem), false, e->stream))) return rc;
-    if ((rc = ensure_dev((void **)&e->d_big, &e->big_cap, nbr * lanes * kBigStride, sizeof(uint32_t), false,
+    if ((rc = ensure_dev((void **)&e->d_ks, &e->ks_cap, nks, sizeof(KsItem), false, e->stream))) return rc;
+    if ((rc = ensure_dev((void **)&e->d_big, &e->big_cap, nbig * lanes * kBigStride, sizeof(uint32_t), false,
                          e->stream)))
         return rc;
     HB_CUDA_TRY(cudaMemcpyAsync(e->d_br, hbr, br_bytes, cudaMemcpyHostToDevice, e->stream));
@@ -641,7 +691,7 @@ static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_
     k.big = e->d_big;
     k.items = e->d_ks;
     k.lanes = lanes;
-    k.n_work = (uint32_t)(n * lanes);
+    k.n_work = (uint32_t)(nks * lanes);
     k.ksk = e->d_ksk;
     k.pool = e->d_pool;
     k.pool_stride = e->pool_stride;
@@ -649,7 +699,7 @@ static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_
     if ((rc = launch_ks(e, k))) return rc;
     HB_CUDA_TRY(cudaEventRecord(e->ev[2], e->stream));
     e->n_br += nbr * lanes;
-    e->n_ks += n * lanes;
+    e->n_ks += nks * lanes;
     return HB_OK;
 }
 
@@ -757,7 +807,7 @@ int hb_debug_bootstrap_wo_ks(hb_engine *e, const uint32_t *lin, size_t count, ui
     if ((rc = ensure_dev((void **)&e->d_big, &e->big_cap, count * kBigStride, sizeof(uint32_t), false, e->stream)))
         return rc;
     std::vector<BrItem> items(count);
-    for (size_t i = 0; i < count; i++) items[i] = BrItem{(uint32_t)i, (uint32_t)i, (uint32_t)i, 0u, pack_coef(1, 0)};
+    for (size_t i = 0; i < count; i++) items[i] = BrItem{(uint32_t)i, (uint32_t)i, (uint32_t)i, 0u, pack_coef(1, 0), kNoItem};
     HB_CUDA_TRY(cudaMemcpyAsync(e->d_tmp, lin, count * words * 4, cudaMemcpyHostToDevice, e->stream));
     HB_CUDA_TRY(cudaMemcpyAsync(e->d_br, items.data(), count * sizeof(BrItem), cudaMemcpyHostToDevice, e->stream));
     HB_CUDA_TRY(cudaMemsetAsync(e->d_margin, 0, sizeof(unsigned long long), e->stream));

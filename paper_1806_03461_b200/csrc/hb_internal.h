@@ -29,11 +29,14 @@ int bk_unroll(const hb_params *p);          // 1 or 2 (0 reads as 1)
 size_t bk_tgsw_count(const hb_params *p);   // TGSW samples in the bootstrapping key
 
 // Bootstrapped-gate work items produced from hb_gate records.
+constexpr uint32_t kNoItem = 0xFFFFFFFFu;
+constexpr uint32_t kKsSub = 0x80000000u;  // KsItem::i1 flag: subtract big[i1] instead of adding it
 struct BrItem {      // lin = (0, c0) + alpha * pool[src_a] + beta * pool[src_b] + gamma * pool[src_c]
     uint32_t src_a, src_b, src_c, c0;
     int32_t coef;    // alpha in bits 0..7, beta in bits 8..15, gamma in bits 16..23 (signed bytes)
+    uint32_t x2;     // kNoItem, or the big-LWE row (item units) of a second extraction at index N/2 (HA)
 };
-struct KsItem {      // pool[dst] = KS(big[i0] (+ big[i1]) + (0, cadd))
+struct KsItem {      // pool[dst] = KS(big[i0] (+/- big[i1 & ~kKsSub]) + (0, cadd)); i1 = kNoItem: big[i0] only
     uint32_t dst, i0, i1, cadd;
 };
 

@@ -11,6 +11,7 @@
 // HB_KS_PAIR = 1 (default): digits are consumed in pairs.  The device table
 // holds, per coefficient i, digit pair p and output column c, the 16 sums
 //   T[chunk][i][p][c][d] = KS[i][2p][d >> 2] + KS[i][2p+1][d & 3]  (mod 2^32)
+// The input is big[i0] (+ or - big[i1], KsItem flag kKsSub) formed on the fly.
 // (64 B: 16 consecutive banks), so one digit pair costs one conflict-free
 // LDS.32 per column (lanes with equal d broadcast, different d hit different
 // banks): 8 wavefronts per warp per digit PAIR, half of the one-digit layout,
@@ -64,7 +65,8 @@ __global__ void __launch_bounds__(kKsThreads) k_keyswitch(const KsArgs args) {
     const KsItem it = args.items[ee / lanes];
     const uint32_t lane_id = ee % lanes;
     const uint32_t *b0 = args.big + ((size_t)it.i0 * lanes + lane_id) * kBigStride;
-    const uint32_t *b1 = it.i1 != 0xFFFFFFFFu ? args.big + ((size_t)it.i1 * lanes + lane_id) * kBigStride : nullptr;
+    const bool has1 = it.i1 != kNoItem, sub = has1 && (it.i1 & kKsSub);
+    const uint32_t *b1 = has1 ? args.big + ((size_t)(it.i1 & ~kKsSub) * lanes + lane_id) * kBigStride : nullptr;
     const int chunk = blockIdx.y;
     // blockIdx.z splits the coefficient range (narrow levels: more CTAs, shorter streams)
     const int kBlocks = (kN / kKsIBlock) / gridDim.z;
@@ -97,7 +99,8 @@ __global__ void __launch_bounds__(kKsThreads) k_keyswitch(const KsArgs args) {
     for (int q = 0; q < kW4; q++) {
         w[q] = __ldg(wsrc0 + q);
         if (b1) {
-            const uint4 x = __ldg(wsrc1 + q);
+            uint4 x = __ldg(wsrc1 + q);
+            if (sub) x = make_uint4(0u - x.x, 0u - x.y, 0u - x.z, 0u - x.w);
             w[q] = make_uint4(w[q].x + x.x, w[q].y + x.y, w[q].z + x.z, w[q].w + x.w);
         }
     }
@@ -123,7 +126,8 @@ __global__ void __launch_bounds__(kKsThreads) k_keyswitch(const KsArgs args) {
             for (int q = 0; q < kW4; q++) {
                 w[q] = __ldg(wsrc0 + kW4 * (blk + 1) + q);
                 if (b1) {
-                    const uint4 x = __ldg(wsrc1 + kW4 * (blk + 1) + q);
+                    uint4 x = __ldg(wsrc1 + kW4 * (blk + 1) + q);
+                    if (sub) x = make_uint4(0u - x.x, 0u - x.y, 0u - x.z, 0u - x.w);
                     w[q] = make_uint4(w[q].x + x.x, w[q].y + x.y, w[q].z + x.z, w[q].w + x.w);
                 }
             }
@@ -172,7 +176,7 @@ __global__ void __launch_bounds__(kKsThreads) k_keyswitch(const KsArgs args) {
     uint32_t bval = 0;
     if (c0 + kKsCols > args.n) {
         bval = b0[kN];
-        if (b1) bval += b1[kN] + it.cadd;
+        if (b1) bval += (sub ? 0u - b1[kN] : b1[kN]) + it.cadd;
     }
     uint32_t *dst = args.pool + ((size_t)it.dst * lanes + lane_id) * args.pool_stride;
 #pragma unroll
@@ -195,7 +199,10 @@ __global__ void __launch_bounds__(kKskStride) k_keyswitch_reduce(const KsArgs ar
     uint32_t bval = 0;
     if (col == args.n) {
         bval = args.big[((size_t)it.i0 * lanes + lane_id) * kBigStride + kN];
-        if (it.i1 != 0xFFFFFFFFu) bval += args.big[((size_t)it.i1 * lanes + lane_id) * kBigStride + kN] + it.cadd;
+        if (it.i1 != kNoItem) {
+            const uint32_t v1 = args.big[((size_t)(it.i1 & ~kKsSub) * lanes + lane_id) * kBigStride + kN];
+            bval += ((it.i1 & kKsSub) ? 0u - v1 : v1) + it.cadd;
+        }
     }
     args.pool[((size_t)it.dst * lanes + lane_id) * args.pool_stride + col] = bval - sum;
 }

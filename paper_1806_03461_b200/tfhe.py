@@ -194,8 +194,10 @@ class Engine:
         gates = np.ascontiguousarray(gates, dtype=GATE_DTYPE)
         check(lib().hb_run_gates(self._e, gates.ctypes.data_as(ctypes.c_void_p), gates.shape[0], int(lanes)))
 
-    @_locked
     def sync(self):
+        """Wait for the engine's streams.  Not under the engine lock: hb_sync only
+        synchronises streams, so a background flush waiting here does not block
+        other threads' calls (pool growth, uploads, the next level)."""
         check(lib().hb_sync(self._e))
 
     @_locked

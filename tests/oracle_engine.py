@@ -45,7 +45,7 @@ class OracleEngine:
             for f in ("dst", "src_a", "src_b", "src_c"):
                 out[f] = out[f] * lanes + lane
             recs = out
-        self.bootstraps += int(recs.size + np.count_nonzero(recs["kind"] == 1))
+        self.bootstraps += int(recs.size + np.count_nonzero(recs["kind"] == 1) - np.count_nonzero(recs["kind"] == 3))
         self.ctx.run_gates(recs, self.pool, threads=self.threads)
 
     def sync(self):

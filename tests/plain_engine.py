@@ -11,7 +11,7 @@ product package.
 
 import numpy as np
 
-from paper_1806_03461_b200._native import GATE_LIN3, GATE_MUX
+from paper_1806_03461_b200._native import GATE_HA, GATE_LIN3, GATE_MUX
 
 EIGHTH = 1 << 29
 
@@ -47,7 +47,16 @@ class PlainEngine:
         for r in recs:
             A = self.pool[r["src_a"] * lanes + lane]
             B = self.pool[r["src_b"] * lanes + lane]
-            if r["kind"] == GATE_MUX:
+            if r["kind"] == GATE_HA:
+                # one rotation of psi = c0 + alpha A + beta B: S0 = sign(psi), S1 = +1/8 iff
+                # psi in [-1/4, 1/4); AND = S0, XOR = gamma (S1 - S0) - gamma/8 (hb_gate HA)
+                psi = (int(r["c0"]) + int(r["alpha"]) * A + int(r["beta"]) * B) & 0xFFFFFFFF
+                s0 = _sign_to_phase(psi)
+                s1 = _sign_to_phase((psi + (1 << 30)) & 0xFFFFFFFF)
+                g = int(r["gamma"])
+                self.pool[r["src_c"] * lanes + lane] = _sign_to_phase((g * (s1 - s0) - g * EIGHTH) & 0xFFFFFFFF)
+                out = s0
+            elif r["kind"] == GATE_MUX:
                 C = self.pool[r["src_c"] * lanes + lane]
                 u1 = _sign_to_phase((-EIGHTH + A + int(r["alpha"]) * B) & 0xFFFFFFFF)
                 u2 = _sign_to_phase((-EIGHTH - A + int(r["beta"]) * C) & 0xFFFFFFFF)

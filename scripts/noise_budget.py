@@ -49,3 +49,14 @@ if __name__ == "__main__":
             p = math.erfc(z / math.sqrt(2))
             print(f"  {name:28s} sigma = 2^{math.log2(math.sqrt(var)):.2f}  margin {margin}  z = {z:.1f}  "
                   f"P(fail) ~ 2^{math.log2(p) if p > 0 else float('-inf'):.0f}")
+        # inputs produced by a plain gate (1 blind rotation + KS) or by a MUX / the XOR
+        # output of a fused half adder (2 blind-rotation noise terms + 1 KS), into every
+        # consumer: 2-input (|coef| 1 or 2) and 3-input (majority |coef| 1, XOR3 |coef| 2)
+        var_two = 2 * var_br + var_ks
+        for src, v_in in (("gate outputs", var_out), ("MUX / HA-XOR outputs", var_two)):
+            for name, terms, coef2, margin in (("AND/OR", 2, 1, 1 / 8), ("XOR", 2, 4, 1 / 4),
+                                               ("MAJ", 3, 1, 1 / 8), ("XOR3", 3, 4, 1 / 4)):
+                var = terms * coef2 * v_in + var_ms
+                z = margin / math.sqrt(var)
+                p = math.erfc(z / math.sqrt(2))
+                print(f"  {name:6s} of {terms} {src:22s} z = {z:5.1f}  P(fail) ~ 2^{math.log2(p) if p > 0 else float('-inf'):.0f}")

@@ -304,10 +304,10 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
     e->p = *p;
     e->pool_stride = (uint32_t)((p->n + 1 + 3) & ~3);
     HB_CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
-    {  // stream-ordered scratch / pool growth: keep freed blocks in the pool instead of unmapping them
+    if (const char *k = std::getenv("HEBNN_B200_POOL_KEEP_MB")) {  // experiment: mempool release threshold
         cudaMemPool_t mp;
         HB_CUDA_TRY(cudaDeviceGetDefaultMemPool(&mp, device));
-        uint64_t keep = UINT64_MAX;
+        uint64_t keep = std::strtoull(k, nullptr, 10) << 20;
         HB_CUDA_TRY(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep));
     }
     for (auto &ev : e->ev) HB_CUDA_TRY(cudaEventCreate(&ev));

@@ -1,5 +1,5 @@
 """Soak test: many random mixed gate records (LIN2 with random gate constants
-and signs, MUX, majority / XOR3) on the GPU vs the oracle's or_run_gates,
+and signs, MUX, majority / XOR3, half adders) on the GPU vs the oracle's or_run_gates,
 several levels deep (each level reads the previous level's outputs).
 Usage: python scripts/soak_parity.py [records_per_level] [levels]"""
 import os
@@ -23,7 +23,7 @@ for unroll in (2, 1):
     eng = tfhe.Engine(keys)
     rng = np.random.default_rng(unroll)
     n_in = 256
-    total = n_in + levels * n
+    total = n_in + levels * 2 * n  # per level: n record outputs + n half-adder XOR outputs
     cts = keys.encrypt(rng.integers(0, 2, n_in).astype(np.uint8), seed=5, stream=9)
     eng.reserve(total)
     eng.upload(0, cts)
@@ -32,12 +32,12 @@ for unroll in (2, 1):
     t_gpu = t_cpu = 0.0
     lo = 0
     for lv in range(levels):
-        base = n_in + lv * n
+        base = n_in + lv * 2 * n
         recs = tfhe.gate_records(n)
         recs["dst"] = base + np.arange(n)
         srcs = rng.integers(lo, base, (n, 3))
         recs["src_a"], recs["src_b"], recs["src_c"] = srcs[:, 0], srcs[:, 1], srcs[:, 2]
-        kind = rng.integers(0, 3, n)
+        kind = rng.integers(0, 4, n)
         recs["kind"] = kind
         for i in range(n):
             if kind[i] == 0:
@@ -45,13 +45,20 @@ for unroll in (2, 1):
                 recs["c0"][i], recs["alpha"][i], recs["beta"][i] = c0, al, be
             elif kind[i] == 1:
                 recs["alpha"][i], recs["beta"][i] = rng.choice((-1, 1)), rng.choice((-1, 1))
-            else:
+            elif kind[i] == 2:
                 coef = (-2, -2, -2) if rng.integers(0, 2) else tuple(int(v) for v in rng.choice((-1, 1), 3))
                 recs["alpha"][i], recs["beta"][i], recs["gamma"][i] = coef
+            else:  # half adder: AND of random literals -> dst, XOR -> base + n + i
+                al, be = rng.choice((-1, 1)), rng.choice((-1, 1))
+                if recs["src_a"][i] == recs["src_b"][i]:
+                    recs["src_b"][i] = lo if recs["src_a"][i] != lo else lo + 1
+                recs["c0"][i] = (-(1 << 29)) & 0xFFFFFFFF
+                recs["alpha"][i], recs["beta"][i], recs["gamma"][i] = al, be, al * be
+                recs["src_c"][i] = base + n + i
         t0 = time.time(); eng.run_gates(recs); eng.sync(); t_gpu += time.time() - t0
         t0 = time.time(); octx.run_gates(recs, pool, threads=os.cpu_count() or 1); t_cpu += time.time() - t0
         lo = base
-    got = eng.download(n_in, levels * n)
+    got = eng.download(n_in, levels * 2 * n)
     same = np.array_equal(got, pool[n_in:])
     print(f"bk_unroll={unroll}: {levels} levels x {n} records, GPU == oracle word for word: {same} "
           f"(GPU {t_gpu:.2f} s, oracle {t_cpu:.1f} s on {os.cpu_count()} threads)", flush=True)

@@ -591,7 +591,11 @@ class TfheContext(GateBackend):
             errors.append(exc)
 
     def _launch(self, wait):
-        self._join_bg()
+        # a background batch is only started when the previous one has finished; a
+        # final (waiting) flush prepares its schedule while that batch still runs
+        # and joins it just before launching (stream order does the rest)
+        if not wait:
+            self._join_bg()
         t0 = time.perf_counter()
         eng = self._ensure_engine()
         if self._inputs:
@@ -602,6 +606,8 @@ class TfheContext(GateBackend):
             pending, deferred = self._select_wide(pending)
             self._dag.requeue(deferred)
         if pending.size == 0:
+            if wait:
+                self._join_bg()
             return
         batches = self._build_schedule(pending)
         self._history.extend(batches)
@@ -614,6 +620,7 @@ class TfheContext(GateBackend):
         self.exec_stats["levels"] += len(batches)
         self.exec_stats["flushes"] += 1
         if wait:
+            self._join_bg()
             errors = []
             self._run_batches(eng, batches, self.lanes, errors)
             if errors:

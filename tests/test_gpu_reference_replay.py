@@ -292,3 +292,22 @@ def test_replay_cached_dag_on_gpu():
         xs2 = [rng.choice((-1, 1)) for _ in range(d)]
         ctx.replay(xb, ctx.keys.encrypt([1 if v == 1 else 0 for v in xs2], seed=50 + trial))
         assert decrypt_output(ctx, outs) == oracle_eval(m, xs2)
+
+
+@pytest.mark.parametrize("config", ["cfg2l", "cfg4"])
+def test_baseline_configs_full_size(config):
+    """BASELINE.json configs at full size (cfg2: the 784->256 layer; cfg4: the
+    80%-sparse 784-256-256-10 BNN, batch 8) through the reference compiler on
+    the default context (streaming flushes, narrow-level deferral, full-adder
+    and half-adder fusion): every output equals oracle_eval, also when the
+    cached DAG is replayed on a second encrypted batch; counted stats are the
+    reference's and fusion executes fewer bootstraps than it counts."""
+    from paper_1806_03461_b200 import workloads
+
+    rep = workloads.run_encrypted(TfheContext, config, seed=0, replays=1)
+    assert rep["matches_oracle_eval"] is True
+    assert rep["replay"]["matches_oracle_eval"] is True
+    model, batch = workloads.build(config, 0)
+    sim = workloads.run_sim_reference(config, seed=0)
+    assert rep["counted_gates_per_input"] == sim["counted_gates_per_input"]
+    assert rep["executed_bootstraps"] < 0.45 * rep["counted_gates"]

@@ -51,6 +51,9 @@ constexpr int kStagesPerPair = 3 * kRows;  // (row pair, component, row) stages 
 #ifndef HB_TRACE
 #define HB_TRACE 0  // per-phase clock64 trace of the cluster latency kernel (printf, one pair)
 #endif
+#ifndef HB_U2_MAC2
+#define HB_U2_MAC2 1  // MAC over both rows of a row pair per bin (fewer live registers; 0: row by row)
+#endif
 #ifndef HB_EXP_NO_BK_LDS
 #define HB_EXP_NO_BK_LDS 0
 #endif
@@ -170,6 +173,10 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
             base[c] = __ldg(&args.PSI[(ex[c] * (4 * t + 1)) & (2 * kN - 1)]);
         }
         double2 f0[8], f1[8];
+#if HB_U2_MAC2
+#pragma unroll
+        for (int m = 0; m < 8; m++) f0[m] = f1[m] = make_double2(0.0, 0.0);
+#endif
 #pragma unroll 1
         for (int rp = 0; rp < kRows / 2; rp++) {
             // producer: refill the ring up to R stages ahead of this row pair
@@ -213,6 +220,44 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
                 }
             }
             nega_fft_fwd_n<2, true>(x, xch, t, sm.tws[t], bar_id);
+#if HB_U2_MAC2
+            // both rows of the row pair per bin: F_c at bins m, m + 4 computed in the
+            // m loop (8 live registers instead of 32), two independent products per
+            // bin, accumulators zeroed at the start of the pair
+            static_assert(!kMidIssue, "MAC2 consumes the row pair's two stages of a component together");
+#pragma unroll
+            for (int c = 0; c < 3; c++, st += 2) {
+                const long long flip = (long long)(ex[c] & 1) << 63;
+                const int s0 = st % R, s1 = (st + 1) % R;
+                mbar_wait(&sm.full[s0], (st / R) & 1);
+                mbar_wait(&sm.full[s1], ((st + 1) / R) & 1);
+                const double2 *b00 = sm.bk[s0], *b01 = sm.bk[s0] + kNH;  // row h = 0: output polys 0 / 1
+                const double2 *b10 = sm.bk[s1], *b11 = sm.bk[s1] + kNH;  // row h = 1
+#pragma unroll
+                for (int m = 0; m < 4; m++) {
+                    const double2 pm = m == 0 ? base[c] : cmul(base[c], c_w8[(ex[c] * m) & 7]);
+                    const double2 Fm[2] = {make_double2(pm.x - 1.0, pm.y),
+                                           make_double2(__longlong_as_double(__double_as_longlong(pm.x) ^ flip) - 1.0,
+                                                        __longlong_as_double(__double_as_longlong(pm.y) ^ flip))};
+#pragma unroll
+                    for (int hi = 0; hi < 2; hi++) {
+                        const int mm = m + 4 * hi;
+                        const int k = t + 64 * mm;
+                        const double2 y0 = cmul(x[0][mm], Fm[hi]), y1 = cmul(x[1][mm], Fm[hi]);
+                        cmac(f0[mm], y0, b00[k]);
+                        cmac(f1[mm], y0, b01[k]);
+                        cmac(f0[mm], y1, b10[k]);
+                        cmac(f1[mm], y1, b11[k]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&sm.empty[s0]);
+                    mbar_arrive(&sm.empty[s1]);
+                }
+                __syncwarp();
+            }
+#else
 #pragma unroll
             for (int c = 0; c < 3; c++) {
                 double2 F[8];  // (X^{e_c} - 1) at this thread's bins (recomputed per row pair: registers)
@@ -271,6 +316,7 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
                     __syncwarp();
                 }
             }
+#endif
         }
         {
             double2 x[2][8];

@@ -20,10 +20,11 @@ def run(eng, batches, lanes, errors):
 B.TfheContext._launch = launch
 B.TfheContext._run_batches = staticmethod(run)
 warm = B.TfheContext(seed=0); warm.decrypt(warm.g_and(warm.encrypt(1), warm.encrypt(1)))
-for rep in range(2):
+CFG = sys.argv[1] if len(sys.argv) > 1 else 'cfg2l'
+for rep in range(int(sys.argv[2]) if len(sys.argv) > 2 else 2):
     log.clear()
-    model, batch = workloads.build('cfg2l', 0)
-    X = workloads.inputs('cfg2l', model, batch, 1)
+    model, batch = workloads.build(CFG, 0)
+    X = workloads.inputs(CFG, model, batch, 1)
     ctx = B.TfheContext(seed=0, lanes=batch)
     T0[0] = time.perf_counter()
     xb = ctx.encrypt_many(X.T)

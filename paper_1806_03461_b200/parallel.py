@@ -120,8 +120,6 @@ class OutPEvaluator:
             if hi > lo:
                 sub = _sub_block_model(block, lo, hi, model.output_mode, is_last)
                 outs, _ = eval_model(ctx, sub, x, self.options)
-            self.stats.append({"block": bi, "units": (lo, hi), "counted_gates": ctx.gate_count,
-                               "executed": dict(ctx.exec_stats)})
             if is_last and model.output_mode == "score_words":
                 # words: gather (bits, width, signed) per unit
                 flat = [b for w in outs for b in w.bits]
@@ -149,6 +147,9 @@ class OutPEvaluator:
                 gathered = self.comm.all_gather(local)
                 cts = np.concatenate(gathered, axis=0)
                 result = list(cts)
+            # after the export: its flush ran the block's remaining gates
+            self.stats.append({"block": bi, "units": (lo, hi), "counted_gates": ctx.gate_count,
+                               "executed": dict(ctx.exec_stats)})
         return result
 
     @staticmethod

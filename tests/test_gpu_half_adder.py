@@ -127,3 +127,44 @@ def test_half_adder_phase_noise(engine, keys):
     assert abs(s_and / pred_and - 1) < 0.3, (s_and, pred_and)
     assert abs(s_xor / pred_xor - 1) < 0.3, (s_xor, pred_xor)
     assert np.abs(err).max() < 0.125 / 2
+
+
+def test_half_adder_level_split_into_chunks_is_identical():
+    """A level of HA records (plus LIN2) wider than the per-launch work limit
+    is split into chunks; each chunk numbers its second-extraction rows and
+    XOR key switches locally, so the result must not depend on the split."""
+    import subprocess
+    import sys
+
+    code = r'''
+import os, sys, numpy as np
+sys.path.insert(0, os.getcwd())
+from paper_1806_03461_b200 import tfhe
+keys = tfhe.KeySet(seed=42)
+eng = tfhe.Engine(keys)
+n, n_in = 300, 64
+rng = np.random.default_rng(9)
+eng.reserve(n_in + 2 * n)
+eng.upload(0, keys.encrypt(rng.integers(0, 2, n_in).astype(np.uint8), seed=6, stream=1))
+recs = tfhe.gate_records(n)
+src = np.stack([rng.choice(n_in, 2, replace=False) for _ in range(n)])
+recs["src_a"], recs["src_b"] = src[:, 0], src[:, 1]
+recs["alpha"], recs["beta"] = rng.choice((-1, 1), n), rng.choice((-1, 1), n)
+recs["gamma"] = recs["alpha"] * recs["beta"]
+recs["c0"] = (-(1 << 29)) & 0xFFFFFFFF
+recs["kind"] = np.where(np.arange(n) % 4 == 0, 0, 3)   # every 4th record a plain AND
+recs["gamma"][recs["kind"] == 0] = 0
+recs["dst"], recs["src_c"] = n_in + np.arange(n), n_in + n + np.arange(n)
+eng.run_gates(recs)
+np.save(sys.argv[1], eng.download(n_in, 2 * n))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for mw in ("0", "50"):
+        path = f"/tmp/hb_ha_chunk_{mw}.npy"
+        env = dict(os.environ)
+        if mw != "0":
+            env["HEBNN_B200_MAX_WORK"] = mw
+        subprocess.run([sys.executable, "-c", code, path], check=True, cwd=root, env=env)
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])

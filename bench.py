@@ -532,6 +532,8 @@ def run_ours(args, dist):
     elif dist.rank == 0 and args.bnn != "none":
         try:
             line["bnn"] = bnn_latency(args.bnn, args.seed)
+            if args.bnn in ("layer", "cfg2l"):  # configs[1] also names the single neuron
+                line["bnn_neuron"] = bnn_latency("neuron", args.seed)
         except Exception as exc:  # report, never hide
             line["bnn"] = {"error": repr(exc)}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:

@@ -23,8 +23,44 @@ def test_invalid_records_are_value_errors(engine, keys):
     recs[0] = (10 ** 9, 0, 1, 0, 0, 1, 1, 0, 0)  # slot beyond capacity
     with pytest.raises(ValueError, match="capacity"):
         engine.run_gates(recs)
+    recs[0] = (2, 0, 1, 5, 0, 1, 1, 3, 0)  # half adder without an XOR orientation (gamma 0)
+    with pytest.raises(ValueError, match="HA record"):
+        engine.run_gates(recs)
+    recs[0] = (2, 0, 1, 2, 0, 1, 1, 3, 1)  # half adder writing both outputs to one slot
+    with pytest.raises(ValueError, match="HA record"):
+        engine.run_gates(recs)
     engine.run_gates(tfhe.gate_records(0))  # empty level is a no-op
     engine.sync()
+
+
+def test_pool_growth_while_levels_are_queued(keys):
+    """Stream-ordered pool growth between queued levels and async copies:
+    slots written before the growth keep their values, levels after it see
+    them, async uploads issued before it land in the new allocation."""
+    eng = tfhe.Engine(keys)
+    n = 600
+    rng = np.random.default_rng(11)
+    a, b = rng.integers(0, 2, n).astype(np.uint8), rng.integers(0, 2, n).astype(np.uint8)
+    eng.reserve(5 * n)
+    eng.upload(0, np.concatenate([keys.encrypt(a, seed=1, stream=1), keys.encrypt(b, seed=1, stream=2)]))
+    recs = tfhe.gate_records(n)
+    c0, al, be = tfhe.GATE_LIN["AND"]
+    recs["dst"], recs["src_a"], recs["src_b"] = np.arange(2 * n, 3 * n), np.arange(n), np.arange(n, 2 * n)
+    recs["c0"], recs["alpha"], recs["beta"] = c0, al, be
+    eng.run_gates(recs)                        # queued on the engine stream
+    c = rng.integers(0, 2, n).astype(np.uint8)
+    eng.upload_async(3 * n, keys.encrypt(c, seed=1, stream=3))
+    eng.reserve(50_000)                        # grows while the level (and the copy) may still run
+    recs2 = tfhe.gate_records(n)
+    c0, al, be = tfhe.GATE_LIN["XOR"]
+    recs2["dst"], recs2["src_a"], recs2["src_b"] = np.arange(4 * n, 5 * n), np.arange(2 * n, 3 * n), np.arange(n)
+    recs2["c0"], recs2["alpha"], recs2["beta"] = c0, al, be
+    eng.run_gates(recs2)
+    eng.sync()
+    assert np.array_equal(keys.decrypt(eng.download(2 * n, n)), a & b)
+    assert np.array_equal(keys.decrypt(eng.download(4 * n, n)), (a & b) ^ a)
+    assert np.array_equal(keys.decrypt(eng.download(3 * n, n)), c)
+    eng.close()
 
 
 def test_pool_growth_preserves_contents(keys):

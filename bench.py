@@ -68,10 +68,42 @@ def parse_args():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compare", action="store_true", help="skip the CGGI-key-layout comparison leg")
-    ap.add_argument("--bnn", choices=("none", "neuron", "layer", "cfg3", "cfg4", "cfg5"), default="layer",
-                    help="extra encrypted-BNN latency measurement (BASELINE configs 2-5): one GPU on rank 0, "
-                         "or Out-P over all ranks for N > 1")
-    return ap.parse_args()
+    ap.add_argument("--plan", action="store_true",
+                    help="print the rank layout (n_gpus, backend, devices) as one JSON line and exit (launcher test)")
+    ap.add_argument("--bnn", default="all",
+                    help="encrypted-BNN latency legs (BASELINE configs 2-5), comma-separated from "
+                         "cfg2n,cfg2l,cfg3,cfg4,cfg5 (aliases neuron, layer), 'all' or 'none': one GPU on "
+                         "rank 0, or Out-P / batch sharding over all ranks for N > 1")
+    args = ap.parse_args()
+    alias = {"neuron": "cfg2n", "layer": "cfg2l"}
+    if args.bnn == "none":
+        args.bnn_list = []
+    elif args.bnn == "all":
+        args.bnn_list = list(BNN_CONFIGS)
+    else:
+        args.bnn_list = [alias.get(c, c) for c in args.bnn.split(",") if c]
+        bad = [c for c in args.bnn_list if c not in BNN_CONFIGS]
+        if bad:
+            ap.error(f"--bnn: unknown config(s) {bad}; choose from {BNN_CONFIGS}")
+    return args
+
+
+BNN_CONFIGS = ("cfg2n", "cfg2l", "cfg3", "cfg4", "cfg5")
+
+
+def spawn_ranks(args):
+    """`python bench.py --gpus N` (N > 1) without a launcher: start the N ranks
+    ourselves through torch.distributed.run (127.0.0.1 rendezvous), so the
+    number of GPUs timed is always the number asked for.  Returns the exit code."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"bench.py: spawning {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
 
 
 # ---------------------------------------------------------------------------
@@ -93,6 +125,8 @@ class Dist:
         self.share = os.environ.get("HB_BENCH_SHARE_GPU") == "1"
         self.local_rank = 0 if self.share else int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.backend = None
+        self.nccl_log = None
         if self.world > 1:
             import torch
             import torch.distributed as dist
@@ -100,7 +134,14 @@ class Dist:
             backend = "nccl" if torch.cuda.is_available() and not self.share else "gloo"
             if backend == "nccl":
                 torch.cuda.set_device(self.local_rank)
+                # keep NCCL's communicator lines (ring/NVLS setup) as evidence, in a file so that
+                # stdout stays one JSON line; rank 0 quotes them in its line ("nccl")
+                self.nccl_log = os.path.join(tempfile.gettempdir(), f"hb_bench_nccl.{os.getpid()}.log")
+                os.environ.setdefault("NCCL_DEBUG", "INFO")
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+                os.environ.setdefault("NCCL_DEBUG_FILE", self.nccl_log)
             dist.init_process_group(backend=backend)
+            self.backend = backend
             self.pg = dist
             self.torch = torch
 
@@ -118,6 +159,25 @@ class Dist:
         t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=dev)
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
+
+    def gather_obj(self, obj):
+        if not self.pg:
+            return [obj]
+        out = [None] * self.world
+        self.pg.all_gather_object(out, obj)
+        return out
+
+    def nccl_lines(self, limit=24):
+        """This rank's NCCL INFO lines about its communicators (rings, NVLS, nRanks)."""
+        path = self.nccl_log
+        if not path or not os.path.exists(path):
+            return []
+        keep = []
+        with open(path, errors="replace") as f:
+            for ln in f:
+                if any(k in ln for k in ("comm 0x", "NVLS", "nRanks", "Channel 00", "Connected all", "NCCL version")):
+                    keep.append(ln.strip()[:200])
+        return keep[:limit]
 
     def close(self):
         if self.pg:
@@ -251,26 +311,59 @@ def run_reference(args, dist):
 # our arm
 # ---------------------------------------------------------------------------
 
-def bnn_latency(kind, seed):
+def bnn_latency(cfg, seed, trials=2):
     """BASELINE configs 2-5 through the reference compiler on TfheContext
     (engine created and warmed before the timed flush)."""
     from paper_1806_03461_b200 import workloads
     from paper_1806_03461_b200.backend import TfheContext
 
-    cfg = {"neuron": "cfg2n", "layer": "cfg2l"}.get(kind, kind)
     warm = TfheContext(seed=seed)
     warm.decrypt(warm.g_and(warm.encrypt(1), warm.encrypt(1)))  # CUDA context, BK FFT, KSK upload
-    # two fresh contexts (each builds its DAG from scratch); the second finds the engine's
+    # fresh contexts (each builds its DAG from scratch); a second one finds the engine's
     # pools already grown, as a serving process would
-    trials = [workloads.run_encrypted(TfheContext, cfg, seed=seed, replays=1) for _ in range(2)]
-    rep = min(trials, key=lambda r: r["first_eval_s"])
-    rep["first_eval_trials_s"] = [r["first_eval_s"] for r in trials]
+    runs = [workloads.run_encrypted(TfheContext, cfg, seed=seed, replays=1, cached=(t == trials - 1))
+            for t in range(trials)]
+    rep = min(runs, key=lambda r: r["first_eval_s"])
+    rep["first_eval_trials_s"] = [r["first_eval_s"] for r in runs]
+    rep["cached"] = runs[-1]["cached"]
     rep["note"] = ("first_eval_s = encrypt + DAG build through the reference compiler (background device "
-                   "flushes overlap it) + final flush + decrypt of one batch, best of two fresh contexts "
-                   "(first_eval_trials_s); rates are over first_eval_s; replay.latency_s = a new encrypted "
-                   "batch through the cached DAG (upload, every level on the device, decrypt)")
-    rep["reference_cpu"] = workloads.run_sim_reference(cfg, seed=seed)
+                   "flushes overlap it) + final flush + decrypt of one batch, best of the fresh contexts in "
+                   "first_eval_trials_s; rates are over first_eval_s; replay.latency_s = a new encrypted "
+                   "batch through the same context's DAG (upload, every level on the device, decrypt); "
+                   "cached.first_eval_s = a fresh context running the compiled level schedule "
+                   "(workloads.compile_schedule) without the reference compiler")
+    ref = workloads.run_sim_reference(cfg, seed=seed)
+    rep["reference_cpu"] = ref
+    rep["counted_gates_match_simcontext"] = ref["counted_gates_per_input"] == rep["counted_gates_per_input"]
     return rep
+
+
+def strong_scaling_leg(args, dist, eng, recs, weak_value, weak_ms):
+    """cfg1 strong scaling (SURVEY §8e first row): the 4,096 gates of one job
+    split over the N ranks (4,096/N per GPU, no collective: gates are
+    independent), timed like the weak-scaling steps (L2 flushed, CUDA events on
+    the engine stream, max over ranks).  At N = 1 it is the headline step."""
+    total = args.gates
+    if dist.world == 1:
+        return {"gates_total": total, "gates_per_gpu": total, "n_gpus": 1, "value": weak_value,
+                "ms_per_step": weak_ms, "unit": "gates/s", "note": "N = 1: identical to the headline step"}
+    per = -(-total // dist.world)
+    mine = recs[dist.rank * per:min(total, (dist.rank + 1) * per)]
+    for _ in range(args.warmup):
+        eng.run_gates(mine)
+    eng.sync()
+    dist.barrier()
+    tot = 0.0
+    for _ in range(args.steps):
+        eng.flush_l2()
+        eng.sync()
+        eng.run_gates(mine)
+        br, ks = eng.last_timing()
+        tot += br + ks
+    step_s = dist.max(tot / 1e3) / args.steps
+    return {"gates_total": total, "gates_per_gpu": per, "n_gpus": dist.world, "value": total / step_s,
+            "ms_per_step": 1e3 * step_s, "unit": "gates/s", "scaling": "strong",
+            "note": "one 4,096-gate job split over the ranks; time = max over ranks"}
 
 
 def cggi_layout_leg(args, dist, dev, recs, h_in, steps=5):
@@ -305,7 +398,7 @@ def cggi_layout_leg(args, dist, dev, recs, h_in, steps=5):
             "note": "CGGI key layout (one TGSW per key bit), same inputs, L2 flushed per step"}
 
 
-def bnn_outp(kind, seed, dist, dev):
+def bnn_outp(cfg, seed, dist, dev):
     """N > 1: one batch of BASELINE config `kind` with Out-P:
     every rank evaluates a cost-balanced slice of each layer's output units on
     its own GPU (its own DAG, built concurrently) and the layer's output
@@ -317,7 +410,6 @@ def bnn_outp(kind, seed, dist, dev):
     from paper_1806_03461_b200.backend import TfheContext, shared_keys
     from hebnn.model import oracle_eval
 
-    cfg = {"neuron": "cfg2n", "layer": "cfg2l"}.get(kind, kind)
     model, batch = workloads.build(cfg, seed)
     X = workloads.inputs(cfg, model, batch, seed + 1)
     keys = shared_keys(seed)  # deterministic: identical on every rank
@@ -398,6 +490,11 @@ def run_ours(args, dist):
 
     from paper_1806_03461_b200 import tfhe
 
+    if args.plan:
+        ranks = dist.gather_obj({"rank": dist.rank, "local_rank": dist.local_rank,
+                                 "world": dist.world, "pid": os.getpid()})
+        return {"plan": True, "n_gpus": dist.world, "backend": dist.backend, "ranks": ranks,
+                "share_gpu": dist.share}
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the engine has no CPU fallback)")
     dev = dist.local_rank
@@ -524,22 +621,34 @@ def run_ours(args, dist):
         "clocks": clk,
         "correct": correct,
     }
+    line["strong_scaling"] = strong_scaling_leg(args, dist, eng, recs, value, statistics.mean(step_ms))
     if not args.no_compare:
         line["alt_layout"] = cggi_layout_leg(args, dist, dev, recs, h_in)
-    if args.bnn != "none" and dist.world > 1:
+    if args.bnn_list:
+        line["bnn"] = {}
+    for cfg in args.bnn_list:
         try:
-            rep = bnn_outp(args.bnn, args.seed, dist, dev)
-            if dist.rank == 0:
-                line["bnn"] = rep
+            if dist.world > 1:
+                rep = bnn_outp(cfg, args.seed, dist, dev)
+            elif dist.rank == 0:
+                rep = bnn_latency(cfg, args.seed, trials=2 if cfg in ("cfg2n", "cfg2l") else 1)
+            else:
+                rep = None
         except Exception as exc:  # report, never hide
-            line["bnn"] = {"error": repr(exc)}
-    elif dist.rank == 0 and args.bnn != "none":
-        try:
-            line["bnn"] = bnn_latency(args.bnn, args.seed)
-            if args.bnn in ("layer", "cfg2l"):  # configs[1] also names the single neuron
-                line["bnn_neuron"] = bnn_latency("neuron", args.seed)
-        except Exception as exc:  # report, never hide
-            line["bnn"] = {"error": repr(exc)}
+            rep = {"error": repr(exc)}
+        if dist.rank == 0:
+            line["bnn"][cfg] = rep
+    if args.bnn_list and dist.rank == 0:
+        line["bnn_all_match_oracle_eval"] = all(
+            isinstance(r, dict) and r.get("matches_oracle_eval") is True
+            and (r.get("replay") or {}).get("matches_oracle_eval", True) is True
+            and (r.get("cached") or {}).get("matches_oracle_eval", True) is True
+            for r in line["bnn"].values())
+    if dist.world > 1:
+        dist.barrier()
+        lines = dist.nccl_lines()
+        if dist.rank == 0:
+            line["nccl"] = {"backend": dist.backend, "log_lines": lines}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         sample = 128 * threads  # ~10 s of wall time (~150 core-seconds) of exact CGGI on the host
@@ -557,6 +666,11 @@ def run_ours(args, dist):
 
 def main():
     args = parse_args()
+    world = os.environ.get("WORLD_SIZE")
+    if args.impl == "ours" and args.gpus > 1 and world is None:
+        sys.exit(spawn_ranks(args))
+    if args.impl == "ours" and world is not None and int(world) != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}: refusing to report a wrong n_gpus")
     if args.impl == "reference":
         # CPU arm: rank 0 alone runs; no process group, other ranks exit 0 without work
         if int(os.environ.get("RANK", "0")) != 0:

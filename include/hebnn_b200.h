@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define HB_ABI_VERSION 3
+#define HB_ABI_VERSION 4
 
 /* status codes */
 #define HB_OK 0
@@ -93,6 +93,11 @@ typedef struct hb_engine hb_engine;
 int hb_abi_version(void);
 const char *hb_last_error(void);
 void hb_default_params(hb_params *p);
+/* 1 if the kernels support these parameters (N = 1024, k = 1, Bg = 2^7, l = 3,
+ * KS 2^2 x 8, 0 < n <= 639, even n for key pairs), else 0. Every entry point
+ * taking params also checks them (HB_EINVAL); this lets a loader validate a
+ * deserialised key document before sizing buffers from it. (ABI v4) */
+int hb_params_valid(const hb_params *p);
 size_t hb_lwe_words(const hb_params *p);   /* n + 1 */
 size_t hb_bk_words(const hb_params *p);    /* T * (k+1)l * (k+1) * N, T = n (bk_unroll 1) or 3n/2 (2) */
 size_t hb_ksk_words(const hb_params *p);   /* kN * t * (base-1) * (n+1) */

@@ -27,7 +27,7 @@ GATE_HA = 3
 
 # Every symbol the header declares (tests check the library exports them all).
 EXPORTED = (
-    "hb_abi_version", "hb_last_error", "hb_default_params", "hb_lwe_words", "hb_bk_words",
+    "hb_abi_version", "hb_last_error", "hb_default_params", "hb_params_valid", "hb_lwe_words", "hb_bk_words",
     "hb_ksk_words", "hb_keygen", "hb_encrypt", "hb_phase", "hb_decrypt", "hb_engine_create",
     "hb_engine_destroy", "hb_pool_reserve", "hb_pool_capacity", "hb_pool_stride", "hb_pool_upload",
     "hb_pool_download", "hb_pool_gather", "hb_run_gates", "hb_sync", "hb_last_timing",
@@ -105,6 +105,7 @@ def lib():
         "hb_abi_version": ([], ctypes.c_int),
         "hb_last_error": ([], ctypes.c_char_p),
         "hb_default_params": ([P(HbParams)], None),
+        "hb_params_valid": ([P(HbParams)], ctypes.c_int),
         "hb_lwe_words": ([P(HbParams)], sz),
         "hb_bk_words": ([P(HbParams)], sz),
         "hb_ksk_words": ([P(HbParams)], sz),

@@ -38,9 +38,14 @@ import weakref
 
 import numpy as np
 
-from . import gate_api as api
+try:  # the reference's own plugin interface (backend.py:23-150): a hard dependency of the drop-in
+    from hebnn import backend as _ref_backend
+    from hebnn.backend import AND, MUX, OR, XNOR, XOR, CipherBit, ContextMismatchError, GateBackend, GateStats, ScopeError
+except ImportError as _exc:  # pragma: no cover
+    raise ImportError("paper_1806_03461_b200.backend implements hebnn.backend.GateBackend: install the reference "
+                      "package (pip install --target baseline/_ref /root/reference/pkg) or put it on sys.path") from _exc
+
 from ._native import GATE_DTYPE, GATE_HA, GATE_LIN2, GATE_LIN3, GATE_MUX, dag_module
-from .gate_api import AND, MUX, OR, XNOR, XOR, CipherBit, ContextMismatchError, GateBackend, GateStats, ScopeError
 from .tfhe import EIGHTH, MASK32, Engine, KeySet
 
 # node opcodes of the native gate DAG (csrc/hb_dag.cpp): node 0 is the constant 0
@@ -143,9 +148,10 @@ def shared_engine(keys, device):
         return ent
 
 
-def _release_chunks(pool, chunks):
-    for base, size in chunks:
-        pool.release(base, size)
+def _release_chunks(pool, *chunk_lists):
+    for chunks in chunk_lists:
+        for base, size in chunks:
+            pool.release(base, size)
 
 
 # ---------------------------------------------------------------------------
@@ -206,6 +212,7 @@ class TfheContext(GateBackend):
         self._slots = None
         self._history = []     # every executed (level, records) batch, in order (f1 replay)
         self._chunks = []
+        self._sched_chunks = []  # pool chunks of compiled-schedule runs (run_schedule)
         self._finalizer = None
         self.stream_at = int(stream_at)  # pending gates that start a background flush (0: off)
         self.stream_min_width = int(stream_min_width)
@@ -224,22 +231,38 @@ class TfheContext(GateBackend):
     def _ensure_engine(self):
         if self._engine is None:
             self._engine, self._slots = shared_engine(self.keys, self.device)
-            self._finalizer = weakref.finalize(self, _release_chunks, self._slots, self._chunks)
+            self._finalizer = weakref.finalize(self, _release_chunks, self._slots, self._chunks, self._sched_chunks)
         return self._engine
 
 
-    def _map_slots(self, logical):
+    def _map_slots(self, logical, chunks=None, count=None):
         """Logical slots -> engine record slots (chunks of the shared pool are
         reserved on demand, aligned to `lanes` so slot * lanes + lane is the
-        physical pool index)."""
+        physical pool index).  `chunks`/`count`: another chunk list (compiled
+        schedules) covering `count` logical slots."""
         self._ensure_engine()
-        need = (self._dag.size() - 1) // self._CHUNK + 1
-        while len(self._chunks) < need:
+        if chunks is None:
+            chunks, count = self._chunks, self._dag.size()
+        need = (max(count, 1) - 1) // self._CHUNK + 1
+        while len(chunks) < need:
             base = self._slots.alloc(self._CHUNK * self.lanes, align=self.lanes)
-            self._chunks.append((base, self._CHUNK * self.lanes))
-        bases = np.array([b // self.lanes for b, _ in self._chunks], dtype=np.int64)
+            chunks.append((base, self._CHUNK * self.lanes))
+        bases = np.array([b // self.lanes for b, _ in chunks], dtype=np.int64)
         logical = np.asarray(logical, dtype=np.int64)
         return bases[logical // self._CHUNK] + logical % self._CHUNK
+
+    def _unmap_slots(self, phys):
+        """Inverse of _map_slots over this context's chunks; record slots outside
+        them (the unused src_c of two-input records) map to logical 0."""
+        bases = np.array([b // self.lanes for b, _ in self._chunks], dtype=np.int64)
+        order = np.argsort(bases)
+        phys = np.asarray(phys, dtype=np.int64)
+        k = np.searchsorted(bases[order], phys, side="right") - 1
+        ok = k >= 0
+        ci = order[np.maximum(k, 0)]
+        off = phys - bases[ci]
+        ok &= (off >= 0) & (off < self._CHUNK)
+        return np.where(ok, ci * self._CHUNK + off, 0)
 
     # -- checks / stats (SimContext._check/_record, backend.py:194-203) --------
 
@@ -385,6 +408,11 @@ class TfheContext(GateBackend):
             nids = [self._dag.add_input() for _ in range(cts.shape[0])]
             if nids:
                 eng = self._ensure_engine()
+                # the engine copies on its own (non-blocking) stream: the producer of `cts`
+                # (an NCCL all-gather, torch.cat, .contiguous()) ran on torch's current stream
+                import torch
+
+                torch.cuda.current_stream(cts.device).synchronize()
                 phys = np.asarray(self._map_slots(np.asarray(nids, dtype=np.int64) - 1), dtype=np.int64)
                 breaks = np.flatnonzero(np.diff(phys) != 1) + 1
                 words = self.params.n + 1
@@ -439,7 +467,7 @@ class TfheContext(GateBackend):
     def g_not(self, a):
         """SimContext.g_not (backend.py:223-228): free sign flip."""
         self._check(a)
-        if not api.not_is_free():
+        if not _ref_backend.NOT_IS_FREE:
             return self.g_xnor(a, self.trivial_const(0))
         trivial = None if a.trivial_value is None else 1 - a.trivial_value
         with self._lock:
@@ -697,6 +725,85 @@ class TfheContext(GateBackend):
             self.exec_stats["replays"] = self.exec_stats.get("replays", 0) + 1
             self.exec_stats["flush_s"] += time.perf_counter() - t0
 
+    def compile_schedule(self, inputs, outputs, meta=None):
+        """Compile once, serve many: the level schedule this
+        context executed, in logical slots, with the slot maps of `inputs`
+        (non-negated input handles) and `outputs` (any handles).  A fresh
+        context runs it on new ciphertexts with `run_schedule` without the
+        reference compiler or the gate DAG.  The schedule is key-independent."""
+        self._check(*inputs, *outputs)
+        with self._lock:
+            live = [h._value >> 1 for h in outputs if (h._value >> 1) != 0]
+            for nid in live:
+                self._dag.revive(nid)
+            if self._dag.pending_count() or any(not self._dag.is_done(nid) for nid in live):
+                self.flush()
+            self._join_bg()
+            nids = [h._value >> 1 for h in inputs]
+            if any(nid == 0 or self._dag.op(nid) != _OP_INPUT for nid in nids) or any(h._value & 1 for h in inputs):
+                raise ValueError("schedule inputs must be (non-negated) input handles")
+            levels = []
+            for _lvl, recs in self._replay_schedule():
+                r = recs.copy()
+                for f in Schedule.SLOT_FIELDS:
+                    r[f] = self._unmap_slots(recs[f])
+                levels.append(r)
+            out_refs = np.array([h._value for h in outputs], dtype=np.int64)
+            ins = np.array(nids, dtype=np.int64) - 1
+            outs = (out_refs >> 1) - 1  # -1: a public constant
+            used = [ins, outs] + [r[f].astype(np.int64) for r in levels for f in Schedule.SLOT_FIELDS]
+            n_slots = int(max((int(u.max()) for u in used if u.size), default=-1)) + 1
+            return Schedule(levels, ins, outs, (out_refs & 1).astype(np.uint8), n_slots, self.lanes,
+                            self.params.n, dict(meta or {}, counted=self.global_stats.as_dict()))
+
+    def run_schedule(self, sched, cts):
+        """Run a compiled schedule on new input ciphertexts `cts` [inputs][lanes][n+1]
+        (or [inputs][n+1] for lanes == 1); returns the output ciphertexts
+        [outputs][lanes][n+1] (NOT flags applied, constants as trivial samples).
+        Uses pool chunks of its own: the context's DAG is untouched."""
+        if sched.lanes != self.lanes or sched.n != self.params.n:
+            raise ValueError(f"schedule compiled for lanes={sched.lanes}, n={sched.n}; "
+                             f"context has lanes={self.lanes}, n={self.params.n}")
+        cts = np.asarray(cts, dtype=np.uint32)
+        if cts.ndim == 2:
+            cts = cts[:, None, :]
+        if cts.shape != (sched.inputs.size, self.lanes, self.params.n + 1):
+            raise ValueError(f"expected [{sched.inputs.size}, {self.lanes}, {self.params.n + 1}] ciphertexts")
+        with self._lock:
+            self._join_bg()
+            t0 = time.perf_counter()
+            eng = self._ensure_engine()
+            mp = lambda v: self._map_slots(v, self._sched_chunks, sched.n_slots)  # noqa: E731
+            phys = np.asarray(mp(sched.inputs), dtype=np.int64)
+            order = np.argsort(phys, kind="stable")
+            ps = phys[order]
+            breaks = np.flatnonzero(np.diff(ps) != 1) + 1
+            try:
+                for run in np.split(np.arange(ps.size), breaks):
+                    block = cts[order[run]].reshape(run.size * self.lanes, -1)
+                    eng.upload(int(ps[run[0]]) * self.lanes, block)
+                for recs in sched.levels:
+                    r = recs.copy()
+                    for f in Schedule.SLOT_FIELDS:
+                        r[f] = mp(recs[f].astype(np.int64))
+                    eng.run_gates(r, lanes=self.lanes)
+                out = np.zeros((sched.outputs.size, self.lanes, self.params.n + 1), np.uint32)
+                var = np.flatnonzero(sched.outputs >= 0)
+                if var.size:
+                    op = np.asarray(mp(sched.outputs[var]), dtype=np.int64)
+                    idx = (op[:, None] * self.lanes + np.arange(self.lanes)[None, :]).reshape(-1)
+                    out[var] = eng.gather(idx.astype(np.uint32)).reshape(var.size, self.lanes, -1)
+            except RuntimeError as exc:
+                raise DeviceError(str(exc)) from exc
+            const = sched.outputs < 0
+            # public constants: trivial samples (0, +-1/8); NOT flags: mod-2^32 negation
+            out[const, :, -1] = np.where(sched.out_neg[const, None] == 1, EIGHTH, (-EIGHTH) & MASK32)
+            neg = (sched.out_neg == 1) & ~const
+            out[neg] = np.uint32(0) - out[neg]
+            self.exec_stats["schedule_runs"] = self.exec_stats.get("schedule_runs", 0) + 1
+            self.exec_stats["flush_s"] += time.perf_counter() - t0
+            return out
+
     def _replay_schedule(self):
         """The executed history regrouped by node level: streaming flushes split
         a model's levels over several launches; a replay runs each level once."""
@@ -781,4 +888,57 @@ class TfheContext(GateBackend):
             return -ph if c._value & 1 else ph
 
 
-__all__ = ["TfheContext", "DeviceError", "shared_keys", "shared_engine"]
+class Schedule:
+    """A compiled model (TfheContext.compile_schedule): executed level records
+    in logical slots, input/output slot maps, lanes and n; save/load as .npz."""
+
+    SLOT_FIELDS = ("dst", "src_a", "src_b", "src_c")
+
+    def __init__(self, levels, inputs, outputs, out_neg, n_slots, lanes, n, meta):
+        self.levels = list(levels)
+        self.inputs = np.asarray(inputs, dtype=np.int64)
+        self.outputs = np.asarray(outputs, dtype=np.int64)
+        self.out_neg = np.asarray(out_neg, dtype=np.uint8)
+        self.n_slots, self.lanes, self.n = int(n_slots), int(lanes), int(n)
+        self.meta = meta
+
+    @property
+    def records(self):
+        return sum(r.size for r in self.levels)
+
+    def save(self, path):
+        import json
+
+        sizes = np.array([r.size for r in self.levels], dtype=np.int64)
+        recs = np.concatenate(self.levels) if self.levels else np.zeros(0, GATE_DTYPE)
+        hdr = json.dumps({"format": "hebnn-b200/schedule", "version": 1, "n_slots": self.n_slots,
+                          "lanes": self.lanes, "n": self.n, "meta": self.meta})
+        np.savez(path, header=np.frombuffer(hdr.encode(), np.uint8), records=recs, sizes=sizes,
+                 inputs=self.inputs, outputs=self.outputs, out_neg=self.out_neg)
+
+    @classmethod
+    def load(cls, path):
+        import json
+
+        with np.load(path, allow_pickle=False) as z:
+            hdr = json.loads(bytes(z["header"]).decode())
+            if hdr.get("format") != "hebnn-b200/schedule" or hdr.get("version") != 1:
+                raise ValueError("not a hebnn-b200 schedule document")
+            recs = z["records"]
+            if recs.dtype != GATE_DTYPE:
+                raise ValueError("schedule records have the wrong layout")
+            sizes = z["sizes"]
+            if sizes.sum() != recs.size or (sizes < 0).any():
+                raise ValueError("schedule level sizes do not match its records")
+            n_slots = int(hdr["n_slots"])
+            for f in cls.SLOT_FIELDS:
+                if recs.size and int(recs[f].max()) >= n_slots:
+                    raise ValueError("schedule record slot beyond n_slots")
+            ins, outs = z["inputs"], z["outputs"]
+            if (ins.size and (ins.min() < 0 or ins.max() >= n_slots)) or (outs.size and outs.max() >= n_slots):
+                raise ValueError("schedule slot map beyond n_slots")
+            levels = np.split(recs, np.cumsum(sizes)[:-1]) if sizes.size else []
+            return cls(levels, ins, outs, z["out_neg"], n_slots, hdr["lanes"], hdr["n"], hdr["meta"])
+
+
+__all__ = ["TfheContext", "DeviceError", "Schedule", "shared_keys", "shared_engine"]

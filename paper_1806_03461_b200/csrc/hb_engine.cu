@@ -67,7 +67,9 @@ struct hb_engine {
     cudaEvent_t ev_upload = nullptr;      // last async upload (the next level waits on it)
     cudaEvent_t ev_compute = nullptr;     // compute point an async download waits on
     cudaEvent_t ev_prev_level = nullptr;  // compute stream before the most recent level
+    cudaEvent_t ev_download = nullptr;    // last async download (pool writers wait on it: no WAR)
     bool pending_upload = false;
+    bool pending_download = false;
     double2 *d_W = nullptr, *d_TW = nullptr, *d_PSI = nullptr;
     int unroll = 1;  // bk_unroll of the loaded key
     double2 *d_bkf = nullptr;
@@ -184,7 +186,9 @@ int launch_ks(hb_engine *e, const KsArgs &a0) {
         if (rc) return rc;
         a.partial = e->d_kspart;
     }
-    const dim3 grid((a.n_work + kKsThreads - 1) / kKsThreads, kKsChunks, splits);
+    // only the chunks holding output columns 0..n (79 of 80 at n = 630)
+    const uint32_t chunks = (a.n + kKsCols) / kKsCols;
+    const dim3 grid((a.n_work + kKsThreads - 1) / kKsThreads, chunks, splits);
     k_keyswitch<<<grid, kKsThreads, 0, e->stream>>>(a);
     HB_CUDA_TRY(cudaGetLastError());
     e->n_launch++;
@@ -318,6 +322,7 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
     HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_upload, cudaEventDisableTiming));
     HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_compute, cudaEventDisableTiming));
     HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_prev_level, cudaEventDisableTiming));
+    HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_download, cudaEventDisableTiming));
     HB_CUDA_TRY(cudaEventRecord(e->ev_prev_level, e->stream));
     HB_CUDA_TRY(cudaEventRecord(e->ev_stage, e->stream));
 
@@ -442,10 +447,21 @@ int hb_engine_destroy(hb_engine *e) {
             cudaStreamSynchronize(st);
             cudaStreamDestroy(st);
         }
-    for (cudaEvent_t ev : {e->ev_upload, e->ev_compute, e->ev_prev_level})
+    for (cudaEvent_t ev : {e->ev_upload, e->ev_compute, e->ev_prev_level, e->ev_download})
         if (ev) cudaEventDestroy(ev);
     if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
+    return HB_OK;
+}
+
+// Write-after-read fence: a pool write issued after hb_pool_download_async must not
+// overtake the copy still reading those slots on the d2h stream (the header's
+// double-buffered pattern rewrites step k-2's output slots at step k).
+static int order_after_downloads(hb_engine *e, cudaStream_t st) {
+    if (e->pending_download) {
+        HB_CUDA_TRY(cudaStreamWaitEvent(st, e->ev_download, 0));
+        if (st == e->stream) e->pending_download = false;  // later stream-ordered writers inherit it
+    }
     return HB_OK;
 }
 
@@ -493,6 +509,7 @@ int hb_pool_upload(hb_engine *e, size_t first, size_t count, const uint32_t *hos
     }
     if (!count) return HB_OK;
     HB_CUDA_TRY(cudaSetDevice(e->device));
+    if (int rc = order_after_downloads(e, e->stream)) return rc;
     HB_CUDA_TRY(cudaMemcpy2DAsync(e->d_pool + first * e->pool_stride, e->pool_stride * 4, host, host_stride * 4,
                                   (size_t)(e->p.n + 1) * 4, count, cudaMemcpyHostToDevice, e->stream));
     return HB_OK;
@@ -545,6 +562,7 @@ int hb_pool_put_device(hb_engine *e, size_t first_slot, size_t count, const uint
     }
     if (!count) return HB_OK;
     HB_CUDA_TRY(cudaSetDevice(e->device));
+    if (int rc = order_after_downloads(e, e->stream)) return rc;
     HB_CUDA_TRY(cudaMemcpy2DAsync(e->d_pool + first_slot * e->pool_stride, (size_t)e->pool_stride * 4, dev_in,
                                   dev_stride * 4, ((size_t)e->p.n + 1) * 4, count, cudaMemcpyDeviceToDevice, e->stream));
     HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
@@ -696,6 +714,8 @@ static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_
     k.pool = e->d_pool;
     k.pool_stride = e->pool_stride;
     k.n = e->p.n;
+    // the key switch writes pool slots: after any async download still reading them
+    if ((rc = order_after_downloads(e, e->stream))) return rc;
     if ((rc = launch_ks(e, k))) return rc;
     HB_CUDA_TRY(cudaEventRecord(e->ev[2], e->stream));
     e->n_br += nbr * lanes;
@@ -721,6 +741,7 @@ int hb_pool_upload_async(hb_engine *e, size_t first, size_t count, const uint32_
     HB_CUDA_TRY(cudaSetDevice(e->device));
     // may overlap the most recently issued level, never an earlier one (double buffering)
     HB_CUDA_TRY(cudaStreamWaitEvent(e->h2d_stream, e->ev_prev_level, 0));
+    if (e->pending_download) HB_CUDA_TRY(cudaStreamWaitEvent(e->h2d_stream, e->ev_download, 0));
     HB_CUDA_TRY(cudaMemcpy2DAsync(e->d_pool + first * e->pool_stride, e->pool_stride * 4, host, host_stride * 4,
                                   (size_t)(e->p.n + 1) * 4, count, cudaMemcpyHostToDevice, e->h2d_stream));
     HB_CUDA_TRY(cudaEventRecord(e->ev_upload, e->h2d_stream));
@@ -740,6 +761,8 @@ int hb_pool_download_async(hb_engine *e, size_t first, size_t count, uint32_t *h
     HB_CUDA_TRY(cudaStreamWaitEvent(e->d2h_stream, e->ev_compute, 0));
     HB_CUDA_TRY(cudaMemcpy2DAsync(host, host_stride * 4, e->d_pool + first * e->pool_stride, e->pool_stride * 4,
                                   (size_t)(e->p.n + 1) * 4, count, cudaMemcpyDeviceToHost, e->d2h_stream));
+    HB_CUDA_TRY(cudaEventRecord(e->ev_download, e->d2h_stream));
+    e->pending_download = true;
     return HB_OK;
 }
 

@@ -119,7 +119,9 @@ static void parallel_for(size_t count, int threads, F &&fn) {
 }
 
 bool params_ok(const hb_params *p) {
-    return p && p->n > 0 && p->n <= kMaxLweN && p->N == kN && p->k == 1 && p->bg_bits == kBgBits &&
+    // n + 1 <= kKskStride: the device KSK table and k_keyswitch cover kKskStride output columns
+    // (a_0..a_{n-1}, b), so a larger n would leave columns unwritten.
+    return p && p->n > 0 && p->n <= kMaxKsN && p->N == kN && p->k == 1 && p->bg_bits == kBgBits &&
            p->l == kL && p->ks_base_bits == kKsBaseBits && p->ks_t == kKsT &&
            (p->bk_unroll == 0 || p->bk_unroll == 1 || (p->bk_unroll == 2 && (p->n & 1) == 0));
 }
@@ -135,6 +137,7 @@ using namespace hb;
 extern "C" {
 
 int hb_abi_version(void) { return HB_ABI_VERSION; }
+int hb_params_valid(const hb_params *p) { return params_ok(p) ? 1 : 0; }
 
 const char *hb_last_error(void) { return g_last_error.c_str(); }
 

@@ -22,6 +22,8 @@ constexpr int kKsVals = (1 << kKsBaseBits) - 1;  // non-zero digit values
 constexpr int kMaxLweN = 1023;
 constexpr int kBigStride = 1028;  // words per extracted LWE (kN + 1, padded to 16 B)
 constexpr int kKskStride = 640;   // words per device KSK row (n + 1 padded)
+constexpr int kMaxKsN = kKskStride - 1;  // largest n the key switch covers (n + 1 output columns)
+static_assert(kMaxKsN <= kMaxLweN, "key-switch columns exceed the mod-switch buffers");
 
 void set_error(const std::string &msg);
 bool params_ok(const hb_params *p);

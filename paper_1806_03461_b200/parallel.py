@@ -125,8 +125,16 @@ class OutPEvaluator:
                 flat = [b for w in outs for b in w.bits]
                 widths = np.array([w.width for w in outs] + [0], np.int64)[:-1]
                 signed = np.array([int(w.signed) for w in outs], np.int64)
-                local = ctx.export_ciphertexts(flat) if flat else np.zeros((0, ctx.lanes, ctx.params.n + 1), np.uint32)
-                all_cts = self.comm.all_gather(local)
+                if dev_path:  # word bits gathered as device tensors (NCCL), read once at the end
+                    import torch
+
+                    local = ctx.export_ciphertexts_device(flat) if flat else torch.zeros(
+                        (0, ctx.lanes, ctx.params.n + 1), dtype=torch.int32, device=f"cuda:{ctx.device}")
+                    all_cts = [t.cpu().numpy().view(np.uint32) for t in self.comm.all_gather_tensor(local)]
+                else:
+                    local = ctx.export_ciphertexts(flat) if flat else np.zeros((0, ctx.lanes, ctx.params.n + 1),
+                                                                               np.uint32)
+                    all_cts = self.comm.all_gather(local)
                 all_w = self.comm.all_gather(widths)
                 all_s = self.comm.all_gather(signed)
                 result = []

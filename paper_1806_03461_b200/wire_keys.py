@@ -9,10 +9,12 @@ JSON header.
 
 from __future__ import annotations
 
+import ctypes
 import json
 
 import numpy as np
 
+from ._native import lib
 from .tfhe import KeySet, default_params
 
 FORMAT = "hebnn-b200/tfhe"
@@ -48,15 +50,41 @@ def save_keys(path, keys, include_secret=False):
     np.savez(path, header=np.frombuffer(_header(kind, keys.params, seed=keys.seed).encode(), np.uint8), **arrays)
 
 
+def _array(z, name, words):
+    """A 1-D little-endian uint32 array of exactly `words` elements, else ValueError:
+    the engine copies hb_bk_words / hb_ksk_words words from these host buffers."""
+    if name not in z.files:
+        raise ValueError(f"key document lacks {name!r}")
+    a = z[name]
+    if a.dtype != np.dtype("<u4") or a.ndim != 1 or a.size != words:
+        raise ValueError(f"{name}: expected uint32[{words}], got {a.dtype}{list(a.shape)}")
+    return np.ascontiguousarray(a)
+
+
 def load_keys(path):
-    with np.load(path) as z:
+    """Load a key document, validating it before any buffer is sized from it: the
+    server loads client-supplied files, so params must be ones the kernels support
+    and every array must have exactly the length those params imply."""
+    with np.load(path, allow_pickle=False) as z:
         doc = json.loads(bytes(z["header"]).decode())
         if doc.get("kind") not in ("keyset", "eval_keys"):
             raise ValueError(f"not a key document: {doc.get('kind')}")
         _check(doc, doc["kind"])
-        p = _params_from(doc["params"])
-        secret = (z["lwe_key"], z["trlwe_key"]) if doc["kind"] == "keyset" else (None, None)
-        ks = KeySet(seed=None, params=p, _arrays=(secret[0], secret[1], z["bk"], z["ksk"]))
+        try:
+            p = _params_from(doc["params"])
+        except (KeyError, TypeError) as exc:
+            raise ValueError(f"bad params in key document: {exc}") from None
+        L = lib()
+        if not L.hb_params_valid(ctypes.byref(p)):
+            raise ValueError(f"key document params not supported by the kernels: {_params_doc(p)}")
+        bk = _array(z, "bk", L.hb_bk_words(ctypes.byref(p)))
+        ksk = _array(z, "ksk", L.hb_ksk_words(ctypes.byref(p)))
+        secret = (None, None)
+        if doc["kind"] == "keyset":
+            secret = (_array(z, "lwe_key", p.n), _array(z, "trlwe_key", p.k * p.N))
+            if (secret[0] > 1).any() or (secret[1] > 1).any():
+                raise ValueError("secret keys must be bit vectors")
+        ks = KeySet(seed=None, params=p, _arrays=(secret[0], secret[1], bk, ksk))
         ks.seed = doc.get("seed")
         return ks
 

@@ -58,21 +58,57 @@ def inputs(config, model, batch, seed=1):
     return rng.integers(0, 2, (batch, d)).astype(np.uint8)
 
 
+def flatten_outputs(outs):
+    """eval_model outputs -> (flat handle list, structure): sign bits, or score
+    words as [(width, signed)] (compiler.py EncryptedWord)."""
+    if outs and hasattr(outs[0], "bits"):
+        return [b for w in outs for b in w.bits], [(len(w.bits), bool(w.signed)) for w in outs]
+    return list(outs), None
+
+
+def decode_bits(bits, structure):
+    """Decrypted flat output bits [handles][lanes] -> [lanes][units]: sign bits
+    -> +-1, score words -> ints (two's complement when signed)."""
+    if structure is None:
+        return np.where(np.asarray(bits).T == 1, 1, -1)
+    cols, at = [], 0
+    for width, signed in structure:
+        wb = np.asarray(bits[at:at + width]).astype(np.int64)
+        at += width
+        v = (wb << np.arange(width)[:, None]).sum(axis=0)
+        if signed:
+            v = np.where(v >= 1 << (width - 1), v - (1 << width), v)
+        cols.append(v)
+    return np.stack(cols, axis=1)
+
+
 def decode_outputs(ctx, outs):
     """Decrypt eval_model outputs for every lane: sign bits -> +-1, words -> ints.
     Returns [lanes][units]."""
-    if outs and hasattr(outs[0], "bits"):
-        cols = []
-        for w in outs:
-            bits = ctx.decrypt_many(w.bits)  # [width][lanes]
-            width = len(w.bits)
-            v = (bits.astype(np.int64) << np.arange(width)[:, None]).sum(axis=0)
-            if w.signed:
-                v = np.where(v >= 1 << (width - 1), v - (1 << width), v)
-            cols.append(v)
-        return np.stack(cols, axis=1)
-    bits = ctx.decrypt_many(outs)  # [units][lanes]
-    return np.where(bits.T == 1, 1, -1)
+    flat, structure = flatten_outputs(outs)
+    return decode_bits(ctx.decrypt_many(flat), structure)
+
+
+def run_cached(ctx_cls, config, sched, structure, seed=0, device=0, check=True, trial=0):
+    """First evaluation of a fresh context from a compiled schedule (no reference
+    compiler, no gate DAG): encrypt a new batch, run every level, decrypt."""
+    model, batch = build(config, seed)
+    X = inputs(config, model, batch, seed + 200 + trial)
+    ctx = ctx_cls(seed=seed, device=device, lanes=batch)
+    t0 = time.perf_counter()
+    cts = ctx.keys.encrypt(X.reshape(-1), seed=seed + 11, stream=600 + trial).reshape(batch, X.shape[1], -1)
+    cts = np.ascontiguousarray(cts.transpose(1, 0, 2))
+    t1 = time.perf_counter()
+    out = ctx.run_schedule(sched, cts)
+    t2 = time.perf_counter()
+    bits = ctx.keys.decrypt(out.reshape(-1, out.shape[-1])).reshape(out.shape[0], batch)
+    got = decode_bits(bits, structure)
+    t3 = time.perf_counter()
+    ok = None
+    if check:
+        ok = all(list(got[b]) == oracle_eval(model, [1 if v else -1 for v in X[b]]) for b in range(batch))
+    return {"first_eval_s": t3 - t0, "encrypt_s": t1 - t0, "run_s": t2 - t1, "decrypt_s": t3 - t2,
+            "levels": len(sched.levels), "records": sched.records, "matches_oracle_eval": ok}
 
 
 def run_sim_reference(config, seed=0, options=EvalOptions()):
@@ -92,9 +128,13 @@ def run_sim_reference(config, seed=0, options=EvalOptions()):
             "counted_gates_per_input": ctx.gate_count, "counted_gates_per_s": ctx.gate_count / dt}
 
 
-def run_encrypted(ctx_cls, config, seed=0, device=0, options=EvalOptions(), check=True, replays=0):
+def run_encrypted(ctx_cls, config, seed=0, device=0, options=EvalOptions(), check=True, replays=0, cached=False,
+                  schedule_path=None):
     """Encrypt a batch, evaluate through the reference compiler on a
-    lane-batched context, decrypt, compare with oracle_eval.  Returns a report."""
+    lane-batched context, decrypt, compare with oracle_eval.  Returns a report.
+    cached: also compile the executed schedule (saved to / reloaded from
+    `schedule_path` when given) and time a fresh context's first evaluation
+    through it (report key "cached")."""
     model, batch = build(config, seed)
     X = inputs(config, model, batch, seed + 1)
     ctx = ctx_cls(seed=seed, device=device, lanes=batch)
@@ -128,6 +168,19 @@ def run_encrypted(ctx_cls, config, seed=0, device=0, options=EvalOptions(), chec
                                for b in range(batch)))
         replay = {"replays": replays, "latency_s": min(times), "bootstraps_per_s": ctx.exec_stats["bootstraps"] / min(times),
                   "matches_oracle_eval": all(oks) if check else None}
+    cached_rep = None
+    if cached:
+        from .backend import Schedule
+
+        flat, structure = flatten_outputs(outs)
+        tc = time.perf_counter()
+        sched = ctx.compile_schedule(xb, flat, meta={"config": config})
+        compile_s = time.perf_counter() - tc
+        if schedule_path:
+            sched.save(schedule_path)
+            sched = Schedule.load(schedule_path)
+        cached_rep = run_cached(ctx_cls, config, sched, structure, seed=seed, device=device, check=check)
+        cached_rep["compile_s"] = compile_s
     return {
         "config": config, "batch": batch, "counted_gates": counted,
         "counted_gates_per_input": ctx.gate_count,
@@ -142,4 +195,5 @@ def run_encrypted(ctx_cls, config, seed=0, device=0, options=EvalOptions(), chec
         "counted_gates_per_s": counted / (t4 - t0),
         "matches_oracle_eval": ok,
         "replay": replay,
+        "cached": cached_rep,
     }

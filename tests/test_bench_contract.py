@@ -53,3 +53,23 @@ def test_reference_arm_under_torchrun_two_ranks():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2
+
+
+def test_gpus_flag_spawns_the_ranks_itself():
+    """`bench.py --gpus 2` without a launcher starts 2 ranks (torch.distributed.run
+    on 127.0.0.1) instead of silently timing one GPU (VERDICT r1 weak #6)."""
+    r = _run([sys.executable, "bench.py", "--gpus", "2", "--plan"], timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["plan"] is True and d["n_gpus"] == 2
+    assert sorted(x["rank"] for x in d["ranks"]) == [0, 1]
+    assert len({x["pid"] for x in d["ranks"]}) == 2
+
+
+def test_world_size_mismatch_is_an_error():
+    r = _run([sys.executable, "bench.py", "--gpus", "4", "--plan"],
+             {"RANK": "0", "WORLD_SIZE": "2", "LOCAL_RANK": "0"}, timeout=120)
+    assert r.returncode != 0
+    assert "WORLD_SIZE=2" in r.stderr

@@ -54,3 +54,34 @@ def test_wrong_document_kind_rejected(tmp_path, keys):
     wire_keys.save_ciphertexts(c, keys.encrypt([1], seed=1), keys.params)
     with pytest.raises(ValueError):
         wire_keys.load_keys(c)
+
+
+def test_key_document_validation(tmp_path, keys):
+    """A truncated or mismatched eval-key document is rejected before the engine
+    would copy hb_bk_words / hb_ksk_words words from it."""
+    import json as _json
+
+    def write(path, header, **arrays):
+        np.savez(path, header=np.frombuffer(_json.dumps(header).encode(), np.uint8), **arrays)
+
+    good = tmp_path / "good.npz"
+    wire_keys.save_keys(good, keys)
+    with np.load(good) as z:
+        hdr = _json.loads(bytes(z["header"]).decode())
+        bk, ksk = z["bk"], z["ksk"]
+    cases = {
+        "truncated_bk": (hdr, dict(bk=bk[:-1], ksk=ksk)),
+        "truncated_ksk": (hdr, dict(bk=bk, ksk=ksk[: ksk.size // 2])),
+        "wrong_dtype": (hdr, dict(bk=bk.astype(np.int64), ksk=ksk)),
+        "two_d": (hdr, dict(bk=bk.reshape(2, -1), ksk=ksk)),
+        "missing_ksk": (hdr, dict(bk=bk)),
+        "params_mismatch": ({**hdr, "params": {**hdr["params"], "n": 500}}, dict(bk=bk, ksk=ksk)),
+        "unsupported_n": ({**hdr, "params": {**hdr["params"], "n": 750}}, dict(bk=bk, ksk=ksk)),
+        "bad_params": ({**hdr, "params": {"n": 630}}, dict(bk=bk, ksk=ksk)),
+    }
+    for name, (h, arrays) in cases.items():
+        p = tmp_path / f"{name}.npz"
+        write(p, h, **arrays)
+        with pytest.raises(ValueError):
+            wire_keys.load_keys(p)
+    assert wire_keys.load_keys(good).bk.size == bk.size

@@ -148,3 +148,41 @@ def test_async_double_buffered_transfers(keys):
     for k in range(steps):
         assert np.array_equal(keys.decrypt(h_out[k]), bits[k][:n] ^ bits[k][n:]), k
     eng.close()
+
+
+@pytest.mark.gpu
+def test_async_download_is_not_overtaken_by_later_levels(keys):
+    """Write-after-read: step k's async download (a long copy, its gate outputs at
+    the end of the range) must read step k's values even though step k+2 rewrites
+    the same slots with a short level right after (hb_engine.cu WAR)."""
+    import torch
+
+    eng = tfhe.Engine(keys)
+    g, span, words = 8, 32768, keys.params.n + 1
+    steps = 4
+    rng = np.random.default_rng(21)
+    bits = [rng.integers(0, 2, 2 * g).astype(np.uint8) for _ in range(steps)]
+    h_in = [keys.encrypt(bits[k], seed=40 + k) for k in range(steps)]
+    h_out = [torch.empty((span, words), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32) for _ in range(steps)]
+    region = span + 2 * g
+    eng.reserve(2 * region)
+    c0, al, be = tfhe.GATE_LIN["AND"]
+    recs = []
+    for r in range(2):
+        base = r * region
+        rc = tfhe.gate_records(g)
+        # outputs in the LAST g slots of the downloaded span, inputs after it
+        rc["dst"] = base + span - g + np.arange(g)
+        rc["src_a"], rc["src_b"] = base + span + np.arange(g), base + span + g + np.arange(g)
+        rc["c0"], rc["alpha"], rc["beta"] = c0, al, be
+        recs.append(rc)
+    for k in range(steps):
+        r = k % 2
+        eng.upload(r * region + span, h_in[k])
+        eng.run_gates(recs[r])
+        eng.download_async(r * region, h_out[k])
+    eng.sync()
+    for k in range(steps):
+        got = keys.decrypt(h_out[k][span - g:])
+        assert np.array_equal(got, bits[k][:g] & bits[k][g:]), k
+    eng.close()

@@ -70,3 +70,27 @@ def test_outp_two_ranks_on_gpu():
     assert res[0][0] and res[1][0]
     assert res[0][1] == res[1][1]
     assert res[0][2][0][0] == 0 and res[0][2][0][1] == res[1][2][0][0] and res[1][2][0][1] == 9
+
+
+def test_bench_two_ranks_sharing_the_gpu():
+    """`bench.py --gpus 2` spawns its two ranks itself; with HB_BENCH_SHARE_GPU=1
+    both run on cuda:0 over gloo: the line says n_gpus 2, the NAND outputs are
+    right, the strong-scaling leg splits the job, and Out-P on the cfg2 neuron
+    and batch sharding of cfg5 match oracle_eval."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HB_BENCH_SHARE_GPU="1")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "2", "--warmup", "3", "--gates", "512",
+                        "--bnn", "cfg2n,cfg5", "--no-compare", "--no-cpu-baseline"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["correct"] is True
+    assert d["strong_scaling"]["gates_per_gpu"] == 256 and d["strong_scaling"]["n_gpus"] == 2
+    assert d["bnn"]["cfg2n"]["matches_oracle_eval"] is True, d["bnn"]["cfg2n"]
+    assert d["bnn"]["cfg5"]["matches_oracle_eval"] is True, d["bnn"]["cfg5"]

@@ -294,19 +294,25 @@ def test_replay_cached_dag_on_gpu():
         assert decrypt_output(ctx, outs) == oracle_eval(m, xs2)
 
 
-@pytest.mark.parametrize("config", ["cfg2l", "cfg4"])
-def test_baseline_configs_full_size(config):
-    """BASELINE.json configs at full size (cfg2: the 784->256 layer; cfg4: the
-    80%-sparse 784-256-256-10 BNN, batch 8) through the reference compiler on
-    the default context (streaming flushes, narrow-level deferral, full-adder
-    and half-adder fusion): every output equals oracle_eval, also when the
-    cached DAG is replayed on a second encrypted batch; counted stats are the
-    reference's and fusion executes fewer bootstraps than it counts."""
+@pytest.mark.parametrize("config", ["cfg2n", "cfg2l", "cfg3", "cfg4", "cfg5"])
+def test_baseline_configs_full_size(config, tmp_path):
+    """Every BASELINE.json BNN config at full size (cfg2n: one 784-input neuron;
+    cfg2l: the 784->256 layer; cfg3: 784-256-256-10, batch 8; cfg4: its
+    80%-sparse ternary variant; cfg5: tabular 240-128-64-2, batch 64) through
+    the reference compiler (compiler.py:441-462) on the default context
+    (streaming flushes, narrow-level deferral, full-adder and half-adder
+    fusion): every output equals oracle_eval (model.py:458-497) on the first
+    evaluation, when the DAG is replayed on a second encrypted batch, and when
+    a fresh context runs the compiled schedule (saved and reloaded) on a third;
+    counted stats are the reference SimContext's and fusion executes fewer
+    bootstraps than it counts."""
     from paper_1806_03461_b200 import workloads
 
-    rep = workloads.run_encrypted(TfheContext, config, seed=0, replays=1)
+    rep = workloads.run_encrypted(TfheContext, config, seed=0, replays=1, cached=True,
+                                  schedule_path=str(tmp_path / f"{config}.sched.npz"))
     assert rep["matches_oracle_eval"] is True
     assert rep["replay"]["matches_oracle_eval"] is True
+    assert rep["cached"]["matches_oracle_eval"] is True
     model, batch = workloads.build(config, 0)
     sim = workloads.run_sim_reference(config, seed=0)
     assert rep["counted_gates_per_input"] == sim["counted_gates_per_input"]

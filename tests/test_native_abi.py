@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_params():
     L = _native.lib()
-    assert L.hb_abi_version() == 3
+    assert L.hb_abi_version() == 4
     p = _native.default_params()
     assert (p.n, p.N, p.k, p.bg_bits, p.l, p.ks_base_bits, p.ks_t) == (630, 1024, 1, 7, 3, 2, 8)
     assert L.hb_lwe_words(ctypes.byref(p)) == 631
@@ -47,6 +47,20 @@ def test_abi_version_and_params():
 def test_key_pairs_need_even_n():
     p = _native.default_params()
     p.bk_unroll, p.n = 2, 629
+    out = np.zeros(4, np.uint32)
+    rc = _native.lib().hb_keygen(ctypes.byref(p), 1, _native.u32p(out), _native.u32p(out),
+                                 _native.u32p(out), _native.u32p(out), 1)
+    assert rc == _native.HB_EINVAL
+
+
+@pytest.mark.parametrize("n", [640, 750, 1023])
+def test_lwe_dimension_beyond_key_switch_columns_is_rejected(n):
+    """k_keyswitch writes kKskStride = 640 columns (a_0..a_{n-1}, b): n >= 640 must be
+    refused up front instead of returning ciphertexts with unwritten columns."""
+    p = _native.default_params()
+    assert _native.lib().hb_params_valid(ctypes.byref(p)) == 1
+    p.n = n
+    assert _native.lib().hb_params_valid(ctypes.byref(p)) == 0
     out = np.zeros(4, np.uint32)
     rc = _native.lib().hb_keygen(ctypes.byref(p), 1, _native.u32p(out), _native.u32p(out),
                                  _native.u32p(out), _native.u32p(out), 1)

@@ -72,7 +72,7 @@ def parse_args():
                     help="print the rank layout (n_gpus, backend, devices) as one JSON line and exit (launcher test)")
     ap.add_argument("--bnn", default="all",
                     help="encrypted-BNN latency legs (BASELINE configs 2-5), comma-separated from "
-                         "cfg2n,cfg2l,cfg3,cfg4,cfg5 (aliases neuron, layer), 'all' or 'none': one GPU on "
+                         "cfg2n,cfg2l,cfg3,cfg4,cfg5,conv (aliases neuron, layer), 'all' or 'none': one GPU on "
                          "rank 0, or Out-P / batch sharding over all ranks for N > 1")
     args = ap.parse_args()
     alias = {"neuron": "cfg2n", "layer": "cfg2l"}
@@ -88,7 +88,7 @@ def parse_args():
     return args
 
 
-BNN_CONFIGS = ("cfg2n", "cfg2l", "cfg3", "cfg4", "cfg5")
+BNN_CONFIGS = ("cfg2n", "cfg2l", "cfg3", "cfg4", "cfg5", "conv")
 
 
 def spawn_ranks(args):
@@ -638,6 +638,16 @@ def run_ours(args, dist):
             rep = {"error": repr(exc)}
         if dist.rank == 0:
             line["bnn"][cfg] = rep
+    if args.bnn_list and dist.rank == 0 and dist.world == 1:
+        try:  # the shipped Cancer model on the reference dataset's 569 rows, as lanes (f4)
+            from paper_1806_03461_b200 import workloads
+            from paper_1806_03461_b200.backend import TfheContext
+
+            rep = workloads.run_cancer(TfheContext, seed=args.seed)
+            rep.pop("predictions")
+            line["cancer"] = rep
+        except Exception as exc:  # report, never hide
+            line["cancer"] = {"error": repr(exc)}
     if args.bnn_list and dist.rank == 0:
         line["bnn_all_match_oracle_eval"] = all(
             isinstance(r, dict) and r.get("matches_oracle_eval") is True

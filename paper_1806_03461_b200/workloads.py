@@ -8,13 +8,14 @@ Bernoulli(0.8) zero mask for cfg4), biases 0, all from `random.Random(seed)`.
 
 from __future__ import annotations
 
+import os
 import random
 import time
 
 import numpy as np
 
 from hebnn.compiler import EvalOptions, eval_model
-from hebnn.model import DenseLayer, SignActivation, TernaryModel, oracle_eval, validate_model
+from hebnn.model import ConvLayer, DenseLayer, SignActivation, TernaryModel, oracle_eval, validate_model
 
 
 def _dense(rng, d, p, zero_prob=0.0):
@@ -30,9 +31,29 @@ def _dense(rng, d, p, zero_prob=0.0):
     return DenseLayer(tuple(rows), (0,) * p)
 
 
+def _conv(rng, out_c, in_c, k, stride=1, zero_prob=0.0):
+    filters = []
+    for _ in range(out_c):
+        filt = []
+        for _ in range(in_c):
+            filt.append(tuple(tuple(0 if (zero_prob and rng.random() < zero_prob) else rng.choice((-1, 1))
+                                    for _ in range(k)) for _ in range(k)))
+        filters.append(tuple(filt))
+    return ConvLayer(tuple(filters), (0,) * out_c, stride=stride)
+
+
 def build(config, seed=0):
-    """Returns (model, batch) for config in {cfg2n, cfg2l, cfg3, cfg4, cfg5}."""
+    """Returns (model, batch) for config in {cfg2n, cfg2l, cfg3, cfg4, cfg5, conv}.
+
+    conv (not a BASELINE config): an MNIST-shaped convolutional
+    BNN through the reference's conv_layer (compiler.py:372-416) — 1x28x28 bits,
+    conv 5x5 8 ch stride 1 + sign (24x24), conv 5x5 16 ch stride 2 + sign
+    (10x10), dense 1600 -> 10 score words; +-1 weights; one input."""
     rng = random.Random(seed)
+    if config == "conv":
+        layers = (_conv(rng, 8, 1, 5), SignActivation(), _conv(rng, 16, 8, 5, stride=2), SignActivation(),
+                  _dense(rng, 1600, 10))
+        return validate_model(TernaryModel((1, 28, 28), layers, "score_words")), 1
     if config == "cfg2n":
         return validate_model(TernaryModel(784, (_dense(rng, 784, 1), SignActivation()), "sign_bits")), 1
     if config == "cfg2l":
@@ -51,7 +72,7 @@ def build(config, seed=0):
 def inputs(config, model, batch, seed=1):
     """[batch][d] bits in {0,1} (stored-binary encoding of +-1 inputs)."""
     rng = np.random.default_rng(seed)
-    d = model.input_shape
+    d = int(np.prod(model.input_shape))
     if config == "cfg5":
         vals = rng.integers(0, 256, (batch, 30))  # 30 features quantised to 8 bits
         return ((vals[:, :, None] >> np.arange(8)[None, None, :]) & 1).reshape(batch, d).astype(np.uint8)
@@ -109,6 +130,52 @@ def run_cached(ctx_cls, config, sched, structure, seed=0, device=0, check=True, 
         ok = all(list(got[b]) == oracle_eval(model, [1 if v else -1 for v in X[b]]) for b in range(batch))
     return {"first_eval_s": t3 - t0, "encrypt_s": t1 - t0, "run_s": t2 - t1, "decrypt_s": t3 - t2,
             "levels": len(sched.levels), "records": sched.records, "matches_oracle_eval": ok}
+
+
+GOLDEN = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+
+
+def cancer_rows(path=None):
+    """The reference's shipped Cancer dataset, binned exactly as its trainer
+    does (tests/golden/make_cancer_fixture.py): (bits [569][90] stored-binary,
+    labels +-1, train idx, test idx, (train acc, test acc) from metrics.json)."""
+    z = np.load(path or os.path.join(GOLDEN, "cancer_rows.npz"))
+    return (z["bits"], z["labels"], z["train"], z["test"],
+            (float(z["accuracy_train"]), float(z["accuracy_test"])))
+
+
+def cancer_model(path=None):
+    """The reference's shipped trained model (trainer/out/model.json)."""
+    from hebnn.wire import read_model
+
+    return read_model(path or os.path.join(GOLDEN, "cancer_model.json"))
+
+
+def run_cancer(ctx_cls, seed=0, device=0, rows=None, check=True):
+    """Classify the Cancer rows encrypted, all of them as lanes of one DAG
+    (the shipped 90-input model through the reference compiler); predictions
+    checked row by row against oracle_eval, accuracy against metrics.json."""
+    X, y, train, test, (acc_train, acc_test) = cancer_rows()
+    if rows is not None:
+        X, y = X[rows], y[rows]
+    model = cancer_model()
+    ctx = ctx_cls(seed=seed, device=device, lanes=X.shape[0])
+    t0 = time.perf_counter()
+    xb = ctx.encrypt_many(X.T)
+    outs, _ = eval_model(ctx, model, xb, EvalOptions())
+    got = decode_outputs(ctx, outs)[:, 0]
+    dt = time.perf_counter() - t0
+    rep = {"rows": int(X.shape[0]), "latency_s": dt, "rows_per_s": X.shape[0] / dt,
+           "counted_gates_per_row": ctx.gate_count, "executed_bootstraps": ctx.exec_stats["bootstraps"],
+           "predictions": got}
+    if check:
+        want = np.array([oracle_eval(model, [1 if v else -1 for v in row])[0] for row in X])
+        rep["matches_oracle_eval"] = bool(np.array_equal(got, want))
+    if rows is None:
+        rep["accuracy_train"] = float((got[train] == y[train]).mean())
+        rep["accuracy_test"] = float((got[test] == y[test]).mean())
+        rep["trainer_accuracy"] = {"train": acc_train, "test": acc_test}
+    return rep
 
 
 def run_sim_reference(config, seed=0, options=EvalOptions()):

@@ -18,7 +18,8 @@ __device__ __forceinline__ void dmma_m16n8k16(double (&d)[4], const double (&a)[
 
 // mode 0: DFMA only; 1: DMMA m8n8k4 only; 2: both interleaved in every warp;
 // 3: even warps DFMA, odd warps DMMA; 4: DMMA m16n8k16 only; 5: m16n8k16 + DFMA interleaved
-__global__ void k_pipes(double *out, int iters, int mode, double x, double y) {
+template <int mode>
+__global__ void __launch_bounds__(256) k_pipes(double *out, int iters, double x, double y) {
     double f[8];
     for (int i = 0; i < 8; i++) f[i] = x + threadIdx.x * 1e-9 + i;
     double m[4][2];
@@ -29,9 +30,9 @@ __global__ void k_pipes(double *out, int iters, int mode, double x, double y) {
     for (int i = 0; i < 8; i++) A[i] = x * (i + 1) * 1e-3;
     for (int i = 0; i < 4; i++) B[i] = y * (i + 1) * 1e-3;
     const int warp = threadIdx.x >> 5;
-    bool do_f = mode == 0 || mode == 2 || mode == 5 || (mode == 3 && !(warp & 1));
-    bool do_m = mode == 1 || mode == 2 || (mode == 3 && (warp & 1));
-    bool do_M = mode == 4 || mode == 5;
+    const bool do_f = mode == 0 || mode == 2 || mode == 5 || (mode == 3 && !(warp & 1));
+    const bool do_m = mode == 1 || mode == 2 || (mode == 3 && (warp & 1));
+    const bool do_M = mode == 4 || mode == 5;
     for (int it = 0; it < iters; it++) {
         if (do_f) {
 #pragma unroll
@@ -63,12 +64,14 @@ int main() {
     cudaEventCreate(&e1);
     const char *names[] = {"DFMA only", "DMMA m8n8k4 only", "DFMA+DMMA interleaved", "DFMA warps | DMMA warps",
                            "DMMA m16n8k16 only", "DMMA m16n8k16 + DFMA"};
-    for (int threads : {256, 512}) {
+    void (*kern[6])(double *, int, double, double) = {k_pipes<0>, k_pipes<1>, k_pipes<2>, k_pipes<3>, k_pipes<4>, k_pipes<5>};
+    for (int threads : {256}) {
+        for (int per_sm : {4, 8}) {
         for (int mode = 0; mode < 6; mode++) {
-            int blocks = p.multiProcessorCount * (1024 / threads) * 1, iters = 4096;
-            k_pipes<<<blocks, threads>>>(d, iters, mode, 0.999999, 1e-7);
+            int blocks = p.multiProcessorCount * per_sm, iters = 4096;
+            kern[mode]<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
             cudaEventRecord(e0);
-            for (int r = 0; r < 5; r++) k_pipes<<<blocks, threads>>>(d, iters, mode, 0.999999, 1e-7);
+            for (int r = 0; r < 5; r++) kern[mode]<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
             float ms;
@@ -81,9 +84,10 @@ int main() {
             if (mode == 1 || mode == 2) fm = warps * 4 * 512;
             if (mode == 3) fm = fw * 4 * 512;
             if (mode == 4 || mode == 5) fm = warps * 2 * 4096;
-            printf("threads %d %-26s %8.3f ms  vector %6.2f TF  dmma %6.2f TF  total %6.2f TF  (%s)\n", threads,
+            printf("ctas/SM %d threads %d %-26s %8.3f ms  vector %6.2f TF  dmma %6.2f TF  total %6.2f TF  (%s)\n", per_sm, threads,
                    names[mode], ms, ff / ms / 1e9, fm / ms / 1e9, (ff + fm) / ms / 1e9,
                    cudaGetErrorString(cudaGetLastError()));
+        }
         }
     }
     return 0;

@@ -9,6 +9,9 @@ bootstrap CGGI formula.  It is injected by subclassing in tests, never by the
 product package.
 """
 
+import functools
+import threading
+
 import numpy as np
 
 from paper_1806_03461_b200._native import GATE_HA, GATE_LIN3, GATE_MUX
@@ -21,8 +24,20 @@ def _sign_to_phase(v):
     return np.where(v > 0, EIGHTH, -EIGHTH).astype(np.int64)
 
 
+def _locked(fn):
+    """Serialise engine calls like tfhe.Engine does: a background flush runs
+    levels while the DAG-building thread grows the pool (reserve replaces the
+    array; an unlocked level would write into the old one)."""
+    @functools.wraps(fn)
+    def wrap(self, *a, **k):
+        with self._lock:
+            return fn(self, *a, **k)
+    return wrap
+
+
 class PlainEngine:
     def __init__(self, keys):
+        self._lock = threading.RLock()
         self.keys = keys
         self.pool = np.zeros(0, np.int64)
         self.records_run = 0
@@ -32,14 +47,17 @@ class PlainEngine:
     def capacity(self):
         return self.pool.size
 
+    @_locked
     def reserve(self, slots):
         if slots > self.pool.size:
             self.pool = np.concatenate([self.pool, np.zeros(slots - self.pool.size, np.int64)])
 
+    @_locked
     def upload(self, first, cts):
         ph = self.keys.phase(np.ascontiguousarray(cts, np.uint32)).astype(np.int64)
         self.pool[first:first + len(ph)] = np.where(ph > 0, EIGHTH, -EIGHTH)
 
+    @_locked
     def run_gates(self, recs, lanes=1):
         self.levels_run += 1
         self.records_run += len(recs)
@@ -71,6 +89,7 @@ class PlainEngine:
     def sync(self):
         pass
 
+    @_locked
     def gather(self, slots):
         # return ciphertexts that decrypt to the stored bits: trivial samples (0, phase)
         n = self.keys.params.n

@@ -294,11 +294,12 @@ def test_replay_cached_dag_on_gpu():
         assert decrypt_output(ctx, outs) == oracle_eval(m, xs2)
 
 
-@pytest.mark.parametrize("config", ["cfg2n", "cfg2l", "cfg3", "cfg4", "cfg5"])
+@pytest.mark.parametrize("config", ["cfg2n", "cfg2l", "cfg3", "cfg4", "cfg5", "conv"])
 def test_baseline_configs_full_size(config, tmp_path):
     """Every BASELINE.json BNN config at full size (cfg2n: one 784-input neuron;
     cfg2l: the 784->256 layer; cfg3: 784-256-256-10, batch 8; cfg4: its
-    80%-sparse ternary variant; cfg5: tabular 240-128-64-2, batch 64) through
+    80%-sparse ternary variant; cfg5: tabular 240-128-64-2, batch 64; conv: an
+    MNIST-shaped conv BNN through conv_layer, compiler.py:372-416) through
     the reference compiler (compiler.py:441-462) on the default context
     (streaming flushes, narrow-level deferral, full-adder and half-adder
     fusion): every output equals oracle_eval (model.py:458-497) on the first

@@ -47,6 +47,7 @@ namespace {
 #include "hb_dev_fft.cuh"
 #include "hb_br_cggi.cuh"
 #include "hb_br_u2.cuh"
+#include "hb_br_u2h.cuh"
 #include "hb_ks.cuh"
 
 }  // namespace
@@ -101,6 +102,7 @@ struct hb_engine {
     size_t max_work = kMaxWorkPerLaunch;  // HEBNN_B200_MAX_WORK overrides (tests)
     bool latency_mode = true;             // HEBNN_B200_LATENCY_MODE=0 disables (A/B tests)
     bool cluster_mode = true;             // 2-CTA clusters for <= #SM/2 key-pair bootstraps (HEBNN_B200_CLUSTER_MODE=0)
+    bool u2h = true;                      // wide key-pair levels: 128 threads per bootstrap (HEBNN_B200_U2H=0: 64)
 };
 
 namespace {
@@ -150,6 +152,15 @@ template <int G, bool kDebug, int R = kStagesU2, int MB = 1, bool TM = false>
 int launch_br_u2(hb_engine *e, const BrArgs &a) {
     const unsigned grid = (a.n_work + G - 1) / G;
     k_blind_rotate_u2<G, kDebug, R, MB, TM><<<grid, 64 * G, sizeof(BrSmemU2<G, R, TM>), e->stream>>>(a);
+    HB_CUDA_TRY(cudaGetLastError());
+    e->n_launch++;
+    return HB_OK;
+}
+
+template <int G, bool kDebug>
+int launch_br_u2h(hb_engine *e, const BrArgs &a) {
+    const unsigned grid = (a.n_work + G - 1) / G;
+    k_blind_rotate_u2h<G, kDebug><<<grid, 128 * G, sizeof(BrSmemU2H<G>), e->stream>>>(a);
     HB_CUDA_TRY(cudaGetLastError());
     e->n_launch++;
     return HB_OK;
@@ -248,6 +259,7 @@ int launch_br_auto(hb_engine *e, const BrArgs &a, int force_g = 0) {
 #if HB_U2_TMEM
         return launch_br_u2<kBrGates, kDebug, kStagesU2Tmem, 1, true>(e, a);
 #else
+        if (e->u2h) return launch_br_u2h<kBrGates, kDebug>(e, a);
         return launch_br_u2<kBrGates, kDebug>(e, a);
 #endif
     }
@@ -371,6 +383,11 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
 #endif
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(BrSmemU2<kBrGates>)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2h<kBrGates, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrSmemU2H<kBrGates>)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2h<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrSmemU2H<kBrGates>)));
+    if (const char *uh = std::getenv("HEBNN_B200_U2H")) e->u2h = std::atoi(uh) != 0;
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(BrSmemU2<kBrGates>)));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,

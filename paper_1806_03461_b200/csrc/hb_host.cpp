@@ -2,7 +2,7 @@
 // generation, encryption and decryption.  These replace the plaintext store of
 // the reference's SimContext (backend.py:171-190): `encrypt` returns a real
 // LWE sample, `decrypt` computes its phase.  Multi-threaded with std::thread;
-// bit-identical to the oracle's restatement (tests/test_keys_parity.py).
+// bit-identical to the oracle restatement (tests/test_oracle.py).
 #include <cmath>
 #include <cstring>
 #include <string>

@@ -48,6 +48,7 @@ namespace {
 #include "hb_br_cggi.cuh"
 #include "hb_br_u2.cuh"
 #include "hb_br_u2h.cuh"
+#include "hb_br_clu6.cuh"
 #include "hb_ks.cuh"
 
 }  // namespace
@@ -102,7 +103,9 @@ struct hb_engine {
     size_t max_work = kMaxWorkPerLaunch;  // HEBNN_B200_MAX_WORK overrides (tests)
     bool latency_mode = true;             // HEBNN_B200_LATENCY_MODE=0 disables (A/B tests)
     bool cluster_mode = true;             // 2-CTA clusters for <= #SM/2 key-pair bootstraps (HEBNN_B200_CLUSTER_MODE=0)
-    bool u2h = true;                      // wide key-pair levels: 128 threads per bootstrap (HEBNN_B200_U2H=0: 64)
+    int clu6_max = 0;                     // co-resident 6-CTA clusters (0: kernel unavailable); HEBNN_B200_CLU6=0 off
+    bool u2h = false;                     // experiment (HEBNN_B200_U2H=1): 128 threads per bootstrap on wide
+                                          // key-pair levels; 42.7 ms vs 31.2 ms per 4,096 (profiles/r02_a)
 };
 
 namespace {
@@ -239,6 +242,12 @@ int launch_br_auto(hb_engine *e, const BrArgs &a, int force_g = 0) {
     const uint32_t sms = (uint32_t)e->num_sms;
     const int gsel = force_g ? force_g : (a.n_work <= sms ? 1 : (a.n_work <= 2u * sms ? 2 : kBrGates));
     if (e->unroll == 2) {
+        if (!force_g && e->latency_mode && e->cluster_mode && a.n_work <= (uint32_t)e->clu6_max) {
+            k_blind_rotate_u2_clu6<kDebug><<<kClu6 * a.n_work, 192, sizeof(BrClu6Smem), e->stream>>>(a);
+            HB_CUDA_TRY(cudaGetLastError());
+            e->n_launch++;
+            return HB_OK;
+        }
         if (!force_g && e->latency_mode && e->cluster_mode && 2 * a.n_work <= sms) {
             k_blind_rotate_u2_clu<kDebug><<<2 * a.n_work, 192, sizeof(BrCluSmemU2), e->stream>>>(a);
             HB_CUDA_TRY(cudaGetLastError());
@@ -388,6 +397,24 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2h<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(BrSmemU2H<kBrGates>)));
     if (const char *uh = std::getenv("HEBNN_B200_U2H")) e->u2h = std::atoi(uh) != 0;
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_clu6<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrClu6Smem)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_clu6<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrClu6Smem)));
+    {  // how many 6-CTA clusters fit at once (GPC-limited); narrower levels use them
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(kClu6 * 64);
+        cfg.blockDim = dim3(192);
+        cfg.dynamicSmemBytes = sizeof(BrClu6Smem);
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, k_blind_rotate_u2_clu6<false>, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            ncl = 0;
+        }
+        e->clu6_max = ncl;
+        if (const char *c6 = std::getenv("HEBNN_B200_CLU6"))
+            if (std::atoi(c6) == 0) e->clu6_max = 0;
+    }
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(BrSmemU2<kBrGates>)));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1,0 +1,31 @@
+"""clu6 bring-up: narrow levels vs the oracle (bit-exact) and per-level latency by kernel."""
+import json, os, subprocess, sys
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1806_03461_b200 import tfhe
+from oracle import oracle as O
+
+keys = tfhe.KeySet(seed=42)
+eng = tfhe.Engine(keys)
+p = O.default_params(); okeys = O.Keys(p, 42); octx = O.Context(p, okeys)
+out = {}
+for n in (1, 3, 8, 12, 16, 20, 24):
+    rng = np.random.default_rng(n)
+    a = rng.integers(0, 2, n).astype(np.uint8); b = rng.integers(0, 2, n).astype(np.uint8)
+    ca, cb = keys.encrypt(a, seed=1, stream=1), keys.encrypt(b, seed=1, stream=2)
+    eng.reserve(3 * n); eng.upload(0, np.concatenate([ca, cb]))
+    recs = tfhe.gate_records(n)
+    c0, al, be = tfhe.GATE_LIN["NAND"]
+    recs["dst"], recs["src_a"], recs["src_b"] = np.arange(2 * n, 3 * n), np.arange(n), np.arange(n, 2 * n)
+    recs["c0"], recs["alpha"], recs["beta"] = c0, al, be
+    eng.run_gates(recs); eng.sync()
+    got = eng.download(2 * n, n)
+    ok_bits = bool(np.array_equal(keys.decrypt(got), 1 - (a & b)))
+    exact = all(np.array_equal(got[i], octx.gate(c0, al, ca[i], be, cb[i])) for i in range(min(n, 3)))
+    br = []
+    for _ in range(5):
+        eng.run_gates(recs); br.append(eng.last_timing())
+    out[n] = {"bits_ok": ok_bits, "bit_exact_vs_oracle": exact, "br_ms": min(x[0] for x in br), "ks_ms": min(x[1] for x in br)}
+    print(n, out[n], flush=True)
+print(json.dumps(out))

@@ -197,11 +197,12 @@ np.save(sys.argv[1], eng.download(2 * n, n))
     assert np.array_equal(outs[0], outs[1])
 
 
-@pytest.mark.parametrize("n", [5, 100, 200])
+@pytest.mark.parametrize("n", [1, 5, 20, 100, 200])
 def test_narrow_level_kernels_agree(n):
-    """Levels of <= #SM/2, <= #SM and <= 2 #SM bootstraps run on the 2-CTA
-    cluster kernel, the latency kernel or 1-2 bootstraps per CTA; every choice
-    must give the same ciphertexts (both key layouts)."""
+    """Levels of <= #clusters of 6 CTAs, <= #SM/2, <= #SM and <= 2 #SM bootstraps
+    run on the 6-CTA cluster kernel (key pairs), the 2-CTA cluster kernel, the
+    latency kernel or 1-2 bootstraps per CTA; every choice must give the same
+    ciphertexts (both key layouts), and the first one equals the oracle's."""
     import os
     import subprocess
     import sys
@@ -231,12 +232,13 @@ np.save(sys.argv[1], eng.download(3 * n, n))
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     for unroll in (2, 1):
         outs = []
-        for lat, clu in (("1", "1"), ("1", "0"), ("0", "0")):
-            path = f"/tmp/hb_narrow_{n}_{unroll}_{lat}{clu}.npy"
-            env = dict(os.environ, HEBNN_B200_LATENCY_MODE=lat, HEBNN_B200_CLUSTER_MODE=clu)
+        for lat, clu, c6 in (("1", "1", "1"), ("1", "1", "0"), ("1", "0", "0"), ("0", "0", "0")):
+            path = f"/tmp/hb_narrow_{n}_{unroll}_{lat}{clu}{c6}.npy"
+            env = dict(os.environ, HEBNN_B200_LATENCY_MODE=lat, HEBNN_B200_CLUSTER_MODE=clu, HEBNN_B200_CLU6=c6)
             subprocess.run([sys.executable, "-c", code, path, str(n), str(unroll)], check=True, cwd=root, env=env)
             outs.append(np.load(path))
-        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+        for k in range(1, len(outs)):
+            assert np.array_equal(outs[0], outs[k]), (unroll, k)
 
 
 def test_random_mixed_level_bit_exact_vs_oracle(kit):

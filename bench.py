@@ -311,7 +311,7 @@ def run_reference(args, dist):
 # our arm
 # ---------------------------------------------------------------------------
 
-def bnn_latency(cfg, seed, trials=2):
+def bnn_latency(cfg, seed, trials=2, cached=True):
     """BASELINE configs 2-5 through the reference compiler on TfheContext
     (engine created and warmed before the timed flush)."""
     from paper_1806_03461_b200 import workloads
@@ -321,7 +321,7 @@ def bnn_latency(cfg, seed, trials=2):
     warm.decrypt(warm.g_and(warm.encrypt(1), warm.encrypt(1)))  # CUDA context, BK FFT, KSK upload
     # fresh contexts (each builds its DAG from scratch); a second one finds the engine's
     # pools already grown, as a serving process would
-    runs = [workloads.run_encrypted(TfheContext, cfg, seed=seed, replays=1, cached=(t == trials - 1))
+    runs = [workloads.run_encrypted(TfheContext, cfg, seed=seed, replays=1, cached=cached and t == trials - 1)
             for t in range(trials)]
     rep = min(runs, key=lambda r: r["first_eval_s"])
     rep["first_eval_trials_s"] = [r["first_eval_s"] for r in runs]
@@ -631,7 +631,10 @@ def run_ours(args, dist):
             if dist.world > 1:
                 rep = bnn_outp(cfg, args.seed, dist, dev)
             elif dist.rank == 0:
-                rep = bnn_latency(cfg, args.seed, trials=2 if cfg in ("cfg2n", "cfg2l") else 1)
+                # the two largest configs skip the cached leg (same device work as their replay;
+                # tests/test_gpu_reference_replay.py runs it) to keep the default run in minutes
+                rep = bnn_latency(cfg, args.seed, trials=2 if cfg in ("cfg2n", "cfg2l") else 1,
+                                  cached=cfg not in ("cfg3", "cfg5"))
             else:
                 rep = None
         except Exception as exc:  # report, never hide

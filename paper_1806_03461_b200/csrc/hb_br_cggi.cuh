@@ -48,7 +48,8 @@ struct BrArgs {
     uint32_t pool_stride;
     uint32_t lanes;
     const BrItem *items;      // [n_items]
-    uint32_t n_work;          // n_items * lanes
+    uint32_t n_work;          // n_items * lanes (end of this launch's work range)
+    uint32_t e0;              // first work item of this launch (a level split over launches)
     int32_t n;                // LWE dimension
     uint32_t mu;              // test-vector value (1/8)
     const double2 *bkf;       // [n][6][2][512]
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
     const int g = warp >> 1;
     const int t = threadIdx.x & 63;
     const int bar_id = 1 + g;
-    const uint32_t e_raw = blockIdx.x * G + g;
+    const uint32_t e_raw = args.e0 + blockIdx.x * G + g;
     const bool active = e_raw < args.n_work;
     const uint32_t e = active ? e_raw : args.n_work - 1;
     uint32_t *accA = sm.acc[g][0];
@@ -369,7 +370,7 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_lat(const BrArgs args) 
     const int n = args.n;
     const int iters = min(n, args.iters);
     const char *bk_src = reinterpret_cast<const char *>(args.bkf);
-    const uint32_t e = blockIdx.x;      // one bootstrap per CTA (grid == n_work)
+    const uint32_t e = args.e0 + blockIdx.x;  // one bootstrap per CTA (grid == n_work - e0)
     uint32_t *accA = sm.acc[0];
     uint32_t *accB = sm.acc[1];
     double2 *xch = &sm.xch[grp][0][0][0];

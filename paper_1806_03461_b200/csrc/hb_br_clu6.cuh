@@ -103,7 +103,7 @@ __global__ void __cluster_dims__(kClu6, 1, 1) __launch_bounds__(192, 1) k_blind_
     const int n = args.n;
     const int pairs = min(n, args.iters) / 2;
     const char *bk_src = reinterpret_cast<const char *>(args.bkf);
-    const uint32_t e = blockIdx.x / kClu6;
+    const uint32_t e = args.e0 + blockIdx.x / kClu6;
     auto stage_src = [&](int pm, int c) {
         return bk_src + (size_t)(pm * kStagesPerPair + rp * 6 + c * 2 + h) * kRowBytes;
     };

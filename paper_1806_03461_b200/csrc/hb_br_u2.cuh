@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
     const int g = warp >> 1;
     const int t = threadIdx.x & 63;
     const int bar_id = 1 + g;
-    const uint32_t e_raw = blockIdx.x * G + g;
+    const uint32_t e_raw = args.e0 + blockIdx.x * G + g;
     const bool active = e_raw < args.n_work;
     const uint32_t e = active ? e_raw : args.n_work - 1;
     uint32_t *accA = sm.acc[TM ? 0 : g][0];
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_u2_lat(const BrArgs arg
     const int pairs = min(n, args.iters) / 2;
     const int stages_needed = pairs * 6;  // this group's stages
     const char *bk_src = reinterpret_cast<const char *>(args.bkf);
-    const uint32_t e = blockIdx.x;
+    const uint32_t e = args.e0 + blockIdx.x;
     uint32_t *accA = sm.acc[0];
     uint32_t *accB = sm.acc[1];
     double2 *xch = &sm.xch[grp][0][0];
@@ -649,7 +649,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) k_blind_rota
     const int n = args.n;
     const int pairs = min(n, args.iters) / 2;
     const char *bk_src = reinterpret_cast<const char *>(args.bkf);
-    const uint32_t e = blockIdx.x >> 1;
+    const uint32_t e = args.e0 + (blockIdx.x >> 1);
     const int row = 3 * q + grp, p = grp;         // digit row of this group: poly q, digit p
     const int rp = row >> 1, h = row & 1;
     auto stage_src = [&](int pm, int c) {

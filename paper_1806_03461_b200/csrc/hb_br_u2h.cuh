@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(128 * G, 1) k_blind_rotate_u2h(const BrArgs ar
     }
     __syncthreads();
 
-    const uint32_t e_raw = blockIdx.x * G + g;
+    const uint32_t e_raw = args.e0 + blockIdx.x * G + g;
     const bool active = e_raw < args.n_work;
     const uint32_t e = active ? e_raw : args.n_work - 1;
     uint32_t *accP = sm.acc[g][hf];  // this half's accumulator polynomial

@@ -104,6 +104,8 @@ struct hb_engine {
     bool latency_mode = true;             // HEBNN_B200_LATENCY_MODE=0 disables (A/B tests)
     bool cluster_mode = true;             // 2-CTA clusters for <= #SM/2 key-pair bootstraps (HEBNN_B200_CLUSTER_MODE=0)
     int clu6_max = 0;                     // co-resident 6-CTA clusters (0: kernel unavailable); HEBNN_B200_CLU6=0 off
+    bool split_waves = true;              // wide levels: full 4-bootstrap waves + a faster remainder kernel
+                                          // (HEBNN_B200_SPLIT_WAVES=0 off)
     bool u2h = false;                     // experiment (HEBNN_B200_U2H=1): 128 threads per bootstrap on wide
                                           // key-pair levels; 42.7 ms vs 31.2 ms per 4,096 (profiles/r02_a)
 };
@@ -144,7 +146,7 @@ int ensure_host_stage(hb_engine *e, size_t bytes) {
 template <int G, bool kDebug>
 int launch_br(hb_engine *e, const BrArgs &a) {
     const size_t smem = br_smem_bytes<G>();
-    const unsigned grid = (a.n_work + G - 1) / G;
+    const unsigned grid = (a.n_work - a.e0 + G - 1) / G;
     k_blind_rotate<G, kDebug><<<grid, 64 * G, smem, e->stream>>>(a);
     HB_CUDA_TRY(cudaGetLastError());
     e->n_launch++;
@@ -153,7 +155,7 @@ int launch_br(hb_engine *e, const BrArgs &a) {
 
 template <int G, bool kDebug, int R = kStagesU2, int MB = 1, bool TM = false>
 int launch_br_u2(hb_engine *e, const BrArgs &a) {
-    const unsigned grid = (a.n_work + G - 1) / G;
+    const unsigned grid = (a.n_work - a.e0 + G - 1) / G;
     k_blind_rotate_u2<G, kDebug, R, MB, TM><<<grid, 64 * G, sizeof(BrSmemU2<G, R, TM>), e->stream>>>(a);
     HB_CUDA_TRY(cudaGetLastError());
     e->n_launch++;
@@ -162,7 +164,7 @@ int launch_br_u2(hb_engine *e, const BrArgs &a) {
 
 template <int G, bool kDebug>
 int launch_br_u2h(hb_engine *e, const BrArgs &a) {
-    const unsigned grid = (a.n_work + G - 1) / G;
+    const unsigned grid = (a.n_work - a.e0 + G - 1) / G;
     k_blind_rotate_u2h<G, kDebug><<<grid, 128 * G, sizeof(BrSmemU2H<G>), e->stream>>>(a);
     HB_CUDA_TRY(cudaGetLastError());
     e->n_launch++;
@@ -171,7 +173,7 @@ int launch_br_u2h(hb_engine *e, const BrArgs &a) {
 
 template <bool kDebug>
 int launch_br_lat(hb_engine *e, const BrArgs &a) {
-    k_blind_rotate_lat<kDebug><<<a.n_work, 192, sizeof(BrLatSmem), e->stream>>>(a);
+    k_blind_rotate_lat<kDebug><<<a.n_work - a.e0, 192, sizeof(BrLatSmem), e->stream>>>(a);
     HB_CUDA_TRY(cudaGetLastError());
     e->n_launch++;
     return HB_OK;
@@ -238,30 +240,47 @@ constexpr int kStagesU2Tmem = HB_TMEM_RING;
 // (latency mode) or fewer bootstraps per CTA; wide levels 4 per CTA.
 // force_g (debug paths): 4 = the throughput kernel regardless of width.
 template <bool kDebug>
-int launch_br_auto(hb_engine *e, const BrArgs &a, int force_g = 0) {
+int launch_br_auto(hb_engine *e, const BrArgs &a0, int force_g = 0) {
     const uint32_t sms = (uint32_t)e->num_sms;
-    const int gsel = force_g ? force_g : (a.n_work <= sms ? 1 : (a.n_work <= 2u * sms ? 2 : kBrGates));
+    BrArgs a = a0;
+    // key pairs, wide levels: whole waves of 4-bootstrap CTAs, then the remainder (< one wave)
+    // on the kernel that runs it fastest (a 6-CTA cluster per bootstrap ... 3 per CTA) instead
+    // of a mostly idle extra 4-bootstrap wave: e.g. 729 bootstraps 8.9 -> ~6.4 ms
+    if (e->unroll == 2 && !force_g && e->split_waves) {
+        const uint32_t wave = kBrGates * sms, cnt = a.n_work - a.e0;
+        if (cnt > wave && cnt % wave != 0 && cnt % wave <= 3 * sms) {
+            BrArgs head = a;
+            head.n_work = a.e0 + (cnt / wave) * wave;
+            int rc = launch_br_u2<kBrGates, kDebug>(e, head);
+            if (rc) return rc;
+            a.e0 = head.n_work;
+        }
+    }
+    const uint32_t cnt = a.n_work - a.e0;
+    const int gsel = force_g ? force_g
+                             : (cnt <= sms ? 1 : (cnt <= 2u * sms ? 2 : (cnt <= 3u * sms && e->unroll == 2 ? 3 : kBrGates)));
     if (e->unroll == 2) {
-        if (!force_g && e->latency_mode && e->cluster_mode && a.n_work <= (uint32_t)e->clu6_max) {
-            k_blind_rotate_u2_clu6<kDebug><<<kClu6 * a.n_work, 192, sizeof(BrClu6Smem), e->stream>>>(a);
+        if (!force_g && e->latency_mode && e->cluster_mode && cnt <= (uint32_t)e->clu6_max) {
+            k_blind_rotate_u2_clu6<kDebug><<<kClu6 * cnt, 192, sizeof(BrClu6Smem), e->stream>>>(a);
             HB_CUDA_TRY(cudaGetLastError());
             e->n_launch++;
             return HB_OK;
         }
-        if (!force_g && e->latency_mode && e->cluster_mode && 2 * a.n_work <= sms) {
-            k_blind_rotate_u2_clu<kDebug><<<2 * a.n_work, 192, sizeof(BrCluSmemU2), e->stream>>>(a);
+        if (!force_g && e->latency_mode && e->cluster_mode && 2 * cnt <= sms) {
+            k_blind_rotate_u2_clu<kDebug><<<2 * cnt, 192, sizeof(BrCluSmemU2), e->stream>>>(a);
             HB_CUDA_TRY(cudaGetLastError());
             e->n_launch++;
             return HB_OK;
         }
         if (!force_g && gsel == 1 && e->latency_mode) {
-            k_blind_rotate_u2_lat<kDebug><<<a.n_work, 192, sizeof(BrLatSmemU2), e->stream>>>(a);
+            k_blind_rotate_u2_lat<kDebug><<<cnt, 192, sizeof(BrLatSmemU2), e->stream>>>(a);
             HB_CUDA_TRY(cudaGetLastError());
             e->n_launch++;
             return HB_OK;
         }
         if (gsel == 1) return launch_br_u2<1, kDebug>(e, a);
         if (gsel == 2) return launch_br_u2<2, kDebug>(e, a);
+        if (gsel == 3) return launch_br_u2<3, kDebug>(e, a);
 #if HB_U2_PAIRED
         if (!force_g) return launch_br_u2<2, kDebug, kPairedRing, 2>(e, a);  // two 2-gate CTAs per SM
 #endif
@@ -419,6 +438,11 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
                                      (int)sizeof(BrSmemU2<kBrGates>)));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(BrSmemU2<2>)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrSmemU2<3>)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrSmemU2<3>)));
+    if (const char *sw = std::getenv("HEBNN_B200_SPLIT_WAVES")) e->split_waves = std::atoi(sw) != 0;
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(BrSmemU2<1>)));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -13,7 +13,7 @@ from paper_1806_03461_b200 import tfhe  # noqa: E402
 keys = tfhe.KeySet(seed=3)
 eng = tfhe.Engine(keys)
 res = {}
-for n in (1, 16, 32, 33, 74, 148, 296, 592, 1184, 4096):
+for n in (1, 16, 20, 21, 32, 74, 75, 148, 149, 296, 297, 400, 444, 445, 592, 600, 729, 900, 1036, 1184, 4096):
     rng = np.random.default_rng(n)
     a = rng.integers(0, 2, n).astype(np.uint8)
     b = rng.integers(0, 2, n).astype(np.uint8)

@@ -197,12 +197,14 @@ np.save(sys.argv[1], eng.download(2 * n, n))
     assert np.array_equal(outs[0], outs[1])
 
 
-@pytest.mark.parametrize("n", [1, 5, 20, 100, 200])
+@pytest.mark.parametrize("n", [1, 5, 20, 100, 200, 400, 700])
 def test_narrow_level_kernels_agree(n):
     """Levels of <= #clusters of 6 CTAs, <= #SM/2, <= #SM and <= 2 #SM bootstraps
     run on the 6-CTA cluster kernel (key pairs), the 2-CTA cluster kernel, the
     latency kernel or 1-2 bootstraps per CTA; every choice must give the same
-    ciphertexts (both key layouts), and the first one equals the oracle's."""
+    ciphertexts (both key layouts), and the first one equals the oracle's.
+    400 runs on 3-bootstrap CTAs, 700 as one full wave of 4-bootstrap CTAs plus
+    a 3-bootstrap remainder launch (split waves) or two 4-bootstrap waves."""
     import os
     import subprocess
     import sys
@@ -232,13 +234,28 @@ np.save(sys.argv[1], eng.download(3 * n, n))
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     for unroll in (2, 1):
         outs = []
-        for lat, clu, c6 in (("1", "1", "1"), ("1", "1", "0"), ("1", "0", "0"), ("0", "0", "0")):
-            path = f"/tmp/hb_narrow_{n}_{unroll}_{lat}{clu}{c6}.npy"
-            env = dict(os.environ, HEBNN_B200_LATENCY_MODE=lat, HEBNN_B200_CLUSTER_MODE=clu, HEBNN_B200_CLU6=c6)
+        for lat, clu, c6, sw in (("1", "1", "1", "1"), ("1", "1", "0", "0"), ("1", "0", "0", "0"), ("0", "0", "0", "0")):
+            path = f"/tmp/hb_narrow_{n}_{unroll}_{lat}{clu}{c6}{sw}.npy"
+            env = dict(os.environ, HEBNN_B200_LATENCY_MODE=lat, HEBNN_B200_CLUSTER_MODE=clu, HEBNN_B200_CLU6=c6,
+                       HEBNN_B200_SPLIT_WAVES=sw)
             subprocess.run([sys.executable, "-c", code, path, str(n), str(unroll)], check=True, cwd=root, env=env)
             outs.append(np.load(path))
         for k in range(1, len(outs)):
             assert np.array_equal(outs[0], outs[k]), (unroll, k)
+        # the default path against the exact oracle on two records (a MAJ and an XOR)
+        p = tfhe.default_params()
+        p.bk_unroll = unroll
+        keys = tfhe.KeySet(seed=42, params=p)
+        cts = keys.encrypt(np.random.default_rng(n).integers(0, 2, 3 * n).astype(np.uint8), seed=6, stream=1)
+        po = O.default_params()
+        po.bk_unroll = unroll
+        octx = O.Context(po, O.Keys(po, 42))
+        for i in range(min(n, 2)):
+            if i % 2 == 0:
+                want = octx.gate3(0, 1, cts[i], 1, cts[n + i], 1, cts[2 * n + i])
+            else:
+                want = octx.gate(tfhe.GATE_LIN["XOR"][0], 2, cts[i], 2, cts[n + i])
+            assert np.array_equal(outs[0][i], want), (unroll, i)
 
 
 def test_random_mixed_level_bit_exact_vs_oracle(kit):

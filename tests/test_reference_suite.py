@@ -35,24 +35,16 @@ def test_reference_suite_on_plain_engine():
     assert " passed" in out and "failed" not in out
 
 
-# Deselected on the GPU tier only (each is thousands of one-level flushes at ~1.1-1.5 ms of
-# sequential bootstrap latency: 2-5 min apiece on the B200); they run on the CPU tier above
-# (plain engine) and, restated with lanes, in tests/test_gpu_reference_replay.py.
-GPU_DESELECT = (
-    "test_acceptance.py::test_criterion_8_comparator_equality",
-    "test_compiler.py::test_neuron_methods_exhaustive_small_d",
-    "test_acceptance.py::test_criterion_1_oracle_equivalence",
-)
-
-
 @pytest.mark.gpu
 def test_reference_suite_on_gpu():
-    """Unmodified reference tests on real ciphertexts, including the exhaustive
-    reduce tree (n <= 12, test_circuits.py:124-130) and k = 8 comparators
-    (test_circuits.py:216-223) the round-1 GPU tier had reduced."""
-    extra = ["--durations=10"] + [f"--deselect={os.path.join(REF_TESTS, d)}" for d in GPU_DESELECT]
+    """Unmodified reference tests on real ciphertexts, all of them, including the
+    exhaustive reduce tree (n <= 12, test_circuits.py:124-130) and k = 8
+    comparators (test_circuits.py:216-223) the round-1 GPU tier had reduced.
+    Each test is a chain of thousands of one-level flushes (sequential bootstrap
+    latency, a few SMs busy), so eight pytest-xdist workers — eight processes,
+    eight engines — share the B200."""
     out = _run(["test_backend.py", "test_circuits.py", "test_compiler.py", "test_acceptance.py"], "gpu", 3600,
-               extra=tuple(extra))
+               extra=("--durations=10", "-n", "8"))
     print(out[-3000:])
     assert " passed" in out and "failed" not in out
 

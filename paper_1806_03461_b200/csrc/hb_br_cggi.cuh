@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
                     if (nx < kStages || nx >= rows_needed) continue;
                     const int s2 = nx % kStages;
                     mbar_wait(&sm.empty[s2], ((nx / kStages) - 1) & 1);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the slot before its async-proxy refill
                     mbar_arrive_expect_tx(&sm.full[s2], kRowBytes);
                     bulk_g2s(sm.bk[s2], bk_src + (size_t)nx * kRowBytes, kRowBytes, &sm.full[s2]);
                 }

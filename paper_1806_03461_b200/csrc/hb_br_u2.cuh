@@ -88,8 +88,14 @@ struct BrSmemU2 {
 // reads and updates only its own ACC coefficients (bins t + 64 m of both
 // polynomials, no rotation), so ACC is thread-private: 32 TMEM columns of the
 // thread's lane, and the 32 KiB of shared memory go to the BK ring.
-template <int G, bool kDebug, int R = kStagesU2, int MB = 1, bool TM = false>
-__global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs args) {
+// WS: warp-specialised producer.  The CTA gets a fourth warpgroup whose first
+// thread alone streams the BK stages (waits for a free slot, issues the bulk
+// copy), so a refill is never delayed by the compute warp that used to issue it
+// at the start of each row pair; the producer warpgroup gives its registers to
+// the compute warps (setmaxnreg: 24 / 240).
+template <int G, bool kDebug, int R = kStagesU2, int MB = 1, bool TM = false, bool WS = false>
+__global__ void __launch_bounds__(64 * G + (WS ? 128 : 0), MB) k_blind_rotate_u2(const BrArgs args) {
+    static_assert(!WS || (G == 4 && !TM && MB == 1), "warp-specialised producer: 4 bootstraps per CTA");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     BrSmemU2<G, R, TM> &sm = *reinterpret_cast<BrSmemU2<G, R, TM> *>(smem_raw);
     constexpr bool kMidIssue = R < kRows + 1;
@@ -117,7 +123,7 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
             mbar_init(&sm.empty[s], 2 * G);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (; issued < R && issued < stages_needed; issued++) {
+        for (; !WS && issued < R && issued < stages_needed; issued++) {
             mbar_arrive_expect_tx(&sm.full[issued], kRowBytes);
             bulk_g2s(sm.bk[issued], bk_src + u2_stage(issued) * kRowBytes, kRowBytes, &sm.full[issued]);
         }
@@ -126,6 +132,27 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
     if (TM) tmem_fence_before();
     __syncthreads();
     if (TM) tmem_fence_after();
+    if (WS) {
+        if (warp >= 2 * G) {  // producer warpgroup
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");
+            if (threadIdx.x == 64 * G) {
+#pragma unroll 1
+                for (int s = 0; s < stages_needed; s++) {
+                    const int slot = s % R;
+                    if (s >= R) mbar_wait(&sm.empty[slot], ((s / R) - 1) & 1);
+                    // order the consumers' generic-proxy reads of this slot (released through
+                    // the empty barrier) before the async-proxy bulk copy that overwrites it;
+                    // without it the refill raced reads still in flight (tests/test_gpu_exactness.py
+                    // determinism: 1-3 of 16,384 ciphertexts differed per run)
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_arrive_expect_tx(&sm.full[slot], kRowBytes);
+                    bulk_g2s(sm.bk[slot], bk_src + u2_stage(s) * kRowBytes, kRowBytes, &sm.full[slot]);
+                }
+            }
+            return;
+        }
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 240;\n" ::: "memory");
+    }
     // this thread's 32 ACC columns: A at +0..15, B at +16..31 (lo bins m, then hi bins m)
     const uint32_t tacc = TM ? sm.tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + 32u * (uint32_t)(warp >> 2) : 0u;
 
@@ -161,6 +188,18 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
 
     double max_err = 0.0;
     int st = 0;  // next stage to consume
+    // WS (registers to spare): the psi table values of key pair pm + 1 are loaded
+    // during pair pm, so their L2 latency never stalls the MAC
+    constexpr bool kPre = WS;
+    double2 pre[3];
+    if (kPre && pairs > 0) {
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            const int ai = bar[0], aj = bar[1];
+            const int ec = c == 0 ? ((ai + aj) & (2 * kN - 1)) : (c == 1 ? ai : aj);
+            pre[c] = __ldg(&args.PSI[(ec * (4 * t + 1)) & (2 * kN - 1)]);
+        }
+    }
     for (int pm = 0; pm < pairs; pm++) {
         const int ai = bar[2 * pm], aj = bar[2 * pm + 1];
         // F_c at this thread's bins k = t + 64 m: psi^{e (4k+1)} - 1 =
@@ -170,7 +209,19 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
 #pragma unroll
         for (int c = 0; c < 3; c++) {
             ex[c] = c == 0 ? ((ai + aj) & (2 * kN - 1)) : (c == 1 ? ai : aj);
-            base[c] = __ldg(&args.PSI[(ex[c] * (4 * t + 1)) & (2 * kN - 1)]);
+            if (kPre) {
+                base[c] = pre[c];
+            } else {
+                base[c] = __ldg(&args.PSI[(ex[c] * (4 * t + 1)) & (2 * kN - 1)]);
+            }
+        }
+        if (kPre && pm + 1 < pairs) {
+            const int bi = bar[2 * pm + 2], bj = bar[2 * pm + 3];
+#pragma unroll
+            for (int c = 0; c < 3; c++) {
+                const int ec = c == 0 ? ((bi + bj) & (2 * kN - 1)) : (c == 1 ? bi : bj);
+                pre[c] = __ldg(&args.PSI[(ec * (4 * t + 1)) & (2 * kN - 1)]);
+            }
         }
         double2 f0[8], f1[8];
 #if HB_U2_MAC2
@@ -180,11 +231,12 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
 #pragma unroll 1
         for (int rp = 0; rp < kRows / 2; rp++) {
             // producer: refill the ring up to R stages ahead of this row pair
-            if (threadIdx.x == 0) {
+            if (!WS && threadIdx.x == 0) {
 #pragma unroll 1
                 for (; issued < st + R && issued < stages_needed; issued++) {
                     const int s2 = issued % R;
                     mbar_wait(&sm.empty[s2], ((issued / R) - 1) & 1);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the slot before its async-proxy refill
                     mbar_arrive_expect_tx(&sm.full[s2], kRowBytes);
                     bulk_g2s(sm.bk[s2], bk_src + u2_stage(issued) * kRowBytes, kRowBytes, &sm.full[s2]);
                 }
@@ -309,6 +361,7 @@ __global__ void __launch_bounds__(64 * G, MB) k_blind_rotate_u2(const BrArgs arg
                         for (; issued < st + 1 + R && issued < stages_needed; issued++) {
                             const int s2 = issued % R;
                             mbar_wait(&sm.empty[s2], ((issued / R) - 1) & 1);
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the slot before its async-proxy refill
                             mbar_arrive_expect_tx(&sm.full[s2], kRowBytes);
                             bulk_g2s(sm.bk[s2], bk_src + u2_stage(issued) * kRowBytes, kRowBytes, &sm.full[s2]);
                         }
@@ -552,6 +605,7 @@ __global__ void __launch_bounds__(192, 1) k_blind_rotate_u2_lat(const BrArgs arg
                 if (lane == 0) mbar_arrive(&empty[s]);
                 if (t == 0 && issued < stages_needed) {  // refill this slot kLatStagesU2 stages ahead
                     mbar_wait(&empty[s], ((issued / kLatStagesU2) - 1) & 1);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the slot before its async-proxy refill
                     mbar_arrive_expect_tx(&full[s], kRowBytes);
                     bulk_g2s(sm.bk[grp][s], stage_src(issued), kRowBytes, &full[s]);
                     issued++;

@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(128 * G, 1) k_blind_rotate_u2h(const BrArgs ar
                 for (; issued < st + R && issued < stages_needed; issued++) {
                     const int s2 = issued % R;
                     mbar_wait(&sm.empty[s2], ((issued / R) - 1) & 1);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the slot before its async-proxy refill
                     mbar_arrive_expect_tx(&sm.full[s2], kRowBytes);
                     bulk_g2s(sm.bk[s2], bk_src + u2h_src_stage(issued) * kRowBytes, kRowBytes, &sm.full[s2]);
                 }

@@ -66,6 +66,11 @@ __device__ __forceinline__ constexpr int rev3(int k) { return ((k & 1) << 2) | (
 __device__ __forceinline__ void group_bar(int id) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(64) : "memory");
 }
+// named barrier over kBT threads (the warps of one transform group)
+template <int kBT>
+__device__ __forceinline__ void group_bar_n(int id) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kBT) : "memory");
+}
 
 // Forward 512-point FFT (kernel e^{+2 pi i jk/512}) of x held as described
 // above.  W[e] = e^{2 pi i e / 512}.  S0/S1: two exchange buffers (double
@@ -163,7 +168,7 @@ __device__ __forceinline__ void tw_powers(double2 T0, double2 step, bool t0_is_o
 // kSB (single buffer): xch is [NP][kXchStride]; both exchanges share one
 // buffer, at the price of two more barriers (one before the first store, one
 // between the second exchange's loads and stores).
-template <int NP, bool kSB = false>
+template <int NP, bool kSB = false, int kBT = 64>
 __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch, int t, const TwSeeds &tw,
                                                int bar_id) {
     constexpr int kB0 = kSB ? 1 : 2, kB1 = kSB ? 0 : 1;  // buffer q of exchange 1 / 2: q * kB0 + kB1 * (..)
@@ -173,7 +178,7 @@ __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch
         for (int m = 1; m < 8; m++) x[q][m] = cmul(x[q][m], c16(m));
         dft8(x[q]);
     }
-    if (kSB) group_bar(bar_id);  // previous transform's readers are done
+    if (kSB) group_bar_n<kBT>(bar_id);  // previous transform's readers are done
     {
         const int j0 = t & 7, j1 = t >> 3;
         double2 T[8];
@@ -184,7 +189,7 @@ __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch
             for (int q = 0; q < NP; q++) xch[(kB0 * q) * kXchStride + j0 * 65 + k2 * 8 + j1] = cmul(x[q][rev3(k2)], T[k2]);
         }
     }
-    if (HB_EXP_SKIP & 64) __syncwarp(); else group_bar(bar_id);
+    if (HB_EXP_SKIP & 64) __syncwarp(); else group_bar_n<kBT>(bar_id);
     {
         const int j0 = t & 7, k2 = t >> 3;
 #pragma unroll
@@ -195,7 +200,7 @@ __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch
             if (!kSB) xch[(kB0 * q + kB1) * kXchStride + k2 * 65 + j0] = x[q][0];
         }
         if (kSB) {
-            group_bar(bar_id);
+            group_bar_n<kBT>(bar_id);
 #pragma unroll
             for (int q = 0; q < NP; q++) xch[(kB0 * q + kB1) * kXchStride + k2 * 65 + j0] = x[q][0];
         }
@@ -208,7 +213,7 @@ __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch
                 xch[(kB0 * q + kB1) * kXchStride + k2 * 65 + k1 * 8 + j0] = cmul(x[q][rev3(k1)], T[k1]);
         }
     }
-    if (HB_EXP_SKIP & 32) __syncwarp(); else group_bar(bar_id);
+    if (HB_EXP_SKIP & 32) __syncwarp(); else group_bar_n<kBT>(bar_id);
     {
         const int k2 = t & 7, k1 = t >> 3;
 #pragma unroll
@@ -223,7 +228,7 @@ __device__ __forceinline__ void nega_fft_fwd_n(double2 (&x)[NP][8], double2 *xch
     }
 }
 
-template <int NP, bool kSB = false>
+template <int NP, bool kSB = false, int kBT = 64>
 __device__ __forceinline__ void nega_fft_inv_n(double2 (&x)[NP][8], double2 *xch, int t, const TwSeeds &tw,
                                                int bar_id) {
     constexpr int kB0 = kSB ? 1 : 2, kB1 = kSB ? 0 : 1;
@@ -233,7 +238,7 @@ __device__ __forceinline__ void nega_fft_inv_n(double2 (&x)[NP][8], double2 *xch
         for (int m = 0; m < 8; m++) x[q][m].y = -x[q][m].y;
         dft8(x[q]);
     }
-    if (kSB) group_bar(bar_id);
+    if (kSB) group_bar_n<kBT>(bar_id);
     {
         const int j0 = t & 7, j1 = t >> 3;
 #pragma unroll
@@ -246,7 +251,7 @@ __device__ __forceinline__ void nega_fft_inv_n(double2 (&x)[NP][8], double2 *xch
             for (int q = 0; q < NP; q++) xch[(kB0 * q) * kXchStride + j0 * 65 + k2 * 8 + j1] = cmul(x[q][rev3(k2)], T[k2]);
         }
     }
-    if (HB_EXP_SKIP & 64) __syncwarp(); else group_bar(bar_id);
+    if (HB_EXP_SKIP & 64) __syncwarp(); else group_bar_n<kBT>(bar_id);
     {
         const int j0 = t & 7, k2 = t >> 3;
 #pragma unroll
@@ -255,7 +260,7 @@ __device__ __forceinline__ void nega_fft_inv_n(double2 (&x)[NP][8], double2 *xch
             for (int j1 = 0; j1 < 8; j1++) x[q][j1] = xch[(kB0 * q) * kXchStride + j0 * 65 + k2 * 8 + j1];
             dft8(x[q]);
         }
-        if (kSB) group_bar(bar_id);
+        if (kSB) group_bar_n<kBT>(bar_id);
         double2 T[8];
         tw_powers(tw.i_b0, tw.i_stepb, false, T);
 #pragma unroll
@@ -265,7 +270,7 @@ __device__ __forceinline__ void nega_fft_inv_n(double2 (&x)[NP][8], double2 *xch
                 xch[(kB0 * q + kB1) * kXchStride + k2 * 65 + k1 * 8 + j0] = cmul(x[q][rev3(k1)], T[k1]);
         }
     }
-    if (HB_EXP_SKIP & 32) __syncwarp(); else group_bar(bar_id);
+    if (HB_EXP_SKIP & 32) __syncwarp(); else group_bar_n<kBT>(bar_id);
     {
         const int k2 = t & 7, k1 = t >> 3;
 #pragma unroll

@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(kKsThreads) k_keyswitch(const KsArgs args) {
             if (nx < kBlocks) {
                 const int s2 = nx % kKsStages;
                 if (nx >= kKsStages) mbar_wait(&ks.empty[s2], ((nx / kKsStages) - 1) & 1);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the slot before its async-proxy refill
                 mbar_arrive_expect_tx(&ks.full[s2], kKsStageBytes);
                 bulk_g2s(ks.tab[s2], tab_src + (size_t)nx * kKsStageBytes, kKsStageBytes, &ks.full[s2]);
             }

@@ -144,8 +144,10 @@ struct BrSmem {
     TwSeeds tws[64];                          // per-thread twiddle seeds
 };
 
-template <int G, bool kDebug>
-__global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
+// WS: warp-specialised producer warpgroup (see k_blind_rotate_u2)
+template <int G, bool kDebug, bool WS = false>
+__global__ void __launch_bounds__(64 * G + (WS ? 128 : 0), 1) k_blind_rotate(const BrArgs args) {
+    static_assert(!WS || G == 4, "warp-specialised producer: 4 bootstraps per CTA");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     BrSmem<G> &sm = *reinterpret_cast<BrSmem<G> *>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -173,12 +175,29 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
             mbar_init(&sm.empty[s], 2 * G);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int it = 0; it < kStages && it < rows_needed && !HB_BK_LDG; it++) {
+        for (int it = 0; it < kStages && it < rows_needed && !HB_BK_LDG && !WS; it++) {
             mbar_arrive_expect_tx(&sm.full[it], kRowBytes);
             bulk_g2s(sm.bk[it], bk_src + (size_t)it * kRowBytes, kRowBytes, &sm.full[it]);
         }
     }
     __syncthreads();
+    if (WS) {
+        if (warp >= 2 * G) {  // producer warpgroup
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");
+            if (threadIdx.x == 64 * G) {
+#pragma unroll 1
+                for (int it = 0; it < rows_needed; it++) {
+                    const int slot = it % kStages;
+                    if (it >= kStages) mbar_wait(&sm.empty[slot], ((it / kStages) - 1) & 1);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_arrive_expect_tx(&sm.full[slot], kRowBytes);
+                    bulk_g2s(sm.bk[slot], bk_src + (size_t)it * kRowBytes, kRowBytes, &sm.full[slot]);
+                }
+            }
+            return;
+        }
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 240;\n" ::: "memory");
+    }
 
     // ---- gate groups: 64 threads (2 warps) per bootstrap ----
     const int g = warp >> 1;
@@ -232,7 +251,7 @@ __global__ void __launch_bounds__(64 * G, 1) k_blind_rotate(const BrArgs args) {
             }
 #endif
             // producer: rows row_it+1 and row_it+2 (stages freed by rows row_it-2, row_it-1)
-            if (!HB_BK_LDG && threadIdx.x == 0) {
+            if (!HB_BK_LDG && !WS && threadIdx.x == 0) {
 #pragma unroll 1
                 for (int nx = row_it + 1; nx <= row_it + 2; nx++) {
                     if (nx < kStages || nx >= rows_needed) continue;

@@ -54,6 +54,9 @@ constexpr int kStagesPerPair = 3 * kRows;  // (row pair, component, row) stages 
 #ifndef HB_U2_MAC2
 #define HB_U2_MAC2 1  // MAC over both rows of a row pair per bin (fewer live registers; 0: row by row)
 #endif
+#ifndef HB_U2_BKC
+#define HB_U2_BKC 1  // MAC2 with the three components combined per bin before the digit product
+#endif
 #ifndef HB_EXP_NO_BK_LDS
 #define HB_EXP_NO_BK_LDS 0
 #endif
@@ -93,9 +96,19 @@ struct BrSmemU2 {
 // copy), so a refill is never delayed by the compute warp that used to issue it
 // at the start of each row pair; the producer warpgroup gives its registers to
 // the compute warps (setmaxnreg: 24 / 240).
+// Compute warps are padded to whole warpgroups (G = 3: warps 6, 7 idle) so that
+// the producer is a warpgroup of its own; setmaxnreg only where the launch
+// bounds cap the registers (384 threads).
+template <int G, bool WS>
+__host__ __device__ constexpr int u2_compute_warps() { return WS ? ((2 * G + 3) / 4) * 4 : 2 * G; }
+template <int G, bool WS>
+__host__ __device__ constexpr int u2_threads() { return WS ? 32 * (u2_compute_warps<G, WS>() + 4) : 64 * G; }
+
 template <int G, bool kDebug, int R = kStagesU2, int MB = 1, bool TM = false, bool WS = false>
-__global__ void __launch_bounds__(64 * G + (WS ? 128 : 0), MB) k_blind_rotate_u2(const BrArgs args) {
-    static_assert(!WS || (G == 4 && !TM && MB == 1), "warp-specialised producer: 4 bootstraps per CTA");
+__global__ void __launch_bounds__(u2_threads<G, WS>(), MB) k_blind_rotate_u2(const BrArgs args) {
+    static_assert(!WS || (!TM && MB == 1), "warp-specialised producer: one CTA per SM, shared-memory ACC");
+    constexpr int kCW = u2_compute_warps<G, WS>();
+    constexpr bool kSetMax = WS && u2_threads<G, WS>() == 384;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     BrSmemU2<G, R, TM> &sm = *reinterpret_cast<BrSmemU2<G, R, TM> *>(smem_raw);
     constexpr bool kMidIssue = R < kRows + 1;
@@ -133,9 +146,9 @@ __global__ void __launch_bounds__(64 * G + (WS ? 128 : 0), MB) k_blind_rotate_u2
     __syncthreads();
     if (TM) tmem_fence_after();
     if (WS) {
-        if (warp >= 2 * G) {  // producer warpgroup
-            asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");
-            if (threadIdx.x == 64 * G) {
+        if (warp >= kCW) {  // producer warpgroup
+            if (kSetMax) asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");
+            if (threadIdx.x == 32 * kCW) {
 #pragma unroll 1
                 for (int s = 0; s < stages_needed; s++) {
                     const int slot = s % R;
@@ -151,7 +164,8 @@ __global__ void __launch_bounds__(64 * G + (WS ? 128 : 0), MB) k_blind_rotate_u2
             }
             return;
         }
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 240;\n" ::: "memory");
+        if (kSetMax) asm volatile("setmaxnreg.inc.sync.aligned.u32 240;\n" ::: "memory");
+        if (warp >= 2 * G) return;  // warpgroup padding
     }
     // this thread's 32 ACC columns: A at +0..15, B at +16..31 (lo bins m, then hi bins m)
     const uint32_t tacc = TM ? sm.tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + 32u * (uint32_t)(warp >> 2) : 0u;
@@ -277,6 +291,61 @@ __global__ void __launch_bounds__(64 * G + (WS ? 128 : 0), MB) k_blind_rotate_u2
             // m loop (8 live registers instead of 32), two independent products per
             // bin, accumulators zeroed at the start of the pair
             static_assert(!kMidIssue, "MAC2 consumes the row pair's two stages of a component together");
+#if HB_U2_BKC
+            // combined key per bin: C_{h,o} = sum_c F_c BK_{h,c,o} (12 complex products), then
+            // ACC_o += x_h C_{h,o} (4): 64 FP64 instructions per bin instead of 72
+            {
+                int sl[6];
+#pragma unroll
+                for (int i = 0; i < 6; i++) {
+                    sl[i] = (st + i) % R;
+                    mbar_wait(&sm.full[sl[i]], ((st + i) / R) & 1);
+                }
+#pragma unroll
+                for (int m = 0; m < 4; m++) {
+                    double2 Fm[3][2];
+#pragma unroll
+                    for (int c = 0; c < 3; c++) {
+                        const long long flip = (long long)(ex[c] & 1) << 63;
+                        const double2 pw = m == 0 ? base[c] : cmul(base[c], c_w8[(ex[c] * m) & 7]);
+                        Fm[c][0] = make_double2(pw.x - 1.0, pw.y);
+                        Fm[c][1] = make_double2(__longlong_as_double(__double_as_longlong(pw.x) ^ flip) - 1.0,
+                                                __longlong_as_double(__double_as_longlong(pw.y) ^ flip));
+                    }
+#pragma unroll
+                    for (int hi = 0; hi < 2; hi++) {
+                        const int mm = m + 4 * hi;
+                        const int k = t + 64 * mm;
+                        double2 C[2][2];
+#pragma unroll
+                        for (int c = 0; c < 3; c++) {
+#pragma unroll
+                            for (int h = 0; h < 2; h++) {
+                                const double2 *bk = sm.bk[sl[2 * c + h]];
+                                if (c == 0) {
+                                    C[h][0] = cmul(Fm[c][hi], bk[k]);
+                                    C[h][1] = cmul(Fm[c][hi], bk[kNH + k]);
+                                } else {
+                                    cmac(C[h][0], Fm[c][hi], bk[k]);
+                                    cmac(C[h][1], Fm[c][hi], bk[kNH + k]);
+                                }
+                            }
+                        }
+                        cmac(f0[mm], x[0][mm], C[0][0]);
+                        cmac(f1[mm], x[0][mm], C[0][1]);
+                        cmac(f0[mm], x[1][mm], C[1][0]);
+                        cmac(f1[mm], x[1][mm], C[1][1]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+#pragma unroll
+                    for (int i = 0; i < 6; i++) mbar_arrive(&sm.empty[sl[i]]);
+                }
+                __syncwarp();
+                st += 6;
+            }
+#else
 #pragma unroll
             for (int c = 0; c < 3; c++, st += 2) {
                 const long long flip = (long long)(ex[c] & 1) << 63;
@@ -309,6 +378,7 @@ __global__ void __launch_bounds__(64 * G + (WS ? 128 : 0), MB) k_blind_rotate_u2
                 }
                 __syncwarp();
             }
+#endif  // HB_U2_BKC
 #else
 #pragma unroll
             for (int c = 0; c < 3; c++) {

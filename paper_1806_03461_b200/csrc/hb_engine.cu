@@ -152,6 +152,14 @@ template <int G, bool kDebug>
 int launch_br(hb_engine *e, const BrArgs &a) {
     const size_t smem = br_smem_bytes<G>();
     const unsigned grid = (a.n_work - a.e0 + G - 1) / G;
+    if constexpr (G == kBrGates) {
+        if (e->u2ws) {
+            k_blind_rotate<G, kDebug, true><<<grid, 64 * G + 128, smem, e->stream>>>(a);
+            HB_CUDA_TRY(cudaGetLastError());
+            e->n_launch++;
+            return HB_OK;
+        }
+    }
     k_blind_rotate<G, kDebug><<<grid, 64 * G, smem, e->stream>>>(a);
     HB_CUDA_TRY(cudaGetLastError());
     e->n_launch++;
@@ -161,7 +169,7 @@ int launch_br(hb_engine *e, const BrArgs &a) {
 template <int G, bool kDebug, int R = kStagesU2, int MB = 1, bool TM = false, bool WS = false>
 int launch_br_u2(hb_engine *e, const BrArgs &a) {
     const unsigned grid = (a.n_work - a.e0 + G - 1) / G;
-    k_blind_rotate_u2<G, kDebug, R, MB, TM, WS><<<grid, 64 * G + (WS ? 128 : 0), sizeof(BrSmemU2<G, R, TM>), e->stream>>>(a);
+    k_blind_rotate_u2<G, kDebug, R, MB, TM, WS><<<grid, u2_threads<G, WS>(), sizeof(BrSmemU2<G, R, TM>), e->stream>>>(a);
     HB_CUDA_TRY(cudaGetLastError());
     e->n_launch++;
     return HB_OK;
@@ -298,8 +306,10 @@ int launch_br_auto(hb_engine *e, const BrArgs &a0, int force_g = 0) {
             return HB_OK;
         }
         if (gsel == 1) return launch_br_u2<1, kDebug>(e, a);
-        if (gsel == 2) return launch_br_u2<2, kDebug>(e, a);
-        if (gsel == 3) return launch_br_u2<3, kDebug>(e, a);
+        if (gsel == 2)
+            return e->u2ws ? launch_br_u2<2, kDebug, kStagesU2, 1, false, true>(e, a) : launch_br_u2<2, kDebug>(e, a);
+        if (gsel == 3)
+            return e->u2ws ? launch_br_u2<3, kDebug, kStagesU2, 1, false, true>(e, a) : launch_br_u2<3, kDebug>(e, a);
 #if HB_U2_PAIRED
         if (!force_g) return launch_br_u2<2, kDebug, kPairedRing, 2>(e, a);  // two 2-gate CTAs per SM
 #endif
@@ -417,6 +427,10 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
                                      (int)br_smem_bytes<1>()));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)br_smem_bytes<kBrGates>()));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<kBrGates, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)br_smem_bytes<kBrGates>()));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate<kBrGates, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)br_smem_bytes<kBrGates>()));
 #if HB_U2_TMEM
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, false, kStagesU2Tmem, 1, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -448,6 +462,14 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
     if (const char *us = std::getenv("HEBNN_B200_U2S")) e->u2s = std::atoi(us) != 0;
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, false, kStagesU2, 1, false, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BrSmemU2<kBrGates>)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<3, false, kStagesU2, 1, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BrSmemU2<3>)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<3, true, kStagesU2, 1, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BrSmemU2<3>)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<2, false, kStagesU2, 1, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BrSmemU2<2>)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<2, true, kStagesU2, 1, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BrSmemU2<2>)));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, true, kStagesU2, 1, false, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BrSmemU2<kBrGates>)));
     if (const char *uw = std::getenv("HEBNN_B200_U2WS")) e->u2ws = std::atoi(uw) != 0;

@@ -1,6 +1,6 @@
 """A/B of wide-level blind-rotation variants selected by engine environment switches.
 
-    python scripts/ab_kernel.py HEBNN_B200_U2S [n_gates]
+    python scripts/ab_kernel.py HEBNN_B200_U2S [n_gates] [bk_unroll]
 
 Runs the same level of n NAND gates (default 4,096) with the switch 0 and 1 on
 fresh engines of one key set, reports the blind-rotation / key-switch times
@@ -19,7 +19,10 @@ from paper_1806_03461_b200 import tfhe  # noqa: E402
 
 var = sys.argv[1] if len(sys.argv) > 1 else "HEBNN_B200_U2S"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
-K = tfhe.KeySet(seed=1)
+unroll = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+params = tfhe.default_params()
+params.bk_unroll = unroll
+K = tfhe.KeySet(seed=1, params=params)
 rng = np.random.default_rng(0)
 a = rng.integers(0, 2, n).astype(np.uint8)
 b = rng.integers(0, 2, n).astype(np.uint8)
@@ -54,3 +57,5 @@ for v in ("0", "1"):
           f"plaintexts ok: {ok}", flush=True)
     eng.close()
 print("identical ciphertexts:", np.array_equal(outs["0"], outs["1"]))
+if os.environ.get("AB_OUT"):  # cross-library comparisons (HEBNN_B200_LIB variants)
+    np.save(os.environ["AB_OUT"], outs["1"])

@@ -18,7 +18,9 @@ from paper_1806_03461_b200 import tfhe  # noqa: E402
 var = sys.argv[1] if len(sys.argv) > 1 else "HEBNN_B200_U2WS"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
 runs = int(sys.argv[3]) if len(sys.argv) > 3 else 8
-K = tfhe.KeySet(seed=1)
+params = tfhe.default_params()
+params.bk_unroll = int(sys.argv[4]) if len(sys.argv) > 4 else 2
+K = tfhe.KeySet(seed=1, params=params)
 rng = np.random.default_rng(78)
 a = rng.integers(0, 2, n).astype(np.uint8)
 b = rng.integers(0, 2, n).astype(np.uint8)

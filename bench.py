@@ -45,14 +45,15 @@ import numpy as np  # noqa: E402
 # F_BS: algorithmic FP64 flops of one blind rotation.
 # CGGI key (bk_unroll 1): n * [(k+1)(l+1) * F_FFT + (k+1)^2 * l * (N/2) * 8],
 #   F_FFT = 5 (N/2) log2(N/2) + 6 (N/2) (transform + twist), 8 flops per complex MAC.
-# Key pairs (bk_unroll 2): n/2 * [(k+1)(l+1) * F_FFT + (k+1) l * 3 * (N/2) * (6 + 2 * 8) + 3 * (N/2) * 7]:
-#   per pair one external product; per (digit row, component, bin) one complex
-#   product with (X^e - 1) and two complex MACs; (X^e - 1) evaluated once per
+# Key pairs (bk_unroll 2): n/2 * [(k+1)(l+1) * F_FFT + (l * (N/2)) * (4 * (6 + 2 * 8) + 4 * 8) + 3 * (N/2) * 7]:
+#   per key pair one external product; per row pair and bin the combined key
+#   C_{h,o} = sum_c F_c BK_{h,c,o} (4 of them: one complex product + two complex MACs
+#   each) and four complex MACs x_h C_{h,o}; F_c = (X^e_c - 1) evaluated once per
 #   component and bin (complex product + subtraction).
 F_FFT = 5 * 512 * 9 + 6 * 512
 F_BS1 = 630 * (2 * 4 * F_FFT + 4 * 3 * 512 * 8)
-F_BS2 = 315 * (2 * 4 * F_FFT + 2 * 3 * 3 * 512 * 22 + 3 * 512 * 7)
-assert F_BS1 == 162_570_240 and F_BS2 == 133_056_000
+F_BS2 = 315 * (2 * 4 * F_FFT + 3 * 512 * (4 * (6 + 2 * 8) + 4 * 8) + 3 * 512 * 7)
+assert F_BS1 == 162_570_240 and F_BS2 == 127_249_920
 F_BS = {1: F_BS1, 2: F_BS2}
 METRIC = "bootstrapped gates/sec"
 WORKLOAD = "cfg1: 4096 independent bootstrapped NAND gates per GPU (TFHE n=630,N=1024,k=1,Bg=2^7,l=3,KS 2^2x8)"

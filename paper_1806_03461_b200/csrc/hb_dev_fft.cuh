@@ -31,34 +31,44 @@ __device__ __forceinline__ void cmac(double2 &acc, double2 a, double2 b) {
 }
 
 // In-place DFT-8 with kernel e^{+2 pi i / 8}; output in bit-reversed order.
+// The two w8 = (1+i)/sqrt2 twiddles of the first radix-2 stage are carried
+// unscaled through the second stage and applied by the FMAs of the third
+// (x4 +- r (u + v)): 52 FP64 instructions instead of 56.
 __device__ __forceinline__ void dft8(double2 (&x)[8]) {
     const double r = 0.70710678118654752440;
+    // stage 1: a_m = x_m + x_{m+4}; odd branch b_m = (x_m - x_{m+4}) w8^m, b_1 and b_3 left unscaled by r
+    double2 b[4];
 #pragma unroll
     for (int m = 0; m < 4; m++) {
-        double2 a = x[m], b = x[m + 4];
-        x[m] = cadd(a, b);
-        double2 d = csub(a, b);
-        if (m == 0) x[m + 4] = d;
-        else if (m == 1) x[m + 4] = make_double2((d.x - d.y) * r, (d.x + d.y) * r);
-        else if (m == 2) x[m + 4] = make_double2(-d.y, d.x);
-        else x[m + 4] = make_double2((-d.x - d.y) * r, (d.x - d.y) * r);
+        const double2 a = x[m], c = x[m + 4];
+        x[m] = cadd(a, c);
+        b[m] = csub(a, c);
     }
+    const double2 b1 = make_double2(b[1].x - b[1].y, b[1].x + b[1].y);     // sqrt2 * b_1 w8
+    const double2 b3 = make_double2(-b[3].x - b[3].y, b[3].x - b[3].y);    // sqrt2 * b_3 w8^3
+    const double2 b2 = make_double2(-b[2].y, b[2].x);                       // b_2 * i
+    // stage 2, even half (x[0..3]) and odd half (b0, b1, b2, b3)
 #pragma unroll
-    for (int h = 0; h < 8; h += 4) {
-#pragma unroll
-        for (int m = 0; m < 2; m++) {
-            double2 a = x[h + m], b = x[h + m + 2];
-            x[h + m] = cadd(a, b);
-            double2 d = csub(a, b);
-            x[h + m + 2] = (m == 0) ? d : make_double2(-d.y, d.x);
-        }
+    for (int m = 0; m < 2; m++) {
+        const double2 a = x[m], c = x[m + 2];
+        x[m] = cadd(a, c);
+        const double2 d = csub(a, c);
+        x[m + 2] = (m == 0) ? d : make_double2(-d.y, d.x);
     }
+    const double2 e0 = cadd(b[0], b2), e2 = csub(b[0], b2);
+    const double2 s5 = cadd(b1, b3), d7 = csub(b1, b3);
+    const double2 s7 = make_double2(-d7.y, d7.x);                           // (b1 - b3) * i, still unscaled
+    // stage 3
 #pragma unroll
-    for (int h = 0; h < 8; h += 2) {
-        double2 a = x[h], b = x[h + 1];
-        x[h] = cadd(a, b);
-        x[h + 1] = csub(a, b);
+    for (int h = 0; h < 4; h += 2) {
+        const double2 a = x[h], c = x[h + 1];
+        x[h] = cadd(a, c);
+        x[h + 1] = csub(a, c);
     }
+    x[4] = make_double2(fma(r, s5.x, e0.x), fma(r, s5.y, e0.y));
+    x[5] = make_double2(fma(-r, s5.x, e0.x), fma(-r, s5.y, e0.y));
+    x[6] = make_double2(fma(r, s7.x, e2.x), fma(r, s7.y, e2.y));
+    x[7] = make_double2(fma(-r, s7.x, e2.x), fma(-r, s7.y, e2.y));
 }
 
 __device__ __forceinline__ constexpr int rev3(int k) { return ((k & 1) << 2) | (k & 2) | ((k >> 2) & 1); }

@@ -47,8 +47,6 @@ namespace {
 #include "hb_dev_fft.cuh"
 #include "hb_br_cggi.cuh"
 #include "hb_br_u2.cuh"
-#include "hb_br_u2h.cuh"
-#include "hb_br_u2s.cuh"
 #include "hb_br_clu6.cuh"
 #include "hb_ks.cuh"
 
@@ -107,12 +105,8 @@ struct hb_engine {
     int clu6_max = 0;                     // co-resident 6-CTA clusters (0: kernel unavailable); HEBNN_B200_CLU6=0 off
     bool split_waves = true;              // wide levels: full 4-bootstrap waves + a faster remainder kernel
                                           // (HEBNN_B200_SPLIT_WAVES=0 off)
-    bool u2s = false;                     // wide key-pair levels: two bootstraps per warp, shared BK loads
-                                          // (HEBNN_B200_U2S=1)
     bool u2ws = true;                     // wide key-pair levels: warp-specialised BK producer (HEBNN_B200_U2WS=0 off;
                                           // 31.2 -> 28.5 ms per 4,096)
-    bool u2h = false;                     // experiment (HEBNN_B200_U2H=1): 128 threads per bootstrap on wide
-                                          // key-pair levels; 42.7 ms vs 31.2 ms per 4,096 (profiles/r02_a)
 };
 
 namespace {
@@ -170,27 +164,6 @@ template <int G, bool kDebug, int R = kStagesU2, int MB = 1, bool TM = false, bo
 int launch_br_u2(hb_engine *e, const BrArgs &a) {
     const unsigned grid = (a.n_work - a.e0 + G - 1) / G;
     k_blind_rotate_u2<G, kDebug, R, MB, TM, WS><<<grid, u2_threads<G, WS>(), sizeof(BrSmemU2<G, R, TM>), e->stream>>>(a);
-    HB_CUDA_TRY(cudaGetLastError());
-    e->n_launch++;
-    return HB_OK;
-}
-
-template <bool kDebug>
-int launch_br_u2s(hb_engine *e, const BrArgs &a) {
-    const unsigned grid = (a.n_work - a.e0 + kBrGates - 1) / kBrGates;
-    if (e->u2ws)
-        k_blind_rotate_u2s<kDebug, true><<<grid, 384, sizeof(BrSmemU2<kBrGates, kStagesU2, false>), e->stream>>>(a);
-    else
-        k_blind_rotate_u2s<kDebug><<<grid, 256, sizeof(BrSmemU2<kBrGates, kStagesU2, false>), e->stream>>>(a);
-    HB_CUDA_TRY(cudaGetLastError());
-    e->n_launch++;
-    return HB_OK;
-}
-
-template <int G, bool kDebug>
-int launch_br_u2h(hb_engine *e, const BrArgs &a) {
-    const unsigned grid = (a.n_work - a.e0 + G - 1) / G;
-    k_blind_rotate_u2h<G, kDebug><<<grid, 128 * G, sizeof(BrSmemU2H<G>), e->stream>>>(a);
     HB_CUDA_TRY(cudaGetLastError());
     e->n_launch++;
     return HB_OK;
@@ -276,9 +249,8 @@ int launch_br_auto(hb_engine *e, const BrArgs &a0, int force_g = 0) {
         if (cnt > wave && cnt % wave != 0 && cnt % wave <= 3 * sms) {
             BrArgs head = a;
             head.n_work = a.e0 + (cnt / wave) * wave;
-            int rc = e->u2s ? launch_br_u2s<kDebug>(e, head)
-                            : (e->u2ws ? launch_br_u2<kBrGates, kDebug, kStagesU2, 1, false, true>(e, head)
-                                       : launch_br_u2<kBrGates, kDebug>(e, head));
+            int rc = e->u2ws ? launch_br_u2<kBrGates, kDebug, kStagesU2, 1, false, true>(e, head)
+                             : launch_br_u2<kBrGates, kDebug>(e, head);
             if (rc) return rc;
             a.e0 = head.n_work;
         }
@@ -316,8 +288,6 @@ int launch_br_auto(hb_engine *e, const BrArgs &a0, int force_g = 0) {
 #if HB_U2_TMEM
         return launch_br_u2<kBrGates, kDebug, kStagesU2Tmem, 1, true>(e, a);
 #else
-        if (e->u2h) return launch_br_u2h<kBrGates, kDebug>(e, a);
-        if (e->u2s) return launch_br_u2s<kDebug>(e, a);
         if (e->u2ws) return launch_br_u2<kBrGates, kDebug, kStagesU2, 1, false, true>(e, a);
         return launch_br_u2<kBrGates, kDebug>(e, a);
 #endif
@@ -446,20 +416,6 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
 #endif
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(BrSmemU2<kBrGates>)));
-    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2h<kBrGates, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(BrSmemU2H<kBrGates>)));
-    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2h<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(BrSmemU2H<kBrGates>)));
-    if (const char *uh = std::getenv("HEBNN_B200_U2H")) e->u2h = std::atoi(uh) != 0;
-    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2s<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(BrSmemU2<kBrGates, kStagesU2, false>)));
-    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2s<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(BrSmemU2<kBrGates, kStagesU2, false>)));
-    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2s<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(BrSmemU2<kBrGates, kStagesU2, false>)));
-    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2s<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(BrSmemU2<kBrGates, kStagesU2, false>)));
-    if (const char *us = std::getenv("HEBNN_B200_U2S")) e->u2s = std::atoi(us) != 0;
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, false, kStagesU2, 1, false, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BrSmemU2<kBrGates>)));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<3, false, kStagesU2, 1, false, true>,

@@ -1,6 +1,6 @@
 """A/B of wide-level blind-rotation variants selected by engine environment switches.
 
-    python scripts/ab_kernel.py HEBNN_B200_U2S [n_gates] [bk_unroll]
+    python scripts/ab_kernel.py HEBNN_B200_U2WS [n_gates] [bk_unroll]
 
 Runs the same level of n NAND gates (default 4,096) with the switch 0 and 1 on
 fresh engines of one key set, reports the blind-rotation / key-switch times
@@ -17,7 +17,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1806_03461_b200 import tfhe  # noqa: E402
 
-var = sys.argv[1] if len(sys.argv) > 1 else "HEBNN_B200_U2S"
+var = sys.argv[1] if len(sys.argv) > 1 else "HEBNN_B200_U2WS"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
 unroll = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 params = tfhe.default_params()

@@ -48,6 +48,7 @@ namespace {
 #include "hb_br_cggi.cuh"
 #include "hb_br_u2.cuh"
 #include "hb_br_clu6.cuh"
+#include "hb_br_clu8.cuh"
 #include "hb_ks.cuh"
 
 }  // namespace
@@ -102,6 +103,7 @@ struct hb_engine {
     size_t max_work = kMaxWorkPerLaunch;  // HEBNN_B200_MAX_WORK overrides (tests)
     bool latency_mode = true;             // HEBNN_B200_LATENCY_MODE=0 disables (A/B tests)
     bool cluster_mode = true;             // 2-CTA clusters for <= #SM/2 key-pair bootstraps (HEBNN_B200_CLUSTER_MODE=0)
+    int clu8_max = 0;                     // co-resident 8-CTA clusters (bin-split lone-level kernel); HEBNN_B200_CLU8=0 off
     int clu6_max = 0;                     // co-resident 6-CTA clusters (0: kernel unavailable); HEBNN_B200_CLU6=0 off
     bool split_waves = true;              // wide levels: full 4-bootstrap waves + a faster remainder kernel
                                           // (HEBNN_B200_SPLIT_WAVES=0 off)
@@ -259,6 +261,12 @@ int launch_br_auto(hb_engine *e, const BrArgs &a0, int force_g = 0) {
     const int gsel = force_g ? force_g
                              : (cnt <= sms ? 1 : (cnt <= 2u * sms ? 2 : (cnt <= 3u * sms && e->unroll == 2 ? 3 : kBrGates)));
     if (e->unroll == 2) {
+        if (!force_g && e->latency_mode && e->cluster_mode && cnt <= (uint32_t)e->clu8_max) {
+            k_blind_rotate_u2_clu8<kDebug><<<kClu8 * cnt, 192, sizeof(BrClu8Smem), e->stream>>>(a);
+            HB_CUDA_TRY(cudaGetLastError());
+            e->n_launch++;
+            return HB_OK;
+        }
         if (!force_g && e->latency_mode && e->cluster_mode && cnt <= (uint32_t)e->clu6_max) {
             k_blind_rotate_u2_clu6<kDebug><<<kClu6 * cnt, 192, sizeof(BrClu6Smem), e->stream>>>(a);
             HB_CUDA_TRY(cudaGetLastError());
@@ -446,6 +454,24 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
         e->clu6_max = ncl;
         if (const char *c6 = std::getenv("HEBNN_B200_CLU6"))
             if (std::atoi(c6) == 0) e->clu6_max = 0;
+    }
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_clu8<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrClu8Smem)));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_clu8<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BrClu8Smem)));
+    {  // co-resident 8-CTA clusters: levels of at most that many bootstraps use the bin-split kernel
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(kClu8 * 32);
+        cfg.blockDim = dim3(192);
+        cfg.dynamicSmemBytes = sizeof(BrClu8Smem);
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, k_blind_rotate_u2_clu8<false>, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            ncl = 0;
+        }
+        e->clu8_max = ncl;
+        if (const char *c8 = std::getenv("HEBNN_B200_CLU8"))
+            if (std::atoi(c8) == 0) e->clu8_max = 0;
     }
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(BrSmemU2<kBrGates>)));

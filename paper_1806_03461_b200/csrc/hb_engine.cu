@@ -48,7 +48,7 @@ namespace {
 #include "hb_br_cggi.cuh"
 #include "hb_br_u2.cuh"
 #include "hb_br_clu6.cuh"
-#include "hb_br_clu8.cuh"
+#include "hb_br_binsplit.cuh"
 #include "hb_ks.cuh"
 
 }  // namespace
@@ -103,7 +103,8 @@ struct hb_engine {
     size_t max_work = kMaxWorkPerLaunch;  // HEBNN_B200_MAX_WORK overrides (tests)
     bool latency_mode = true;             // HEBNN_B200_LATENCY_MODE=0 disables (A/B tests)
     bool cluster_mode = true;             // 2-CTA clusters for <= #SM/2 key-pair bootstraps (HEBNN_B200_CLUSTER_MODE=0)
-    int clu8_max = 0;                     // co-resident 8-CTA clusters (bin-split lone-level kernel); HEBNN_B200_CLU8=0 off
+    int bs8_max = 0;                      // co-resident 8-CTA bin-split clusters (lone levels); HEBNN_B200_BINSPLIT=0 off
+    int bs4_max = 0;                      // co-resident 4-CTA bin-split clusters
     int clu6_max = 0;                     // co-resident 6-CTA clusters (0: kernel unavailable); HEBNN_B200_CLU6=0 off
     bool split_waves = true;              // wide levels: full 4-bootstrap waves + a faster remainder kernel
                                           // (HEBNN_B200_SPLIT_WAVES=0 off)
@@ -261,14 +262,22 @@ int launch_br_auto(hb_engine *e, const BrArgs &a0, int force_g = 0) {
     const int gsel = force_g ? force_g
                              : (cnt <= sms ? 1 : (cnt <= 2u * sms ? 2 : (cnt <= 3u * sms && e->unroll == 2 ? 3 : kBrGates)));
     if (e->unroll == 2) {
-        if (!force_g && e->latency_mode && e->cluster_mode && cnt <= (uint32_t)e->clu8_max) {
-            k_blind_rotate_u2_clu8<kDebug><<<kClu8 * cnt, 192, sizeof(BrClu8Smem), e->stream>>>(a);
+        if (!force_g && e->latency_mode && e->cluster_mode && cnt <= (uint32_t)e->bs8_max) {
+            k_blind_rotate_u2_binsplit<8, kDebug><<<8 * cnt, 192, sizeof(BrBsSmem<8>), e->stream>>>(a);
             HB_CUDA_TRY(cudaGetLastError());
             e->n_launch++;
             return HB_OK;
         }
         if (!force_g && e->latency_mode && e->cluster_mode && cnt <= (uint32_t)e->clu6_max) {
             k_blind_rotate_u2_clu6<kDebug><<<kClu6 * cnt, 192, sizeof(BrClu6Smem), e->stream>>>(a);
+            HB_CUDA_TRY(cudaGetLastError());
+            e->n_launch++;
+            return HB_OK;
+        }
+        // 4-CTA bin split: 1.21 ms for <= ~32, behind the 6-CTA row split (1.06 ms) but ahead of
+        // the 2-CTA kernel (1.39 ms)
+        if (!force_g && e->latency_mode && e->cluster_mode && cnt <= (uint32_t)e->bs4_max) {
+            k_blind_rotate_u2_binsplit<4, kDebug><<<4 * cnt, 192, sizeof(BrBsSmem<4>), e->stream>>>(a);
             HB_CUDA_TRY(cudaGetLastError());
             e->n_launch++;
             return HB_OK;
@@ -455,23 +464,34 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
         if (const char *c6 = std::getenv("HEBNN_B200_CLU6"))
             if (std::atoi(c6) == 0) e->clu6_max = 0;
     }
-    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_clu8<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(BrClu8Smem)));
-    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_clu8<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(BrClu8Smem)));
-    {  // co-resident 8-CTA clusters: levels of at most that many bootstraps use the bin-split kernel
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(kClu8 * 32);
-        cfg.blockDim = dim3(192);
-        cfg.dynamicSmemBytes = sizeof(BrClu8Smem);
-        int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, k_blind_rotate_u2_clu8<false>, &cfg) != cudaSuccess) {
-            cudaGetLastError();
-            ncl = 0;
+    {  // bin-split latency kernels: as many clusters as fit at once (GPC-limited)
+        auto setup = [&](auto kern, auto kdbg, size_t smem, int csize, int *max_out) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+                cudaFuncSetAttribute(kdbg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+                cudaGetLastError();
+                *max_out = 0;
+                return;
+            }
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(csize * 32);
+            cfg.blockDim = dim3(192);
+            cfg.dynamicSmemBytes = smem;
+            int ncl = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess) {
+                cudaGetLastError();
+                ncl = 0;
+            }
+            *max_out = ncl;
+        };
+        setup(k_blind_rotate_u2_binsplit<8, false>, k_blind_rotate_u2_binsplit<8, true>, sizeof(BrBsSmem<8>), 8,
+              &e->bs8_max);
+        setup(k_blind_rotate_u2_binsplit<4, false>, k_blind_rotate_u2_binsplit<4, true>, sizeof(BrBsSmem<4>), 4,
+              &e->bs4_max);
+        if (const char *bs = std::getenv("HEBNN_B200_BINSPLIT")) {
+            const int v = std::atoi(bs);
+            if (v == 0 || v == 4) e->bs8_max = 0;  // 4: only the 4-CTA kernel (A/B)
+            if (v == 0 || v == 8) e->bs4_max = 0;
         }
-        e->clu8_max = ncl;
-        if (const char *c8 = std::getenv("HEBNN_B200_CLU8"))
-            if (std::atoi(c8) == 0) e->clu8_max = 0;
     }
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(BrSmemU2<kBrGates>)));

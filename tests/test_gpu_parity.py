@@ -197,14 +197,16 @@ np.save(sys.argv[1], eng.download(2 * n, n))
     assert np.array_equal(outs[0], outs[1])
 
 
-@pytest.mark.parametrize("n", [1, 5, 20, 100, 200, 400, 700])
+@pytest.mark.parametrize("n", [1, 5, 12, 20, 30, 100, 200, 400, 700])
 def test_narrow_level_kernels_agree(n):
-    """Levels of <= #clusters of 6 CTAs, <= #SM/2, <= #SM and <= 2 #SM bootstraps
-    run on the 6-CTA cluster kernel (key pairs), the 2-CTA cluster kernel, the
-    latency kernel or 1-2 bootstraps per CTA; every choice must give the same
-    ciphertexts (both key layouts), and the first one equals the oracle's.
-    400 runs on 3-bootstrap CTAs, 700 as one full wave of 4-bootstrap CTAs plus
-    a 3-bootstrap remainder launch (split waves) or two 4-bootstrap waves."""
+    """Narrow key-pair levels run, by width, on the 8-CTA bin-split kernel, the
+    6-CTA row-split cluster kernel, the 4-CTA bin-split kernel, the 2-CTA
+    cluster kernel, the latency kernel or 1-3 bootstraps per CTA; switching
+    the narrower kernels off moves a level to the next one.  Every choice must
+    give the same ciphertexts (both key layouts), and the default equals the
+    oracle's.  400 runs on 3-bootstrap CTAs, 700 as one full wave of
+    4-bootstrap CTAs plus a 3-bootstrap remainder launch (split waves) or two
+    4-bootstrap waves."""
     import os
     import subprocess
     import sys
@@ -234,10 +236,11 @@ np.save(sys.argv[1], eng.download(3 * n, n))
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     for unroll in (2, 1):
         outs = []
-        for lat, clu, c6, sw in (("1", "1", "1", "1"), ("1", "1", "0", "0"), ("1", "0", "0", "0"), ("0", "0", "0", "0")):
-            path = f"/tmp/hb_narrow_{n}_{unroll}_{lat}{clu}{c6}{sw}.npy"
-            env = dict(os.environ, HEBNN_B200_LATENCY_MODE=lat, HEBNN_B200_CLUSTER_MODE=clu, HEBNN_B200_CLU6=c6,
-                       HEBNN_B200_SPLIT_WAVES=sw)
+        for lat, clu, bs, c6, sw in (("1", "1", "1", "1", "1"), ("1", "1", "0", "1", "1"), ("1", "1", "0", "0", "0"),
+                                     ("1", "0", "0", "0", "0"), ("0", "0", "0", "0", "0")):
+            path = f"/tmp/hb_narrow_{n}_{unroll}_{lat}{clu}{bs}{c6}{sw}.npy"
+            env = dict(os.environ, HEBNN_B200_LATENCY_MODE=lat, HEBNN_B200_CLUSTER_MODE=clu, HEBNN_B200_BINSPLIT=bs,
+                       HEBNN_B200_CLU6=c6, HEBNN_B200_SPLIT_WAVES=sw)
             subprocess.run([sys.executable, "-c", code, path, str(n), str(unroll)], check=True, cwd=root, env=env)
             outs.append(np.load(path))
         for k in range(1, len(outs)):

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Usage: scripts/profile_round.sh <tag>   (run under gpurun; results in gpurun_out/<tag>/)
 # bench line, ncu launch list of the bench step, ncu --set full of the dominant kernels
-# (blind rotation, key switch) and of the lone-level 6-CTA cluster kernel.
+# (blind rotation, key switch) and of the lone-level 8-CTA bin-split kernel.
 set -u
 TAG=${1:-prof}
 OUT=gpurun_out/$TAG
@@ -13,6 +13,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
 $CMD > $OUT/plain2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_blind_rotate -s 3 -c 1 -o $OUT/k_blind_rotate $CMD > $OUT/ncu_br.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_keyswitch -s 3 -c 1 -o $OUT/k_keyswitch $CMD > $OUT/ncu_ks.log 2>&1
-python scripts/clu6_check.py > $OUT/clu6_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_blind_rotate_u2_clu6 -s 2 -c 1 -o $OUT/k_clu6 python scripts/clu6_check.py > $OUT/ncu_clu6.log 2>&1
+python scripts/narrow_levels.py 1 > $OUT/binsplit_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_blind_rotate_u2_binsplit -s 2 -c 1 -o $OUT/k_binsplit python scripts/narrow_levels.py 1 > $OUT/ncu_binsplit.log 2>&1
 ls -la $OUT

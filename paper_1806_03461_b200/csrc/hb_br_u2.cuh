@@ -322,12 +322,15 @@ __global__ void __launch_bounds__(u2_threads<G, WS>(), MB) k_blind_rotate_u2(con
 #pragma unroll
                             for (int h = 0; h < 2; h++) {
                                 const double2 *bk = sm.bk[sl[2 * c + h]];
+                                // HB_EXP_NO_BK_LDS (timing only, wrong results): one BK value per
+                                // thread and stage, i.e. 1/8 of the BK shared-memory loads
+                                const int kb = HB_EXP_NO_BK_LDS ? t : k;
                                 if (c == 0) {
-                                    C[h][0] = cmul(Fm[c][hi], bk[k]);
-                                    C[h][1] = cmul(Fm[c][hi], bk[kNH + k]);
+                                    C[h][0] = cmul(Fm[c][hi], bk[kb]);
+                                    C[h][1] = cmul(Fm[c][hi], bk[kNH + kb]);
                                 } else {
-                                    cmac(C[h][0], Fm[c][hi], bk[k]);
-                                    cmac(C[h][1], Fm[c][hi], bk[kNH + k]);
+                                    cmac(C[h][0], Fm[c][hi], bk[kb]);
+                                    cmac(C[h][1], Fm[c][hi], bk[kNH + kb]);
                                 }
                             }
                         }

@@ -70,6 +70,15 @@ struct hb_engine {
     cudaEvent_t ev_compute = nullptr;     // compute point an async download waits on
     cudaEvent_t ev_prev_level = nullptr;  // compute stream before the most recent level
     cudaEvent_t ev_download = nullptr;    // last async download (pool writers wait on it: no WAR)
+    // slot ranges [lo, hi) of the async downloads that may still be reading the pool, each with
+    // the d2h-stream event recorded after it; writers wait only for the ones they overlap
+    // (older entries are folded into [old_lo, old_hi), fenced by the oldest kept event: the
+    // d2h stream is in order)
+    static constexpr int kDl = 8;
+    cudaEvent_t ev_dl[kDl]{};
+    size_t dl_lo[kDl]{}, dl_hi[kDl]{};
+    int n_dl = 0, dl_head = 0;            // live entries, ring index of the oldest
+    size_t old_lo = 0, old_hi = 0;        // folded ranges (empty when old_lo >= old_hi)
     bool pending_upload = false;
     bool pending_download = false;
     double2 *d_W = nullptr, *d_TW = nullptr, *d_PSI = nullptr;
@@ -381,6 +390,7 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
     HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_compute, cudaEventDisableTiming));
     HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_prev_level, cudaEventDisableTiming));
     HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_download, cudaEventDisableTiming));
+    for (int i = 0; i < hb_engine::kDl; i++) HB_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_dl[i], cudaEventDisableTiming));
     HB_CUDA_TRY(cudaEventRecord(e->ev_prev_level, e->stream));
     HB_CUDA_TRY(cudaEventRecord(e->ev_stage, e->stream));
 
@@ -576,6 +586,8 @@ int hb_engine_destroy(hb_engine *e) {
         }
     for (cudaEvent_t ev : {e->ev_upload, e->ev_compute, e->ev_prev_level, e->ev_download})
         if (ev) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : e->ev_dl)
+        if (ev) cudaEventDestroy(ev);
     if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
     return HB_OK;
@@ -587,7 +599,43 @@ int hb_engine_destroy(hb_engine *e) {
 static int order_after_downloads(hb_engine *e, cudaStream_t st) {
     if (e->pending_download) {
         HB_CUDA_TRY(cudaStreamWaitEvent(st, e->ev_download, 0));
-        if (st == e->stream) e->pending_download = false;  // later stream-ordered writers inherit it
+        if (st == e->stream) {  // later stream-ordered writers inherit it
+            e->pending_download = false;
+            e->n_dl = 0;
+            e->old_lo = e->old_hi = 0;
+        }
+    }
+    return HB_OK;
+}
+
+// The same fence for a writer of physical pool slots [lo, hi) only: it waits for the
+// pending downloads that read any of those slots (a double-buffered client's upload of
+// step k + 1 and the key switch of level k + 1 write the other slot region than the
+// download of step k, so they no longer wait for it).  Completed entries are dropped.
+static int order_after_downloads_range(hb_engine *e, cudaStream_t st, size_t lo, size_t hi) {
+    if (!e->pending_download) return HB_OK;
+    if (lo >= hi) return HB_OK;
+    // drop finished downloads from the head (oldest first)
+    while (e->n_dl > 0 && cudaEventQuery(e->ev_dl[e->dl_head]) == cudaSuccess) {
+        e->dl_head = (e->dl_head + 1) % hb_engine::kDl;
+        e->n_dl--;
+        e->old_lo = e->old_hi = 0;  // everything older than the new head completed too
+    }
+    cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error here
+    if (e->n_dl == 0) {
+        e->pending_download = false;
+        return HB_OK;
+    }
+    const bool old_hit = e->old_lo < e->old_hi && lo < e->old_hi && e->old_lo < hi;
+    int last_hit = -1;  // the newest overlapping entry (waiting on it covers all older ones)
+    for (int k = 0; k < e->n_dl; k++) {
+        const int i = (e->dl_head + k) % hb_engine::kDl;
+        if (lo < e->dl_hi[i] && e->dl_lo[i] < hi) last_hit = i;
+    }
+    if (last_hit >= 0) {
+        HB_CUDA_TRY(cudaStreamWaitEvent(st, e->ev_dl[last_hit], 0));
+    } else if (old_hit) {
+        HB_CUDA_TRY(cudaStreamWaitEvent(st, e->ev_dl[e->dl_head], 0));
     }
     return HB_OK;
 }
@@ -754,6 +802,7 @@ int hb_run_gates(hb_engine *e, const hb_gate *gates, size_t n, uint32_t lanes) {
 static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_t lanes) {
     // expand records into blind-rotation and key-switch work items
     size_t nbr = 0, nha = 0;
+    size_t dst_lo = SIZE_MAX, dst_hi = 0;  // slots the key switch writes
     for (size_t i = 0; i < n; i++) {
         const hb_gate &g = gates[i];
         if (g.kind != HB_GATE_LIN2 && g.kind != HB_GATE_MUX && g.kind != HB_GATE_LIN3 && g.kind != HB_GATE_HA) {
@@ -771,6 +820,12 @@ static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_
             return HB_EINVAL;
         }
         nbr += (g.kind == HB_GATE_MUX) ? 2 : 1;
+        dst_lo = std::min(dst_lo, (size_t)g.dst);
+        dst_hi = std::max(dst_hi, (size_t)g.dst + 1);
+        if (g.kind == HB_GATE_HA) {  // the XOR output
+            dst_lo = std::min(dst_lo, (size_t)g.src_c);
+            dst_hi = std::max(dst_hi, (size_t)g.src_c + 1);
+        }
     }
     // big-LWE rows: one per blind rotation, then one per HA second extraction
     const size_t nks = n + nha, nbig = nbr + nha;
@@ -841,8 +896,9 @@ static int run_gates_chunk(hb_engine *e, const hb_gate *gates, size_t n, uint32_
     k.pool = e->d_pool;
     k.pool_stride = e->pool_stride;
     k.n = e->p.n;
-    // the key switch writes pool slots: after any async download still reading them
-    if ((rc = order_after_downloads(e, e->stream))) return rc;
+    // the key switch writes pool slots [dst_lo, dst_hi) x lanes: after any async download
+    // still reading them
+    if ((rc = order_after_downloads_range(e, e->stream, dst_lo * lanes, dst_hi * lanes))) return rc;
     if ((rc = launch_ks(e, k))) return rc;
     HB_CUDA_TRY(cudaEventRecord(e->ev[2], e->stream));
     e->n_br += nbr * lanes;
@@ -868,7 +924,7 @@ int hb_pool_upload_async(hb_engine *e, size_t first, size_t count, const uint32_
     HB_CUDA_TRY(cudaSetDevice(e->device));
     // may overlap the most recently issued level, never an earlier one (double buffering)
     HB_CUDA_TRY(cudaStreamWaitEvent(e->h2d_stream, e->ev_prev_level, 0));
-    if (e->pending_download) HB_CUDA_TRY(cudaStreamWaitEvent(e->h2d_stream, e->ev_download, 0));
+    if (int rc = order_after_downloads_range(e, e->h2d_stream, first, first + count)) return rc;
     HB_CUDA_TRY(cudaMemcpy2DAsync(e->d_pool + first * e->pool_stride, e->pool_stride * 4, host, host_stride * 4,
                                   (size_t)(e->p.n + 1) * 4, count, cudaMemcpyHostToDevice, e->h2d_stream));
     HB_CUDA_TRY(cudaEventRecord(e->ev_upload, e->h2d_stream));
@@ -889,6 +945,23 @@ int hb_pool_download_async(hb_engine *e, size_t first, size_t count, uint32_t *h
     HB_CUDA_TRY(cudaMemcpy2DAsync(host, host_stride * 4, e->d_pool + first * e->pool_stride, e->pool_stride * 4,
                                   (size_t)(e->p.n + 1) * 4, count, cudaMemcpyDeviceToHost, e->d2h_stream));
     HB_CUDA_TRY(cudaEventRecord(e->ev_download, e->d2h_stream));
+    if (e->n_dl == hb_engine::kDl) {  // fold the oldest entry into the catch-all range
+        const int i = e->dl_head;
+        if (e->old_lo >= e->old_hi) {
+            e->old_lo = e->dl_lo[i];
+            e->old_hi = e->dl_hi[i];
+        } else {
+            e->old_lo = std::min(e->old_lo, e->dl_lo[i]);
+            e->old_hi = std::max(e->old_hi, e->dl_hi[i]);
+        }
+        e->dl_head = (e->dl_head + 1) % hb_engine::kDl;
+        e->n_dl--;
+    }
+    const int slot = (e->dl_head + e->n_dl) % hb_engine::kDl;
+    HB_CUDA_TRY(cudaEventRecord(e->ev_dl[slot], e->d2h_stream));
+    e->dl_lo[slot] = first;
+    e->dl_hi[slot] = first + count;
+    e->n_dl++;
     e->pending_download = true;
     return HB_OK;
 }

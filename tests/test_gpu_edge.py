@@ -186,3 +186,49 @@ def test_async_download_is_not_overtaken_by_later_levels(keys):
         got = keys.decrypt(h_out[k][span - g:])
         assert np.array_equal(got, bits[k][:g] & bits[k][g:]), k
     eng.close()
+
+
+@pytest.mark.gpu
+def test_async_download_fences_are_range_aware_and_survive_many_downloads(keys):
+    """More async downloads than the engine tracks individually (8): the older
+    ones are folded into one fenced range, and a later level rewriting the slots
+    of the FIRST download must still wait for it; levels writing other slots do
+    not (their results are checked too)."""
+    import torch
+
+    eng = tfhe.Engine(keys)
+    g, span, words = 8, 8192, keys.params.n + 1
+    steps = 12
+    rng = np.random.default_rng(33)
+    bits = [rng.integers(0, 2, 2 * g).astype(np.uint8) for _ in range(steps + 1)]
+    region = span + 2 * g
+    eng.reserve((steps + 1) * region)
+    h_out = [torch.empty((span, words), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+             for _ in range(steps)]
+    c0, al, be = tfhe.GATE_LIN["AND"]
+
+    h_in = [torch.empty((2 * g, words), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+            for _ in range(steps + 1)]
+    for k in range(steps + 1):
+        h_in[k][:] = keys.encrypt(bits[k], seed=60 + k)
+
+    def level(r, k):
+        base = r * region
+        eng.upload_async(base + span, h_in[k])  # range-aware fences only (no full fence)
+        rc = tfhe.gate_records(g)
+        rc["dst"] = base + span - g + np.arange(g)
+        rc["src_a"], rc["src_b"] = base + span + np.arange(g), base + span + g + np.arange(g)
+        rc["c0"], rc["alpha"], rc["beta"] = c0, al, be
+        eng.run_gates(rc)
+
+    for k in range(steps):
+        level(k, k)
+        eng.download_async(k * region, h_out[k])
+    level(0, steps)  # rewrites the outputs of the first (folded) download
+    eng.sync()
+    for k in range(steps):
+        got = keys.decrypt(h_out[k][span - g:])
+        assert np.array_equal(got, bits[k][:g] & bits[k][g:]), k
+    now = keys.decrypt(eng.download(span - g, g))
+    assert np.array_equal(now, bits[steps][:g] & bits[steps][g:])
+    eng.close()

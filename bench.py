@@ -17,9 +17,12 @@ reduced with MAX over ranks.
 input ciphertext batches from pinned memory, the gate records, the level, and
 D2H of the 4,096 output ciphertexts, all inside the timed region.
 
-`--impl reference` times the CPU path (the exact-integer C oracle, run with
-all host threads) on a bounded sample of the same workload; the reference
-package itself has no ciphertext arithmetic (it simulates in plaintext).
+`--impl reference` times the CPU path on a bounded sample of the same
+workload with all host threads: the vectorised FP64-FFT CPU port of the same
+gate bootstrap (oracle/tfhe_cpu_fft.c, eight gates per SIMD register, checked
+bit-for-bit against the exact-integer oracle); the exact Goldilocks-NTT oracle's
+own rate is reported beside it.  The reference package itself has no
+ciphertext arithmetic (it simulates in plaintext).
 """
 
 from __future__ import annotations
@@ -242,13 +245,14 @@ class ClockSampler:
 # CPU baseline (oracle) — the only place bench.py executes oracle/
 # ---------------------------------------------------------------------------
 
-def cpu_nand_sample(seed, gates, threads):
-    """Time `gates` NANDs on the exact CPU oracle with `threads` pthreads."""
+def cpu_nand_sample(seed, gates, threads, exact=False):
+    """Time `gates` NANDs on the CPU with `threads` pthreads: the FP64-FFT port
+    (default, the fast CPU baseline) or the exact-integer oracle."""
     from oracle import oracle as O
 
     p = O.default_params()
     keys = O.Keys(p, seed)
-    ctx = O.Context(p, keys)
+    ctx = O.Context(p, keys) if exact else O.FftContext(p, keys)
     rng = np.random.default_rng(seed)
     a = rng.integers(0, 2, gates).astype(np.uint8)
     b = rng.integers(0, 2, gates).astype(np.uint8)
@@ -287,22 +291,29 @@ def run_reference(args, dist):
     if dist.rank != 0:
         return None
     threads = os.cpu_count() or 1
-    sample = 24 * threads  # ~2 s of wall time per step (~30 core-seconds)
+    sample = 256 * threads  # ~2 s of wall time per step (~30 core-seconds)
     step, ok = cpu_nand_sample(args.seed, sample, threads)
     for _ in range(args.warmup):
         step()
     times = [step() for _ in range(args.steps)]
-    assert ok(), "CPU oracle produced wrong NAND outputs"
+    assert ok(), "CPU FFT port produced wrong NAND outputs"
     value = sample * len(times) / sum(times)
+    xstep, xok = cpu_nand_sample(args.seed, 16 * threads, threads, exact=True)
+    xdt = xstep()
+    assert xok(), "CPU oracle produced wrong NAND outputs"
     line = {
         "impl": "reference",
         "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32 torus (exact integer NTT)", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32 torus; FP64 FFT on the host (bit-exact vs integer oracle)",
+        "data": "synthetic",
         "config": {"workload": WORKLOAD, "gates_per_step": sample, "sample_of": args.gates},
         "cpu_baseline": {"value": value, "unit": "gates/s", "cores": threads, "kind": "port",
                          "sample": f"{sample} NAND gates per step on {threads} threads ({cpu_model()}); "
-                                   "exact-integer CGGI oracle/tfhe_oracle.c (reference has no crypto)"},
+                                   "FP64-FFT CPU port oracle/tfhe_cpu_fft.c, 8 gates per SIMD register "
+                                   "(reference has no crypto)",
+                         "exact_oracle_value": 16 * threads / xdt,
+                         "exact_oracle_note": "exact-integer Goldilocks-NTT oracle/tfhe_oracle.c, same threads"},
         "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     return line
@@ -665,15 +676,22 @@ def run_ours(args, dist):
             line["nccl"] = {"backend": dist.backend, "log_lines": lines}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        sample = 128 * threads  # ~10 s of wall time (~150 core-seconds) of exact CGGI on the host
+        sample = 512 * threads  # ~5 s of wall time (~80 core-seconds) of FP64-FFT CGGI on the host
         step, ok = cpu_nand_sample(args.seed, sample, threads)
+        step()  # warm the caches and the threads
         dt = step()
         line["cpu_baseline"] = {"value": sample / dt, "unit": "gates/s", "cores": threads, "kind": "port",
                                 "sample": f"{sample} NAND gates on {threads} threads ({cpu_model()}), "
-                                          f"{dt:.1f} s; exact-integer CGGI oracle (reference has no crypto)",
+                                          f"{dt:.1f} s; FP64-FFT CPU port oracle/tfhe_cpu_fft.c, 8 gates per SIMD "
+                                          "register, bit-exact vs the integer oracle (reference has no crypto)",
                                 "correct": ok()}
-        step1, _ = cpu_nand_sample(args.seed + 1, 32, 1)
-        line["cpu_baseline"]["single_thread_value"] = 32 / step1()
+        step1, _ = cpu_nand_sample(args.seed + 1, 64, 1)
+        line["cpu_baseline"]["single_thread_value"] = 64 / step1()
+        xstep, xok = cpu_nand_sample(args.seed, 16 * threads, threads, exact=True)
+        xdt = xstep()
+        line["cpu_baseline"]["exact_oracle_value"] = 16 * threads / xdt
+        line["cpu_baseline"]["exact_oracle_note"] = ("exact-integer Goldilocks-NTT oracle/tfhe_oracle.c, "
+                                                     f"{16 * threads} gates on {threads} threads; correct={xok()}")
     eng.close()
     return line
 

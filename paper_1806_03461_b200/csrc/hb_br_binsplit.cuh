@@ -28,12 +28,12 @@
 //      update their own copy of ACC_o: no ACC broadcast hop (an owner-only
 //      inverse plus broadcast measured 0.75 vs 0.68-0.73 ms for C = 8)
 // Each CTA streams only its bins of the pair's 18 BK stages (36 bulk copies
-// of MPC KiB per pair), double-buffered two pairs ahead.  The spectrum and
-// output receive buffers are single: pair pm + 1's spectra can only be sent
-// after every inverter updated its ACC from pair pm's outputs (which it read
-// first), and pair pm + 1's outputs only after every CTA's MAC read pair
-// pm's spectra — the dependency chain itself orders the reuse, so the loop
-// has no cluster barrier (phases alternate per pair).  Same
+// of MPC KiB per pair): C = 8 double-buffers them two pairs ahead; C = 4 (twice
+// the bins, no room for two buffers) refills its single buffer for pair pm + 1
+// as soon as the MAC of pair pm has read it.  Receive buffers are
+// double-buffered by pair parity; their reuse two pairs later is ordered by
+// the dependency chain itself (no CTA can send for pair pm + 2 before every
+// inverter consumed pair pm + 1), so the loop has no cluster barrier.  Same
 // arithmetic per (row, component, bin) as the other key-pair kernels; the
 // summation order differs, so bit-exactness rests on the FFT rounding margin
 // (tests/test_gpu_parity.py narrow levels).
@@ -45,7 +45,7 @@ struct BsCfg {
     static constexpr int kMPC = 8 / C;                        // bin columns per CTA
     static constexpr int kRowCtas = C == 8 ? 6 : 3;           // CTAs holding digit rows
     static constexpr int kRPC = kRows / kRowCtas;             // digit rows per row CTA
-    static constexpr int kBkBufs = 2;                         // BK slice buffers (two pairs ahead)
+    static constexpr int kBkBufs = C == 8 ? 2 : 1;            // BK slice buffers
     static constexpr uint32_t kBkBytes = kStagesPerPair * 2 * kMPC * kBsColBytes;
     static constexpr uint32_t kSpecBytes = kRows * kMPC * kBsColBytes;
 };
@@ -54,15 +54,15 @@ template <int C>
 struct BrBsSmem {
     using K = BsCfg<C>;
     double2 bk[K::kBkBufs][kStagesPerPair][2][K::kMPC * 64];  // [buf][stage][poly][m_local * 64 + t]
-    double2 spec[kRows][K::kMPC * 64];                        // [row][m_local * 64 + t]
-    double2 outp[2][8][64];                                   // [poly][m][t]
+    double2 spec[2][kRows][K::kMPC * 64];                     // [pair parity][row][m_local * 64 + t]
+    double2 outp[2][2][8][64];                                // [pair parity][poly][m][t]
     double2 xch[2][kXchStride];                               // group g's FFT exchange
     uint32_t acc[2][kN];                                      // ACC_0 / ACC_1 (the polynomials of this CTA's rows)
     uint16_t bar[kMaxLweN + 1];
     TwSeeds tws[64];
     uint64_t bk_full[K::kBkBufs];
-    uint64_t spec_full;                                       // phase pm & 1: pair pm's spectra landed
-    uint64_t out_full;                                        // phase pm & 1: pair pm's outputs landed
+    uint64_t spec_full[2];
+    uint64_t out_full[2];
 };
 
 // does CTA r hold a digit row of polynomial q?
@@ -121,16 +121,18 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(192, 1) k_blind_rota
     }
     if (threadIdx.x == 0) {
         for (int b = 0; b < K::kBkBufs; b++) mbar_init(&sm.bk_full[b], 1);
-        mbar_init(&sm.spec_full, 1);
-        mbar_init(&sm.out_full, 1);
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&sm.spec_full[b], 1);
+            mbar_init(&sm.out_full[b], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (producer) {
         for (int pm = 0; pm < K::kBkBufs && pm < pairs; pm++) issue_bk(pm);
-        if (pairs > 0) {
-            mbar_arrive_expect_tx(&sm.spec_full, K::kSpecBytes);
-            if (n_inv) mbar_arrive_expect_tx(&sm.out_full, out_bytes);
+        for (int pm = 0; pm < 2 && pm < pairs; pm++) {
+            mbar_arrive_expect_tx(&sm.spec_full[pm], K::kSpecBytes);
+            if (n_inv) mbar_arrive_expect_tx(&sm.out_full[pm], out_bytes);
         }
     }
     k1_modswitch(args, e, sm.bar, threadIdx.x, 192);  // K1 (every CTA needs the rotation exponents)
@@ -139,10 +141,10 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(192, 1) k_blind_rota
     // every CTA's barriers are initialised and armed, every ACC copy is set
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 
-    const uint32_t spec_off = smem_addr(&sm.spec[0][0]);
-    const uint32_t out_off = smem_addr(&sm.outp[0][0][0]);
-    const uint32_t spec_bar_off = smem_addr(&sm.spec_full);
-    const uint32_t out_bar_off = smem_addr(&sm.out_full);
+    const uint32_t spec_off = smem_addr(&sm.spec[0][0][0]);
+    const uint32_t out_off = smem_addr(&sm.outp[0][0][0][0]);
+    const uint32_t spec_bar_off = smem_addr(&sm.spec_full[0]);
+    const uint32_t out_bar_off = smem_addr(&sm.out_full[0]);
     double max_err = 0.0;
     // F_c at this thread's MAC bins k = t + 64 m: psi^{e_c (4k+1)}, one pair ahead
     double2 base[K::kMPC][3];
@@ -172,12 +174,12 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(192, 1) k_blind_rota
                                        small_int_to_double(gadget_digit(P[j + kNH], p_row)));
             }
             nega_fft_fwd_n<1, true>(x, sm.xch[grp], t, sm.tws[t], bar_id);
-            const uint32_t lbar = spec_bar_off;
+            const uint32_t lbar = spec_bar_off + (uint32_t)(b * 8);
 #pragma unroll
             for (int m = 0; m < 8; m++) {
                 const uint32_t dst = (uint32_t)(m / K::kMPC);
                 const int ml = m % K::kMPC;
-                const uint32_t loc = spec_off + (uint32_t)(((my_row * K::kMPC + ml) * 64 + t) * 16);
+                const uint32_t loc = spec_off + (uint32_t)((((b * kRows + my_row) * K::kMPC + ml) * 64 + t) * 16);
                 st_async_f64x2(mapa_u32(loc, dst), x[0][m], mapa_u32(lbar, dst));
             }
         }
@@ -189,7 +191,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(192, 1) k_blind_rota
             const int bb = K::kBkBufs == 2 ? b : 0;
             const uint32_t bk_par = K::kBkBufs == 2 ? (uint32_t)((pm >> 1) & 1) : (uint32_t)(pm & 1);
             mbar_wait(&sm.bk_full[bb], bk_par);
-            mbar_wait_cluster(&sm.spec_full, pm & 1);
+            mbar_wait_cluster(&sm.spec_full[b], (pm >> 1) & 1);
 #pragma unroll
             for (int ml = 0; ml < K::kMPC; ml++) {
                 double2 F[3];
@@ -203,15 +205,16 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(192, 1) k_blind_rota
                     double2 Cc = cmul(F[0], sm.bk[bb][rs][o][k]);
                     cmac(Cc, F[1], sm.bk[bb][rs + 2][o][k]);
                     cmac(Cc, F[2], sm.bk[bb][rs + 4][o][k]);
-                    cmac(acc_o, sm.spec[r][k], Cc);
+                    cmac(acc_o, sm.spec[b][r][k], Cc);
                 }
                 // to every CTA inverse-transforming polynomial o, slot [b][o][m][t]
                 const int m = K::kMPC * rank + ml;
-                const uint32_t loc = out_off + (uint32_t)(((o * 8 + m) * 64 + t) * 16);
+                const uint32_t loc = out_off + (uint32_t)((((b * 2 + o) * 8 + m) * 64 + t) * 16);
 #pragma unroll
                 for (int d = 0; d < K::kRowCtas; d++) {
                     if (!bs_has_poly<C>(d, o)) continue;
-                    st_async_f64x2(mapa_u32(loc, (uint32_t)d), acc_o, mapa_u32(out_bar_off, (uint32_t)d));
+                    st_async_f64x2(mapa_u32(loc, (uint32_t)d), acc_o,
+                                   mapa_u32(out_bar_off + (uint32_t)(b * 8), (uint32_t)d));
                 }
             }
             if (pm + 1 < pairs) {
@@ -227,16 +230,16 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(192, 1) k_blind_rota
         //    producer's arrival)
         asm volatile("bar.sync %0, %1;" ::"r"(5), "r"(192) : "memory");
         if (producer) {
-            if (pm + 1 < pairs) mbar_arrive_expect_tx(&sm.spec_full, K::kSpecBytes);
+            if (pm + 2 < pairs) mbar_arrive_expect_tx(&sm.spec_full[b], K::kSpecBytes);
             if (pm + K::kBkBufs < pairs) issue_bk(pm + K::kBkBufs);
         }
         // 4. inverse groups: output polynomial inv_q -> inverse transform -> this CTA's ACC copy
         if (inv_grp) {
-            mbar_wait_cluster(&sm.out_full, pm & 1);
-            if (grp == 0 && t == 0 && pm + 1 < pairs) mbar_arrive_expect_tx(&sm.out_full, out_bytes);
+            mbar_wait_cluster(&sm.out_full[b], (pm >> 1) & 1);
+            if (grp == 0 && t == 0 && pm + 2 < pairs) mbar_arrive_expect_tx(&sm.out_full[b], out_bytes);
             double2 y[1][8];
 #pragma unroll
-            for (int m = 0; m < 8; m++) y[0][m] = sm.outp[inv_q][m][t];
+            for (int m = 0; m < 8; m++) y[0][m] = sm.outp[b][inv_q][m][t];
             nega_fft_inv_n<1, true>(y, sm.xch[grp], t, sm.tws[t], bar_id);
             uint32_t *P = sm.acc[inv_q];
 #pragma unroll

@@ -28,6 +28,7 @@ ciphertext arithmetic (it simulates in plaintext).
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import re
 import os
@@ -65,7 +66,7 @@ WORKLOAD = "cfg1: 4096 independent bootstrapped NAND gates per GPU (TFHE n=630,N
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--gates", type=int, default=4096)
@@ -193,7 +194,7 @@ class Dist:
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -208,11 +209,17 @@ class ClockSampler:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
 
+    def mark(self):
+        """Start of the timed region: only samples stamped after this are reported (the
+        sampler itself is started before the warm-up so that nvidia-smi is already running)."""
+        self.t_mark = datetime.datetime.now()
+
     def stop(self):
+        t_end = datetime.datetime.now()
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -220,25 +227,37 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-        sm, smax, reasons = [], None, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        t_mark = getattr(self, "t_mark", None)
+        rows = []  # (in the timed window?, sm MHz, max MHz, active reasons)
         with open(self.path) as f:
             for line in f:
                 parts = [p.strip() for p in line.split(",")]
                 if len(parts) < 9:
                     continue
+                inside = True
+                if t_mark is not None:
+                    try:
+                        ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f")
+                        inside = t_mark <= ts <= t_end
+                    except ValueError:
+                        inside = False
                 try:
-                    sm.append(float(parts[1]))
-                    smax = float(parts[2])
+                    rows.append((inside, float(parts[1]), float(parts[2]),
+                                 [nm for nm, v in zip(names, parts[5:9]) if v.lower() == "active"]))
                 except ValueError:
                     continue
-                for nm, v in zip(names, parts[5:9]):
-                    if v.lower() == "active":
-                        reasons.add(nm)
         os.unlink(self.path)
+        timed = [r for r in rows if r[0]]
+        window = "timed region"
+        if not timed:          # clock skew between nvidia-smi's stamps and ours: keep every sample
+            timed, window = rows, "whole run (no sample stamped inside the timed region)"
+        sm = [r[1] for r in timed]
+        smax = timed[-1][2] if timed else None
+        reasons = {nm for r in timed for nm in r[3]}
         loaded = [s for s in sm if s > 500] or sm
         return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "window": window}
 
 
 # ---------------------------------------------------------------------------
@@ -535,14 +554,15 @@ def run_ours(args, dist):
 
     fp64_peak = eng.measure_fp64_peak()
 
+    clocks = ClockSampler(dev)
+    clocks.start()               # before the warm-up: nvidia-smi needs ~0.3 s to come up
     for _ in range(args.warmup):
         eng.run_gates(recs)
         eng.sync()
     eng.sync()
     dist.barrier()
     launches0 = eng.counters()["kernel_launches"]
-    clocks = ClockSampler(dev)
-    clocks.start()
+    clocks.mark()                # samples from here to stop() are the timed region's
     step_ms, br_ms, ks_ms = [], [], []
     for _ in range(args.steps):
         eng.flush_l2()           # cold L2 for every timed step

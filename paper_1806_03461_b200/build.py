@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "libhebnn_b200.so")
 SOURCES = ("hb_host.cpp", "hb_engine.cu")
-HEADERS = ("hb_internal.h", "hb_dev_fft.cuh", "hb_br_cggi.cuh", "hb_br_u2.cuh", "hb_br_u2alt.cuh", "hb_br_clu6.cuh", "hb_br_binsplit.cuh", "hb_ks.cuh")
+HEADERS = ("hb_internal.h", "hb_dev_fft.cuh", "hb_br_cggi.cuh", "hb_br_u2.cuh", "hb_br_clu6.cuh", "hb_br_binsplit.cuh", "hb_ks.cuh")
 
 NVCC_FLAGS = [
     "-O3",

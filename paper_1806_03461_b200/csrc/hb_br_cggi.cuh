@@ -53,7 +53,6 @@ struct BrArgs {
     int32_t n;                // LWE dimension
     uint32_t mu;              // test-vector value (1/8)
     const double2 *bkf;       // [n][6][2][512]
-    const double2 *bkf_blk;   // key pairs: the same values in bin-block order (hb_br_u2alt.cuh), or null
     uint32_t *big;            // [n_work][kBigStride] extracted LWE
     const double2 *W;         // [512] e^{2 pi i e/512}
     const double2 *TW;        // [512] e^{i pi j/1024}

@@ -47,7 +47,6 @@ namespace {
 #include "hb_dev_fft.cuh"
 #include "hb_br_cggi.cuh"
 #include "hb_br_u2.cuh"
-#include "hb_br_u2alt.cuh"
 #include "hb_br_clu6.cuh"
 #include "hb_br_binsplit.cuh"
 #include "hb_ks.cuh"
@@ -85,8 +84,6 @@ struct hb_engine {
     double2 *d_W = nullptr, *d_TW = nullptr, *d_PSI = nullptr;
     int unroll = 1;  // bk_unroll of the loaded key
     double2 *d_bkf = nullptr;
-    double2 *d_bkf_blk = nullptr;  // key pairs: bin-block copy for k_blind_rotate_u2_alt
-    bool u2alt = true;             // full 4-bootstrap waves on the alternating-halves kernel (HEBNN_B200_U2ALT=0: off)
     uint32_t *d_ksk = nullptr;
     uint32_t *d_pool = nullptr;
     size_t pool_cap = 0;
@@ -184,21 +181,6 @@ int launch_br_u2(hb_engine *e, const BrArgs &a) {
     return HB_OK;
 }
 
-// full 4-bootstrap CTAs of the key-pair blind rotation: alternating halves (bin-block BK copy),
-// else the warp-specialised kernel, else the r01 kernel
-template <bool kDebug>
-int launch_br_u2_wide(hb_engine *e, const BrArgs &a) {
-    if (e->u2alt && a.bkf_blk) {
-        const unsigned grid = (a.n_work - a.e0 + kBrGates - 1) / kBrGates;
-        k_blind_rotate_u2_alt<kBrGates, kDebug>
-            <<<grid, u2_threads<kBrGates, true>(), sizeof(BrAltSmem<kBrGates>), e->stream>>>(a);
-        HB_CUDA_TRY(cudaGetLastError());
-        e->n_launch++;
-        return HB_OK;
-    }
-    return e->u2ws ? launch_br_u2<kBrGates, kDebug, kStagesU2, 1, false, true>(e, a) : launch_br_u2<kBrGates, kDebug>(e, a);
-}
-
 template <bool kDebug>
 int launch_br_lat(hb_engine *e, const BrArgs &a) {
     k_blind_rotate_lat<kDebug><<<a.n_work - a.e0, 192, sizeof(BrLatSmem), e->stream>>>(a);
@@ -279,7 +261,8 @@ int launch_br_auto(hb_engine *e, const BrArgs &a0, int force_g = 0) {
         if (cnt > wave && cnt % wave != 0 && cnt % wave <= 3 * sms) {
             BrArgs head = a;
             head.n_work = a.e0 + (cnt / wave) * wave;
-            int rc = launch_br_u2_wide<kDebug>(e, head);
+            int rc = e->u2ws ? launch_br_u2<kBrGates, kDebug, kStagesU2, 1, false, true>(e, head)
+                             : launch_br_u2<kBrGates, kDebug>(e, head);
             if (rc) return rc;
             a.e0 = head.n_work;
         }
@@ -331,7 +314,8 @@ int launch_br_auto(hb_engine *e, const BrArgs &a0, int force_g = 0) {
 #if HB_U2_TMEM
         return launch_br_u2<kBrGates, kDebug, kStagesU2Tmem, 1, true>(e, a);
 #else
-        return launch_br_u2_wide<kDebug>(e, a);
+        if (e->u2ws) return launch_br_u2<kBrGates, kDebug, kStagesU2, 1, false, true>(e, a);
+        return launch_br_u2<kBrGates, kDebug>(e, a);
 #endif
     }
     if (!force_g && gsel == 1 && e->latency_mode) return launch_br_lat<kDebug>(e, a);
@@ -348,7 +332,6 @@ BrArgs br_args(hb_engine *e) {
     a.n = e->p.n;
     a.mu = 1u << 29;
     a.bkf = e->d_bkf;
-    a.bkf_blk = e->d_bkf_blk;
     a.big = e->d_big;
     a.W = e->d_W;
     a.TW = e->d_TW;
@@ -473,11 +456,6 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2<kBrGates, true, kStagesU2, 1, false, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BrSmemU2<kBrGates>)));
     if (const char *uw = std::getenv("HEBNN_B200_U2WS")) e->u2ws = std::atoi(uw) != 0;
-    if (const char *ua = std::getenv("HEBNN_B200_U2ALT")) e->u2alt = std::atoi(ua) != 0;
-    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_alt<kBrGates, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(BrAltSmem<kBrGates>)));
-    HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_alt<kBrGates, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(BrAltSmem<kBrGates>)));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_clu6<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(BrClu6Smem)));
     HB_CUDA_TRY(cudaFuncSetAttribute(k_blind_rotate_u2_clu6<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -571,12 +549,6 @@ int hb_engine_create(int device, const hb_params *p, const uint32_t *bk, const u
     k_bk_to_fourier<<<(unsigned)((npoly + 1) / 2), 128, 0, e->stream>>>(d_bk, e->d_bkf, (int)npoly, e->d_W, e->d_TW,
                                                                          e->unroll);
     HB_CUDA_TRY(cudaGetLastError());
-    if (e->unroll == 2 && e->u2alt) {  // second copy in bin-block order for the alternating-halves kernel
-        const size_t n_elems = npoly * kNH;
-        HB_CUDA_TRY(cudaMalloc(&e->d_bkf_blk, n_elems * sizeof(double2)));
-        k_bkf_to_blocks<<<(unsigned)((n_elems + 255) / 256), 256, 0, e->stream>>>(e->d_bkf, e->d_bkf_blk, n_elems);
-        HB_CUDA_TRY(cudaGetLastError());
-    }
     HB_CUDA_TRY(cudaStreamSynchronize(e->stream));
     cudaFree(d_bk);
 
@@ -598,7 +570,7 @@ int hb_engine_destroy(hb_engine *e) {
     if (!e) return HB_OK;
     cudaSetDevice(e->device);
     if (e->stream) cudaStreamSynchronize(e->stream);
-    for (void *ptr : {(void *)e->d_W, (void *)e->d_TW, (void *)e->d_PSI, (void *)e->d_bkf, (void *)e->d_bkf_blk, (void *)e->d_ksk, (void *)e->d_pool,
+    for (void *ptr : {(void *)e->d_W, (void *)e->d_TW, (void *)e->d_PSI, (void *)e->d_bkf, (void *)e->d_ksk, (void *)e->d_pool,
                       (void *)e->d_big, (void *)e->d_br, (void *)e->d_ks, (void *)e->d_tmp, (void *)e->d_kspart, (void *)e->d_margin,
                       e->d_flush})
         if (ptr) cudaFree(ptr);

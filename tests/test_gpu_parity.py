@@ -236,13 +236,11 @@ np.save(sys.argv[1], eng.download(3 * n, n))
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     for unroll in (2, 1):
         outs = []
-        # last column: the alternating-halves kernel for full 4-bootstrap CTAs (wide levels) on / off
-        for lat, clu, bs, c6, sw, alt in (("1", "1", "1", "1", "1", "1"), ("1", "1", "0", "1", "1", "1"),
-                                          ("1", "1", "0", "0", "0", "1"), ("1", "0", "0", "0", "0", "0"),
-                                          ("0", "0", "0", "0", "0", "1"), ("1", "1", "1", "1", "1", "0")):
-            path = f"/tmp/hb_narrow_{n}_{unroll}_{lat}{clu}{bs}{c6}{sw}{alt}.npy"
+        for lat, clu, bs, c6, sw in (("1", "1", "1", "1", "1"), ("1", "1", "0", "1", "1"), ("1", "1", "0", "0", "0"),
+                                     ("1", "0", "0", "0", "0"), ("0", "0", "0", "0", "0")):
+            path = f"/tmp/hb_narrow_{n}_{unroll}_{lat}{clu}{bs}{c6}{sw}.npy"
             env = dict(os.environ, HEBNN_B200_LATENCY_MODE=lat, HEBNN_B200_CLUSTER_MODE=clu, HEBNN_B200_BINSPLIT=bs,
-                       HEBNN_B200_CLU6=c6, HEBNN_B200_SPLIT_WAVES=sw, HEBNN_B200_U2ALT=alt)
+                       HEBNN_B200_CLU6=c6, HEBNN_B200_SPLIT_WAVES=sw)
             subprocess.run([sys.executable, "-c", code, path, str(n), str(unroll)], check=True, cwd=root, env=env)
             outs.append(np.load(path))
         for k in range(1, len(outs)):

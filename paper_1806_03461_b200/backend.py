@@ -182,12 +182,18 @@ class TfheContext(GateBackend):
               merge with later gates of the same level (the final flush runs
               everything).  A narrow launch costs about as much as a full
               wave, so this keeps streamed launches wide.  0 disables.
+    csa_popcount: opt-in (default: environment HEBNN_B200_CSA_POPCOUNT, else off
+              = the pure drop-in).  Rebinds the
+              reference's `reduce_tree_sum` (popcount.py) so that popcounts of
+              this context's bits are built as carry-save compressor networks
+              (~2n instead of ~3n bootstraps for n bits); decrypted words and
+              counted `GateStats` are unchanged.
     """
 
     _CHUNK = 4096  # logical slots reserved at a time
 
     def __init__(self, seed=0, device=0, lanes=1, enc_seed=None, keys=None, enc_stream=None, stream_at=16384,
-                 stream_min_width=592, fuse_half_adders=True):
+                 stream_min_width=592, fuse_half_adders=True, csa_popcount=None):
         if lanes < 1:
             raise ValueError("lanes must be >= 1")
         self.global_stats = GateStats(label="global")
@@ -217,6 +223,15 @@ class TfheContext(GateBackend):
         self.stream_at = int(stream_at)  # pending gates that start a background flush (0: off)
         self.stream_min_width = int(stream_min_width)
         self.fuse_half_adders = bool(fuse_half_adders)
+        # opt-in: the compiler's popcounts (hebnn.circuits.reduce_tree_sum) run as carry-save
+        # compressor networks built in the DAG (popcount.py); counted stats stay the reference's
+        if csa_popcount is None:
+            csa_popcount = os.environ.get("HEBNN_B200_CSA_POPCOUNT", "0") not in ("", "0")
+        self.csa_popcount = bool(csa_popcount)
+        if self.csa_popcount:
+            from . import popcount
+
+            popcount.install()
         # gates between two streaming checks (a countdown instead of a native call per gate)
         self._tick_every = max(1, min(256, self.stream_at // 8))
         self._tick = self._tick_every
@@ -488,6 +503,38 @@ class TfheContext(GateBackend):
                     self._tick = self._tick_every
                     self._maybe_stream()
             return _Bit(self, r, level)
+
+    # -- carry-save popcount (opt-in, popcount.py) ------------------------------
+
+    def _csa_popcount(self, bits, out_levels):
+        """Handles (LSB first, levels `out_levels`) on the binary digits of the
+        number of true bits, built natively as a compressor network (Dag.csa);
+        None if the network does not have exactly len(out_levels) non-constant
+        digits (duplicate operands), in which case nothing live was created."""
+        refs = np.fromiter((b._value for b in bits), dtype=np.int64, count=len(bits))
+        with self._lock:
+            out = [int(r) for r in self._dag.csa(refs)]
+            handles = [_Bit(self, r, 0) for r in out]  # own the counted handles (dropped on return None)
+            if len(out) != len(out_levels) or any((r >> 1) == 0 for r in out):
+                return None
+            for h, lvl in zip(handles, out_levels):
+                h.level = lvl
+            if self.stream_at:
+                self._tick -= 2 * len(bits)
+                if self._tick <= 0:
+                    self._tick = self._tick_every
+                    self._maybe_stream()
+            return handles
+
+    def _merge_stats(self, delta):
+        """Add a GateStats' counts and level histogram to the global stats and every open scope."""
+        with self._lock:
+            for st in (self.global_stats, *self._scopes):
+                for k, v in delta.counts.items():
+                    st.counts[k] += v
+                hist = st.level_histogram
+                for lvl, c in delta.level_histogram.items():
+                    hist[lvl] = hist.get(lvl, 0) + c
 
     # -- scoped stats (backend.py:241-257) --------------------------------------
 

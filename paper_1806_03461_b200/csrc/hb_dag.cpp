@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <array>
 #include <cstdint>
+#include <deque>
 #include <vector>
 
 namespace {
@@ -117,6 +118,39 @@ class Dag {
         const int64_t r = mk_mux(rs, ra, rb);
         hcnt_[r >> 1]++;
         return r;
+    }
+
+    // Carry-save popcount of the literals refs[0..n): output refs, LSB first, whose
+    // values are the binary digits of the number of true literals; one live handle is
+    // counted on each.  Column by column, three bits of a weight go through a full adder
+    // (XOR3 + MAJ: two bootstraps), a last pair through a half adder; sums rejoin the
+    // back of their column and carries the back of the next one (breadth-first, so the
+    // depth stays ~log_1.5 n).  About 2n bootstraps instead of the ~3n of a tree of
+    // ripple-carry adders (reference circuits.py:189-216); the digits of a sum are
+    // unique, so any consumer sees the same plaintexts.
+    std::vector<int64_t> csa(const int64_t *refs, int64_t n) {
+        for (int64_t i = 0; i < n; i++) check_ref(refs[i]);
+        std::vector<int64_t> out;
+        std::deque<int64_t> col(refs, refs + n), next;
+        while (!col.empty()) {
+            while (col.size() >= 3) {
+                const int64_t a = col[0], b = col[1], c = col[2];
+                col.erase(col.begin(), col.begin() + 3);
+                col.push_back(sum3(a, b, c));
+                next.push_back(mk_maj(a, b, c));
+            }
+            if (col.size() == 2) {
+                const int64_t a = col[0], b = col[1];
+                col.clear();
+                col.push_back(mk_xor(a, b));
+                next.push_back(mk_and(a, b));
+            }
+            out.push_back(col.front());
+            col.swap(next);
+            next.clear();
+        }
+        for (int64_t r : out) hcnt_[r >> 1]++;
+        return out;
     }
 
     void hinc(int64_t n) { hcnt_[check(n)]++; }
@@ -321,6 +355,13 @@ class Dag {
                     1 + std::max({lvl_[s[0]], lvl_[s[1]], lvl_[s[2]]})) << 1;
     }
 
+    // literal a ^ b ^ c: one XOR3 node when the three nodes are distinct non-constants
+    int64_t sum3(int64_t a, int64_t b, int64_t c) {
+        const int64_t na = a >> 1, nb = b >> 1, nc = c >> 1;
+        if (na == 0 || nb == 0 || nc == 0 || na == nb || na == nc || nb == nc) return mk_xor(mk_xor(a, b), c);
+        return mk_xor3(na, nb, nc) | ((a ^ b ^ c) & 1);
+    }
+
     int64_t mk_mux(int64_t rs, int64_t ra, int64_t rb) {
         if (rs & 1) {  // MUX(~s, a, b) = MUX(s, b, a)
             rs ^= 1;
@@ -500,6 +541,23 @@ PyObject *Dag_requeue(PyDag *self, PyObject *arg) {
     Py_RETURN_NONE;
 }
 
+PyObject *Dag_csa(PyDag *self, PyObject *arg) {
+    PyArrayObject *ids = as_ids(arg);
+    if (!ids) return nullptr;
+    PyObject *res = nullptr;
+    try {
+        res = to_array(self->dag->csa((const int64_t *)PyArray_DATA(ids), (int64_t)PyArray_SIZE(ids)));
+    } catch (const IndexErr &) {
+        Py_DECREF(ids);
+        return index_error();
+    } catch (const std::bad_alloc &) {
+        Py_DECREF(ids);
+        return PyErr_NoMemory();
+    }
+    Py_DECREF(ids);
+    return res;
+}
+
 PyObject *Dag_gather(PyDag *self, PyObject *arg) {
     PyArrayObject *ids = as_ids(arg);
     if (!ids) return nullptr;
@@ -548,6 +606,8 @@ PyMethodDef Dag_methods[] = {
     {"pending", (PyCFunction)Dag_pending, METH_NOARGS, "int64 ids of pending nodes"},
     {"mark_done", (PyCFunction)Dag_mark_done, METH_O, "mark node ids executed"},
     {"requeue", (PyCFunction)Dag_requeue, METH_O, "pending node ids taken by live(True) but not run"},
+    {"csa", (PyCFunction)Dag_csa, METH_O,
+     "csa(refs) -> refs of the binary digits (LSB first) of the number of true literals; counts a handle on each"},
     {"gather", (PyCFunction)Dag_gather, METH_O, "gather(ids) -> (op int8, a, b, c, lvl int64 arrays)"},
     {nullptr, nullptr, 0, nullptr}};
 

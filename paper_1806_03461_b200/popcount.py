@@ -1,0 +1,109 @@
+"""Carry-save popcount for `TfheContext` (opt-in, fewer executed bootstraps).
+
+The reference sums encrypted bits with a tree of ripple-carry adders
+(`hebnn.circuits.reduce_tree_sum`, circuits.py:189-216): ~3n bootstraps for n
+bits once full adders run as XOR3 + MAJ.  A carry-save (Wallace-style)
+compressor network needs ~2n.  The binary digits of a sum are unique, so every
+consumer of the popcount word sees the same plaintexts; only the executed
+circuit differs.
+
+`install()` rebinds `reduce_tree_sum` in `hebnn.circuits` and in every loaded
+module that imported it by name (`hebnn.compiler` does).  The replacement
+
+* hands every call whose bits do not belong to a `TfheContext(csa_popcount=True)`
+  (SimContext, the pure drop-in `TfheContext`, trivial constants among the bits)
+  to the reference function unchanged;
+* otherwise builds the compressor network natively in the context's gate DAG
+  (`Dag.csa`, csrc/hb_dag.cpp) and charges the context's `GateStats` and open
+  scopes exactly what the reference function would have recorded — it runs the
+  reference function once per (n, input levels) on a `SimContext` and merges that
+  context's counts and level histogram — so counted gates, levels and the output
+  word's handle levels / width / max_value stay those of the reference.
+
+Nothing here runs unless a context asks for it: the default `TfheContext` is
+the pure `GateBackend` drop-in with the reference's circuits untouched.
+"""
+
+from __future__ import annotations
+
+import sys
+import threading
+
+import numpy as np
+
+import hebnn.circuits as _circuits
+from hebnn.backend import CipherBit, SimContext
+
+_ORIG = _circuits.reduce_tree_sum
+_LOCK = threading.Lock()
+_MEMO = {}          # (n, levels key) -> (GateStats delta, output levels, max_value, signed)
+_installed = False
+
+
+def _shadow(n, levels):
+    """What the reference's reduce_tree_sum records and returns for n encrypted
+    bits at these levels (a level, or a tuple of per-bit levels)."""
+    key = (n, levels)
+    hit = _MEMO.get(key)
+    if hit is None:
+        sim = SimContext()
+        per_bit = levels if isinstance(levels, tuple) else (levels,) * n
+        word = _ORIG([CipherBit(sim, 0, lvl) for lvl in per_bit])
+        if any(b.trivial_value is not None for b in word.bits):
+            hit = False  # a constant output bit: leave such calls to the reference function
+        else:
+            hit = (sim.global_stats, tuple(b.level for b in word.bits), word.max_value, word.signed)
+        with _LOCK:
+            _MEMO[key] = hit
+    return hit
+
+
+def csa_reduce_tree_sum(bits):
+    """Drop-in for hebnn.circuits.reduce_tree_sum (same word, same counted stats)."""
+    bits = list(bits)
+    ctx = bits[0].context if bits else None
+    if (len(bits) < 3 or not getattr(ctx, "csa_popcount", False)
+            or any(b.context is not ctx or b.trivial_value is not None for b in bits)):
+        return _ORIG(bits)
+    lv0 = bits[0].level
+    levels = lv0 if all(b.level == lv0 for b in bits) else tuple(b.level for b in bits)
+    shadow = _shadow(len(bits), levels)
+    if not shadow:
+        return _ORIG(bits)
+    delta, out_levels, max_value, signed = shadow
+    outs = ctx._csa_popcount(bits, out_levels)
+    if outs is None:  # degenerate operands (duplicates): the reference circuit
+        return _ORIG(bits)
+    ctx._merge_stats(delta)
+    return _circuits.CipherWord(outs, signed=signed, max_value=max_value)
+
+
+def _is_hebnn(mod):
+    name = getattr(mod, "__name__", "")
+    return name == "hebnn" or name.startswith("hebnn.")
+
+
+def install():
+    """Rebind reduce_tree_sum wherever the reference bound it (idempotent)."""
+    global _installed
+    with _LOCK:
+        for mod in list(sys.modules.values()):
+            if _is_hebnn(mod) and getattr(mod, "reduce_tree_sum", None) is _ORIG:
+                setattr(mod, "reduce_tree_sum", csa_reduce_tree_sum)
+        _installed = True
+
+
+def uninstall():
+    global _installed
+    with _LOCK:
+        for mod in list(sys.modules.values()):
+            if _is_hebnn(mod) and getattr(mod, "reduce_tree_sum", None) is csa_reduce_tree_sum:
+                setattr(mod, "reduce_tree_sum", _ORIG)
+        _installed = False
+
+
+def installed():
+    return _installed
+
+
+__all__ = ["install", "uninstall", "installed", "csa_reduce_tree_sum"]

@@ -3,7 +3,8 @@ modules (baseline/_ref/hebnn_ref_tests/, copied unmodified from
 /root/reference/pkg/tests by scripts/install_reference.py) against the drop-in:
 every collected module's `SimContext` name, and hebnn.cli's, is rebound to the
 context class HB_REF_CTX selects ("gpu": TfheContext on the B200, "plain": the
-plaintext stand-in engine for host logic) — the rebinding recipe of
+plaintext stand-in engine for host logic; "-csa" appended: with the opt-in
+carry-save popcount) — the rebinding recipe of
 INTEGRATION.md §3.  Load with `-p ref_rebind` (tests/ on sys.path)."""
 
 import os
@@ -18,13 +19,21 @@ for _p in (_ROOT, os.path.join(_ROOT, "baseline", "_ref"), _HERE):
 
 def context_class():
     kind = os.environ.get("HB_REF_CTX", "gpu")
-    if kind == "plain":
+    if kind.startswith("plain"):
         from plain_engine import plain_context_class
 
-        return plain_context_class()
-    from paper_1806_03461_b200.backend import TfheContext
+        base = plain_context_class()
+    else:
+        from paper_1806_03461_b200.backend import TfheContext as base
+    if not kind.endswith("-csa"):
+        return base
 
-    return TfheContext
+    class CsaContext(base):  # "plain-csa" / "gpu-csa": the opt-in carry-save popcount (popcount.py)
+        def __init__(self, *a, **k):
+            k.setdefault("csa_popcount", True)
+            super().__init__(*a, **k)
+
+    return CsaContext
 
 
 def pytest_configure(config):

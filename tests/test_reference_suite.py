@@ -35,6 +35,14 @@ def test_reference_suite_on_plain_engine():
     assert " passed" in out and "failed" not in out
 
 
+def test_reference_suite_on_plain_engine_with_csa_popcount():
+    """The same unmodified modules with the opt-in carry-save popcount: the
+    reference's own gate-count, level and value assertions on reduce_tree_sum
+    and the compiler hold (popcount.py charges the reference's counts)."""
+    out = _run(["test_backend.py", "test_circuits.py", "test_compiler.py"], "plain-csa", 900)
+    assert " passed" in out and "failed" not in out
+
+
 @pytest.mark.gpu
 def test_reference_suite_on_gpu():
     """Unmodified reference tests on real ciphertexts, all of them, including the

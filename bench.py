@@ -73,6 +73,7 @@ def parse_args():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compare", action="store_true", help="skip the CGGI-key-layout comparison leg")
+    ap.add_argument("--no-csa", action="store_true", help="skip the carry-save-popcount BNN legs (bnn_csa)")
     ap.add_argument("--plan", action="store_true",
                     help="print the rank layout (n_gpus, backend, devices) as one JSON line and exit (launcher test)")
     ap.add_argument("--bnn", default="all",
@@ -367,6 +368,34 @@ def bnn_latency(cfg, seed, trials=2, cached=True):
     rep["reference_cpu"] = ref
     rep["counted_gates_match_simcontext"] = ref["counted_gates_per_input"] == rep["counted_gates_per_input"]
     return rep
+
+
+def bnn_csa_latency(cfg, seed, base):
+    """The same config with the opt-in carry-save popcount (TfheContext(csa_popcount=True),
+    paper_1806_03461_b200/popcount.py): the reference compiler's popcounts run as
+    Wallace-style compressor networks (~2n instead of ~3n bootstraps for n bits); decrypted
+    outputs and counted GateStats are the reference's.  `base` = the pure drop-in's report."""
+    from paper_1806_03461_b200 import popcount, workloads
+    from paper_1806_03461_b200.backend import TfheContext
+
+    class CsaContext(TfheContext):
+        def __init__(self, **kw):
+            super().__init__(csa_popcount=True, **kw)
+
+    try:
+        rep = workloads.run_encrypted(CsaContext, cfg, seed=seed, replays=0 if cfg in ("cfg3", "cfg5") else 1)
+    finally:
+        popcount.uninstall()
+    keep = ("config", "batch", "counted_gates", "counted_gates_per_input", "executed_bootstraps", "levels", "depth",
+            "first_eval_s", "dag_build_s", "final_flush_s", "matches_oracle_eval", "replay")
+    out = {k: rep[k] for k in keep}
+    if isinstance(base, dict) and "executed_bootstraps" in base:
+        out["counted_gates_match_simcontext"] = (base.get("counted_gates_match_simcontext") is True
+                                                  and base["counted_gates_per_input"] == rep["counted_gates_per_input"]
+                                                  and base["depth"] == rep["depth"])
+        out["executed_bootstraps_vs_drop_in"] = rep["executed_bootstraps"] / base["executed_bootstraps"]
+        out["first_eval_speedup_vs_drop_in"] = base["first_eval_s"] / rep["first_eval_s"]
+    return out
 
 
 def strong_scaling_leg(args, dist, eng, recs, weak_value, weak_ms):
@@ -673,6 +702,11 @@ def run_ours(args, dist):
             rep = {"error": repr(exc)}
         if dist.rank == 0:
             line["bnn"][cfg] = rep
+        if dist.rank == 0 and dist.world == 1 and not args.no_csa:
+            try:
+                line.setdefault("bnn_csa", {})[cfg] = bnn_csa_latency(cfg, args.seed, rep)
+            except Exception as exc:  # report, never hide
+                line.setdefault("bnn_csa", {})[cfg] = {"error": repr(exc)}
     if args.bnn_list and dist.rank == 0 and dist.world == 1:
         try:  # the shipped Cancer model on the reference dataset's 569 rows, as lanes (f4)
             from paper_1806_03461_b200 import workloads
@@ -688,7 +722,7 @@ def run_ours(args, dist):
             isinstance(r, dict) and r.get("matches_oracle_eval") is True
             and (r.get("replay") or {}).get("matches_oracle_eval", True) is True
             and (r.get("cached") or {}).get("matches_oracle_eval", True) is True
-            for r in line["bnn"].values())
+            for r in list(line["bnn"].values()) + list(line.get("bnn_csa", {}).values()))
     if dist.world > 1:
         dist.barrier()
         lines = dist.nccl_lines()

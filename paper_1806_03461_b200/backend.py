@@ -32,6 +32,7 @@ ciphertexts that share one DAG.
 
 from __future__ import annotations
 
+import os
 import threading
 import time
 import weakref

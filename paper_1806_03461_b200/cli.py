@@ -65,6 +65,9 @@ def main(argv=None):
     pre.add_argument("--backend", choices=("tfhe-b200", "sim"), default="tfhe-b200")
     pre.add_argument("--key-seed", type=int, default=0)
     pre.add_argument("--device", type=int, default=0)
+    pre.add_argument("--csa-popcount", action="store_true",
+                     help="popcounts as carry-save compressor networks (popcount.py): ~40%% fewer bootstraps, "
+                          "same outputs and counted gates")
     known, rest = pre.parse_known_args(argv)
 
     if rest[:1] == ["calibrate"]:
@@ -90,8 +93,8 @@ def main(argv=None):
     if known.backend == "tfhe-b200":
         from .backend import TfheContext
 
-        seed, device = known.key_seed, known.device
-        ref_cli.SimContext = lambda: TfheContext(seed=seed, device=device)
+        seed, device, csa = known.key_seed, known.device, (True if known.csa_popcount else None)
+        ref_cli.SimContext = lambda: TfheContext(seed=seed, device=device, csa_popcount=csa)
     t0 = time.perf_counter()
     rc = ref_cli.main(rest)
     print(f"[hebnn-b200] backend={known.backend} wall={time.perf_counter() - t0:.3f}s", file=sys.stderr)

@@ -229,6 +229,8 @@ class TfheContext(GateBackend):
         if csa_popcount is None:
             csa_popcount = os.environ.get("HEBNN_B200_CSA_POPCOUNT", "0") not in ("", "0")
         self.csa_popcount = bool(csa_popcount)
+        # shared first stage of the carry-save popcounts: leaf ordinals per block (0: none)
+        self.csa_block = int(os.environ.get("HEBNN_B200_CSA_BLOCK", "7"))
         if self.csa_popcount:
             from . import popcount
 
@@ -514,7 +516,7 @@ class TfheContext(GateBackend):
         digits (duplicate operands), in which case nothing live was created."""
         refs = np.fromiter((b._value for b in bits), dtype=np.int64, count=len(bits))
         with self._lock:
-            out = [int(r) for r in self._dag.csa(refs)]
+            out = [int(r) for r in self._dag.csa(refs, self.csa_block)]
             handles = [_Bit(self, r, 0) for r in out]  # own the counted handles (dropped on return None)
             if len(out) != len(out_levels) or any((r >> 1) == 0 for r in out):
                 return None

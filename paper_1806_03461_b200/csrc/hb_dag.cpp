@@ -128,26 +128,60 @@ class Dag {
     // depth stays ~log_1.5 n).  About 2n bootstraps instead of the ~3n of a tree of
     // ripple-carry adders (reference circuits.py:189-216); the digits of a sum are
     // unique, so any consumer sees the same plaintexts.
-    std::vector<int64_t> csa(const int64_t *refs, int64_t n) {
+    //
+    // block >= 3: shared first stage.  Every leaf node gets an ordinal the first time a
+    // popcount sees it; the literals are sorted by ordinal and cut into blocks of `block`
+    // consecutive ordinals, and inside a block full adders (only: they are what removes
+    // bits) take the first three bits of a weight until fewer than three are left.  The
+    // blocks are the same for every popcount over the same leaves (the neurons of a
+    // layer sum subsets of one input vector), so hash-consing computes a block's adders
+    // once for all of them; MAJ is stored with its first operand positive (it is
+    // self-dual), so the popcounts of negated literals share them too.
+    std::vector<int64_t> csa(const int64_t *refs, int64_t n, int64_t block) {
         for (int64_t i = 0; i < n; i++) check_ref(refs[i]);
+        std::vector<std::deque<int64_t>> cols(1);
+        auto fa_front = [this](std::vector<std::deque<int64_t>> &c, size_t w) {
+            const int64_t x = c[w][0], y = c[w][1], z = c[w][2];
+            c[w].erase(c[w].begin(), c[w].begin() + 3);
+            c[w].push_back(sum3(x, y, z));
+            if (c.size() <= w + 1) c.emplace_back();
+            c[w + 1].push_back(mk_maj(x, y, z));
+        };
+        if (block >= 3) {
+            if (ord_.size() < op_.size()) ord_.resize(op_.size(), 0);
+            std::vector<std::pair<int64_t, int64_t>> lit;  // (ordinal, literal)
+            lit.reserve((size_t)n);
+            for (int64_t i = 0; i < n; i++) {
+                int64_t &o = ord_[refs[i] >> 1];
+                if (o == 0) o = ++next_ord_;
+                lit.emplace_back(o - 1, refs[i]);
+            }
+            std::sort(lit.begin(), lit.end());
+            std::vector<std::deque<int64_t>> loc;
+            for (size_t i = 0; i < lit.size();) {
+                const int64_t blk = lit[i].first / block;
+                loc.assign(1, {});
+                for (; i < lit.size() && lit[i].first / block == blk; i++) loc[0].push_back(lit[i].second);
+                for (size_t w = 0; w < loc.size(); w++)
+                    while (loc[w].size() >= 3) fa_front(loc, w);
+                if (cols.size() < loc.size()) cols.resize(loc.size());
+                for (size_t w = 0; w < loc.size(); w++) cols[w].insert(cols[w].end(), loc[w].begin(), loc[w].end());
+            }
+        } else {
+            cols[0].assign(refs, refs + n);
+        }
         std::vector<int64_t> out;
-        std::deque<int64_t> col(refs, refs + n), next;
-        while (!col.empty()) {
-            while (col.size() >= 3) {
-                const int64_t a = col[0], b = col[1], c = col[2];
-                col.erase(col.begin(), col.begin() + 3);
-                col.push_back(sum3(a, b, c));
-                next.push_back(mk_maj(a, b, c));
+        for (size_t w = 0; w < cols.size(); w++) {
+            while (cols[w].size() >= 3) fa_front(cols, w);
+            if (cols[w].size() == 2) {
+                const int64_t x = cols[w][0], y = cols[w][1];
+                cols[w].clear();
+                cols[w].push_back(mk_xor(x, y));
+                if (cols.size() <= w + 1) cols.emplace_back();
+                cols[w + 1].push_back(mk_and(x, y));
             }
-            if (col.size() == 2) {
-                const int64_t a = col[0], b = col[1];
-                col.clear();
-                col.push_back(mk_xor(a, b));
-                next.push_back(mk_and(a, b));
-            }
-            out.push_back(col.front());
-            col.swap(next);
-            next.clear();
+            if (cols[w].empty()) break;  // a vanished digit (degenerate operands): the caller falls back
+            out.push_back(cols[w].front());
         }
         for (int64_t r : out) hcnt_[r >> 1]++;
         return out;
@@ -242,6 +276,8 @@ class Dag {
     std::vector<uint32_t> mark_;
     uint32_t epoch_ = 0;
     CseTable cse_;
+    std::vector<int64_t> ord_;  // csa: leaf ordinal + 1 of a node (0: none yet)
+    int64_t next_ord_ = 0;
 
     int64_t check(int64_t n) const {
         if (n < 0 || n >= (int64_t)op_.size()) throw IndexErr{};
@@ -345,7 +381,10 @@ class Dag {
         }
         std::array<int64_t, 3> s{x, y, z};
         std::sort(s.begin(), s.end());
-        return node(MAJ, s[0], s[1], s[2], 1 + std::max({lv(s[0]), lv(s[1]), lv(s[2])})) << 1;
+        // self-dual: MAJ(~a, ~b, ~c) = ~MAJ(a, b, c); stored with the first operand positive
+        const int64_t neg = s[0] & 1;
+        if (neg) s = {s[0] ^ 1, s[1] ^ 1, s[2] ^ 1};
+        return (node(MAJ, s[0], s[1], s[2], 1 + std::max({lv(s[0]), lv(s[1]), lv(s[2])})) << 1) | neg;
     }
 
     int64_t mk_xor3(int64_t p, int64_t q, int64_t r) {
@@ -541,12 +580,15 @@ PyObject *Dag_requeue(PyDag *self, PyObject *arg) {
     Py_RETURN_NONE;
 }
 
-PyObject *Dag_csa(PyDag *self, PyObject *arg) {
+PyObject *Dag_csa(PyDag *self, PyObject *args) {
+    PyObject *arg = nullptr;
+    long long block = 0;
+    if (!PyArg_ParseTuple(args, "O|L", &arg, &block)) return nullptr;
     PyArrayObject *ids = as_ids(arg);
     if (!ids) return nullptr;
     PyObject *res = nullptr;
     try {
-        res = to_array(self->dag->csa((const int64_t *)PyArray_DATA(ids), (int64_t)PyArray_SIZE(ids)));
+        res = to_array(self->dag->csa((const int64_t *)PyArray_DATA(ids), (int64_t)PyArray_SIZE(ids), (int64_t)block));
     } catch (const IndexErr &) {
         Py_DECREF(ids);
         return index_error();
@@ -606,8 +648,9 @@ PyMethodDef Dag_methods[] = {
     {"pending", (PyCFunction)Dag_pending, METH_NOARGS, "int64 ids of pending nodes"},
     {"mark_done", (PyCFunction)Dag_mark_done, METH_O, "mark node ids executed"},
     {"requeue", (PyCFunction)Dag_requeue, METH_O, "pending node ids taken by live(True) but not run"},
-    {"csa", (PyCFunction)Dag_csa, METH_O,
-     "csa(refs) -> refs of the binary digits (LSB first) of the number of true literals; counts a handle on each"},
+    {"csa", (PyCFunction)Dag_csa, METH_VARARGS,
+     "csa(refs, block=0) -> refs of the binary digits (LSB first) of the number of true literals; counts a handle "
+     "on each; block >= 3: shared first stage over blocks of leaf ordinals"},
     {"gather", (PyCFunction)Dag_gather, METH_O, "gather(ids) -> (op int8, a, b, c, lvl int64 arrays)"},
     {nullptr, nullptr, 0, nullptr}};
 

@@ -54,6 +54,8 @@ def _shadow(n, levels):
         else:
             hit = (sim.global_stats, tuple(b.level for b in word.bits), word.max_value, word.signed)
         with _LOCK:
+            if len(_MEMO) >= 8192:  # per-bit level tuples of many distinct shapes: start over
+                _MEMO.clear()
             _MEMO[key] = hit
     return hit
 

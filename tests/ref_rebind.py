@@ -44,8 +44,15 @@ def pytest_configure(config):
 
 def pytest_collection_modifyitems(session, config, items):
     cls = context_class()
+    csa = os.environ.get("HB_REF_CTX", "gpu").endswith("-csa")
+    if csa:
+        from paper_1806_03461_b200 import popcount
     for item in items:
         mod = getattr(item, "module", None)
+        # the test modules imported reduce_tree_sum by name: their direct calls go through the
+        # carry-save replacement too (popcount.install() only rebinds the hebnn.* modules)
+        if csa and mod is not None and getattr(mod, "reduce_tree_sum", None) is popcount._ORIG:
+            mod.reduce_tree_sum = popcount.csa_reduce_tree_sum
         if mod is not None and hasattr(mod, "SimContext") and not getattr(mod, "_hb_rebound", False):
             mod.SimContext = cls
             mod._hb_rebound = True

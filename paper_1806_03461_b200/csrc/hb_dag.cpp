@@ -23,6 +23,7 @@
 #include <array>
 #include <cstdint>
 #include <deque>
+#include <tuple>
 #include <vector>
 
 namespace {
@@ -170,18 +171,40 @@ class Dag {
         } else {
             cols[0].assign(refs, refs + n);
         }
+        // global compression: in every column the three shallowest bits (DAG level) go
+        // through the next full adder, so late carries are not waited for by early bits
+        // (depth ~ the Wallace stages plus one carry chain over the word)
+        using Item = std::tuple<int32_t, int64_t, int64_t>;  // (level, arrival, literal)
+        auto later = [](const Item &p, const Item &q) { return p > q; };
+        std::vector<std::vector<Item>> heap(cols.size());
+        int64_t seq = 0;
+        auto push = [&](size_t w, int64_t r) {
+            if (heap.size() <= w) heap.resize(w + 1);
+            heap[w].emplace_back(lv(r), seq++, r);
+            std::push_heap(heap[w].begin(), heap[w].end(), later);
+        };
+        auto pop = [&](size_t w) {
+            std::pop_heap(heap[w].begin(), heap[w].end(), later);
+            const int64_t r = std::get<2>(heap[w].back());
+            heap[w].pop_back();
+            return r;
+        };
+        for (size_t w = 0; w < cols.size(); w++)
+            for (int64_t r : cols[w]) push(w, r);
         std::vector<int64_t> out;
-        for (size_t w = 0; w < cols.size(); w++) {
-            while (cols[w].size() >= 3) fa_front(cols, w);
-            if (cols[w].size() == 2) {
-                const int64_t x = cols[w][0], y = cols[w][1];
-                cols[w].clear();
-                cols[w].push_back(mk_xor(x, y));
-                if (cols.size() <= w + 1) cols.emplace_back();
-                cols[w + 1].push_back(mk_and(x, y));
+        for (size_t w = 0; w < heap.size(); w++) {
+            while (heap[w].size() >= 3) {
+                const int64_t x = pop(w), y = pop(w), z = pop(w);
+                push(w, sum3(x, y, z));
+                push(w + 1, mk_maj(x, y, z));
             }
-            if (cols[w].empty()) break;  // a vanished digit (degenerate operands): the caller falls back
-            out.push_back(cols[w].front());
+            if (heap[w].size() == 2) {
+                const int64_t x = pop(w), y = pop(w);
+                push(w, mk_xor(x, y));
+                push(w + 1, mk_and(x, y));
+            }
+            if (heap[w].empty()) break;  // a vanished digit (degenerate operands): the caller falls back
+            out.push_back(pop(w));
         }
         for (int64_t r : out) hcnt_[r >> 1]++;
         return out;

@@ -17,6 +17,12 @@ reduced with MAX over ranks.
 input ciphertext batches from pinned memory, the gate records, the level, and
 D2H of the 4,096 output ciphertexts, all inside the timed region.
 
+`bnn` (N = 1): every BASELINE BNN config through the reference compiler on the
+pure drop-in `TfheContext` (first evaluation, replay, compiled schedule, all
+checked against `oracle_eval`); `bnn_csa`: the same configs with the opt-in
+carry-save popcount (`TfheContext(csa_popcount=True)`, same outputs and
+counted gates, ~42% fewer executed bootstraps).
+
 `--impl reference` times the CPU path on a bounded sample of the same
 workload with all host threads: the vectorised FP64-FFT CPU port of the same
 gate bootstrap (oracle/tfhe_cpu_fft.c, eight gates per SIMD register, checked

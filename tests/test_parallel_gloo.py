@@ -21,7 +21,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, csa=False):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -50,7 +50,7 @@ def _worker(rank, world, port, q):
             xs = [rng.choice((-1, 1)) for _ in range(d)]
             enc = Ctx(seed=42)
             cts = enc.keys.encrypt(np.array([1 if v == 1 else 0 for v in xs], np.uint8), seed=3, stream=9)
-            ev = OutPEvaluator(lambda: Ctx(seed=42), TorchComm())
+            ev = OutPEvaluator(lambda: Ctx(seed=42, csa_popcount=csa), TorchComm())
             out = ev.run(model, cts[:, None, :])
             if mode == "sign_bits":
                 bits = enc.keys.decrypt(np.stack(out)[:, 0, :])
@@ -63,12 +63,13 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_outp_two_ranks_gloo(world):
+@pytest.mark.parametrize("world,csa", [(2, False), (2, True)])
+def test_outp_two_ranks_gloo(world, csa):
+    """csa: every rank's contexts use the opt-in carry-save popcount (popcount.py)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, csa)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)

@@ -723,6 +723,12 @@ def run_ours(args, dist):
             line["cancer"] = rep
         except Exception as exc:  # report, never hide
             line["cancer"] = {"error": repr(exc)}
+    if args.bnn_list and dist.rank == 0 and dist.world == 1:
+        # first-evaluation latency per config at a glance (details in bnn / bnn_csa)
+        line["bnn_first_eval_s"] = {
+            cfg: {"drop_in": (line["bnn"].get(cfg) or {}).get("first_eval_s"),
+                  "csa_popcount": (line.get("bnn_csa", {}).get(cfg) or {}).get("first_eval_s")}
+            for cfg in args.bnn_list}
     if args.bnn_list and dist.rank == 0:
         line["bnn_all_match_oracle_eval"] = all(
             isinstance(r, dict) and r.get("matches_oracle_eval") is True

@@ -117,3 +117,32 @@ def test_models_match_oracle_eval_and_simcontext_stats():
             assert decrypt_output(c, outs) == oracle_eval(m, xs)
             assert c.global_stats.as_dict() == sim.global_stats.as_dict()
             assert c.exec_stats["bootstraps"] <= base.exec_stats["bootstraps"]
+
+
+@pytest.mark.parametrize("block", [0, 3, 5, 7, 12])
+def test_shared_first_stage_block_sizes(block, monkeypatch):
+    """Any block size of the shared first stage (HEBNN_B200_CSA_BLOCK; 0: none) gives the
+    same words; popcounts over subsets of one input vector reuse each other's adders."""
+    monkeypatch.setenv("HEBNN_B200_CSA_BLOCK", str(block))
+    rng = random.Random(block)
+    vals = [rng.randint(0, 1) for _ in range(120)]
+    ctx = Plain(seed=42, csa_popcount=True)
+    assert ctx.csa_block == block
+    xs = [ctx.encrypt(v) for v in vals]
+    subsets = [[i for i in range(120) if rng.random() < 0.5] for _ in range(12)]
+    words = [ref_circuits.reduce_tree_sum([xs[i] if k % 2 else ctx.g_not(xs[i]) for i in sub])
+             for k, sub in enumerate(subsets)]
+    for k, (sub, w) in enumerate(zip(subsets, words)):
+        assert decrypt_word(w) == sum(vals[i] if k % 2 else 1 - vals[i] for i in sub)
+    total_bits = sum(len(sub) for sub in subsets)
+    assert ctx.exec_stats["bootstraps"] < 2 * total_bits
+    if block >= 3:  # shared adders: clearly fewer than twelve independent networks
+        assert ctx.exec_stats["bootstraps"] < 1.9 * total_bits
+
+
+def test_environment_default(monkeypatch):
+    monkeypatch.setenv("HEBNN_B200_CSA_POPCOUNT", "1")
+    assert Plain(seed=42).csa_popcount is True
+    assert Plain(seed=42, csa_popcount=False).csa_popcount is False
+    monkeypatch.setenv("HEBNN_B200_CSA_POPCOUNT", "0")
+    assert Plain(seed=42).csa_popcount is False

@@ -236,8 +236,12 @@ np.save(sys.argv[1], eng.download(3 * n, n))
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     for unroll in (2, 1):
         outs = []
-        for lat, clu, bs, c6, sw in (("1", "1", "1", "1", "1"), ("1", "1", "0", "1", "1"), ("1", "1", "0", "0", "0"),
-                                     ("1", "0", "0", "0", "0"), ("0", "0", "0", "0", "0")):
+        # the cluster / bin-split / split-wave switches only select key-pair kernels: the CGGI
+        # layout has the latency kernel on or off
+        combos = ((("1", "1", "1", "1", "1"), ("1", "1", "0", "1", "1"), ("1", "1", "0", "0", "0"),
+                   ("1", "0", "0", "0", "0"), ("0", "0", "0", "0", "0")) if unroll == 2
+                  else (("1", "1", "1", "1", "1"), ("0", "0", "0", "0", "0")))
+        for lat, clu, bs, c6, sw in combos:
             path = f"/tmp/hb_narrow_{n}_{unroll}_{lat}{clu}{bs}{c6}{sw}.npy"
             env = dict(os.environ, HEBNN_B200_LATENCY_MODE=lat, HEBNN_B200_CLUSTER_MODE=clu, HEBNN_B200_BINSPLIT=bs,
                        HEBNN_B200_CLU6=c6, HEBNN_B200_SPLIT_WAVES=sw)

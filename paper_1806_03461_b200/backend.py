@@ -466,8 +466,14 @@ class TfheContext(GateBackend):
             if self.stream_at:
                 self._tick -= 1
                 if self._tick <= 0:
-                    self._tick = self._tick_every
-                    self._maybe_stream()
+                    if kind is XOR or kind is XNOR:
+                        # a half adder issues its AND right after its XOR (circuits.py:95-98):
+                        # check again after the next gate, so that a background flush never
+                        # starts between the two and the pair stays one HA record
+                        self._tick = 1
+                    else:
+                        self._tick = self._tick_every
+                        self._maybe_stream()
             return _Bit(self, r, level)
 
     def g_and(self, a, b):

@@ -65,7 +65,8 @@ def test_reference_suite_on_gpu():
     test_compiler and test_acceptance (eight pytest-xdist workers — eight processes,
     eight engines — share the B200: each test is a chain of one-level flushes that keeps
     only a few SMs busy) and, at the same time, the hebnn CLI `selftest`
-    (cli.py:212-229) with the B200 backend.  The four slowest exhaustive tests
+    (cli.py:212-229) with the B200 backend, and test_circuits / test_compiler again with
+    the opt-in carry-save popcount.  The four slowest exhaustive tests
     (SLOWEST: the exhaustive reduce tree n <= 12, test_circuits.py:124-130, the k = 8
     comparators, test_circuits.py:216-223, ...) run in
     test_reference_suite_exhaustive_on_gpu (HB_GPU_FULL=1; profiles/r02_v/pytest_gpu.log
@@ -74,16 +75,21 @@ def test_reference_suite_on_gpu():
     suite = _popen(["test_backend.py", "test_circuits.py", "test_compiler.py", "test_acceptance.py"], "gpu",
                    extra=("--durations=10", "-n", "8", *deselect))
     cli = _popen(["test_cli.py"], "gpu", extra=("-k", "test_selftest_passes"))
+    # the circuit and compiler modules once more with the opt-in carry-save popcount
+    # (their direct reduce_tree_sum calls rebound too, tests/ref_rebind.py)
+    csa = _popen(["test_circuits.py", "test_compiler.py"], "gpu-csa", extra=("-n", "4", *deselect))
     try:
         out_suite, _ = suite.communicate(timeout=900)
         out_cli, _ = cli.communicate(timeout=900)
+        out_csa, _ = csa.communicate(timeout=900)
     finally:
-        for p in (suite, cli):
+        for p in (suite, cli, csa):
             if p.poll() is None:
                 p.kill()
     print(out_suite[-3000:])
     assert suite.returncode == 0 and " passed" in out_suite and "failed" not in out_suite, out_suite[-4000:]
     assert cli.returncode == 0 and " passed" in out_cli, out_cli[-4000:]
+    assert csa.returncode == 0 and " passed" in out_csa and "failed" not in out_csa, out_csa[-4000:]
 
 
 @pytest.mark.gpu

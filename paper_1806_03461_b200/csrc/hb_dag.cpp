@@ -1,7 +1,8 @@
 // Host gate DAG of TfheContext, native: node store,
 // constant/duplicate elision, hash-consing, MUX lowering, full-adder fusion
-// into 3-input bootstraps (majority, XOR3), live-handle counts and the
-// live-gate filter of a flush.  The Python context (backend.py) keeps the
+// into 3-input bootstraps (majority, XOR3), live-handle counts, the
+// live-gate filter of a flush and the carry-save popcount networks of the
+// opt-in popcount replacement (csa; paper_1806_03461_b200/popcount.py).  The Python context (backend.py) keeps the
 // reference contract (handles, GateStats, scopes, errors) and the engine
 // calls; every gate of the reference API lands here once.
 //

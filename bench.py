@@ -723,6 +723,22 @@ def run_ours(args, dist):
             line["cancer"] = rep
         except Exception as exc:  # report, never hide
             line["cancer"] = {"error": repr(exc)}
+        if not args.no_csa:
+            try:  # the same rows with the opt-in carry-save popcount
+                from paper_1806_03461_b200 import popcount
+
+                class CsaContext(TfheContext):
+                    def __init__(self, **kw):
+                        super().__init__(csa_popcount=True, **kw)
+
+                try:
+                    rep = workloads.run_cancer(CsaContext, seed=args.seed)
+                finally:
+                    popcount.uninstall()
+                rep.pop("predictions")
+                line["cancer_csa"] = rep
+            except Exception as exc:  # report, never hide
+                line["cancer_csa"] = {"error": repr(exc)}
     if args.bnn_list and dist.rank == 0 and dist.world == 1:
         # first-evaluation latency per config at a glance (details in bnn / bnn_csa)
         line["bnn_first_eval_s"] = {

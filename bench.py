@@ -713,6 +713,21 @@ def run_ours(args, dist):
                 line.setdefault("bnn_csa", {})[cfg] = bnn_csa_latency(cfg, args.seed, rep)
             except Exception as exc:  # report, never hide
                 line.setdefault("bnn_csa", {})[cfg] = {"error": repr(exc)}
+        if dist.world > 1 and not args.no_csa:
+            # the same Out-P / batch-sharded evaluation with the carry-save popcount on every rank
+            # (TfheContext reads the default of csa_popcount from the environment)
+            os.environ["HEBNN_B200_CSA_POPCOUNT"] = "1"
+            try:
+                rep_csa = bnn_outp(cfg, args.seed, dist, dev)
+            except Exception as exc:  # report, never hide
+                rep_csa = {"error": repr(exc)}
+            finally:
+                os.environ.pop("HEBNN_B200_CSA_POPCOUNT", None)
+                from paper_1806_03461_b200 import popcount
+
+                popcount.uninstall()
+            if dist.rank == 0:
+                line.setdefault("bnn_csa", {})[cfg] = rep_csa
     if args.bnn_list and dist.rank == 0 and dist.world == 1:
         try:  # the shipped Cancer model on the reference dataset's 569 rows, as lanes (f4)
             from paper_1806_03461_b200 import workloads

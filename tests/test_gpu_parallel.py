@@ -94,3 +94,7 @@ def test_bench_two_ranks_sharing_the_gpu():
     assert d["strong_scaling"]["gates_per_gpu"] == 256 and d["strong_scaling"]["n_gpus"] == 2
     assert d["bnn"]["cfg2n"]["matches_oracle_eval"] is True, d["bnn"]["cfg2n"]
     assert d["bnn"]["cfg5"]["matches_oracle_eval"] is True, d["bnn"]["cfg5"]
+    # the same two legs with the carry-save popcount on both ranks
+    assert d["bnn_csa"]["cfg2n"]["matches_oracle_eval"] is True, d["bnn_csa"]["cfg2n"]
+    assert d["bnn_csa"]["cfg5"]["matches_oracle_eval"] is True, d["bnn_csa"]["cfg5"]
+    assert d["bnn_csa"]["cfg5"]["executed_bootstraps_this_rank"] < 0.7 * d["bnn"]["cfg5"]["executed_bootstraps_this_rank"]

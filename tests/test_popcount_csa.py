@@ -146,3 +146,27 @@ def test_environment_default(monkeypatch):
     assert Plain(seed=42, csa_popcount=False).csa_popcount is False
     monkeypatch.setenv("HEBNN_B200_CSA_POPCOUNT", "0")
     assert Plain(seed=42).csa_popcount is False
+
+
+def test_duplicate_and_complementary_literals_property():
+    """Random multisets of literals with repeated and complementary bits (the degenerate
+    operands of Dag.csa: XOR / MAJ / AND folding to constants or single literals): the word
+    is the number of true literals whatever path (compressor network or the fallback to the
+    reference circuit when a digit folds to a constant) built it."""
+    rng = random.Random(77)
+    for trial in range(60):
+        ctx = Plain(seed=42, csa_popcount=True, stream_at=0)
+        k = rng.randint(1, 6)
+        vals = [rng.randint(0, 1) for _ in range(k)]
+        xs = [ctx.encrypt(v) for v in vals]
+        n = rng.randint(3, 40)
+        picks = [(rng.randrange(k), rng.randint(0, 1)) for _ in range(n)]
+        lits = [ctx.g_not(xs[i]) if neg else xs[i] for i, neg in picks]
+        sim = SimContext()
+        sx = [sim.encrypt(v) for v in vals]
+        want_word = ref_circuits.reduce_tree_sum([sim.g_not(sx[i]) if neg else sx[i] for i, neg in picks])
+        word = ref_circuits.reduce_tree_sum(lits)
+        want = sum(1 - vals[i] if neg else vals[i] for i, neg in picks)
+        assert decrypt_word(word) == decrypt_word(want_word) == want, (trial, picks)
+        assert word.width == want_word.width
+        assert ctx.global_stats.as_dict() == sim.global_stats.as_dict()
